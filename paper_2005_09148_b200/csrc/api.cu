@@ -1,0 +1,674 @@
+// C-ABI of liboocgb (include/oocgb.h): argument checking, handle lifetime, host<->device
+// marshalling, NCCL plumbing and the page streamer.  The arithmetic of the method lives in
+// quantise.cu, sample.cu and tree.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+#include "stream.cuh"
+
+namespace oocgb {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string &m) { g_last_error = m; }
+
+void *dmalloc(size_t bytes) {
+  void *p = nullptr;
+  cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(OOCGB_ERR_NOMEM, "device allocation of " + std::to_string(bytes) +
+                                     " bytes failed (" + cudaGetErrorString(e) +
+                                     "); lower the sampling ratio or use PINNED_HOST pages");
+  }
+  return p;
+}
+void dfree(void *p) {
+  if (p) cudaFree(p);
+}
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void allreduce_sum_i64(oocgb_ctx c, long long *d_buf, size_t count) {
+  if (c->world <= 1 || count == 0) return;
+  OOCGB_NCCL(ncclAllReduce(d_buf, d_buf, count, ncclInt64, ncclSum, c->comm, c->stream));
+}
+void allreduce_max_u64(oocgb_ctx c, unsigned long long *d_buf, size_t count) {
+  if (c->world <= 1 || count == 0) return;
+  OOCGB_NCCL(ncclAllReduce(d_buf, d_buf, count, ncclUint64, ncclMax, c->comm, c->stream));
+}
+
+cudaEvent_t pool_event(oocgb_ctx c) {
+  if (c->ev_pool.empty()) {
+    cudaEvent_t e;
+    OOCGB_CK(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = c->ev_pool.back();
+  c->ev_pool.pop_back();
+  return e;
+}
+PhaseTimer::PhaseTimer(oocgb_ctx c_, int s) : c(c_), slot(s) {
+  if (c->profiling) {
+    a = pool_event(c);
+    OOCGB_CK(cudaEventRecord(a, c->stream));
+  }
+}
+PhaseTimer::~PhaseTimer() {
+  if (!a) return;
+  cudaEvent_t b = pool_event(c);
+  cudaEventRecord(b, c->stream);
+  c->pending_slot.push_back(slot);
+  c->pending_a.push_back(a);
+  c->pending_b.push_back(b);
+}
+void record_copy_timing(oocgb_ctx c, cudaEvent_t a, cudaEvent_t b) {
+  c->pending_slot.push_back(5);
+  c->pending_a.push_back(a);
+  c->pending_b.push_back(b);
+}
+void drain_timers(oocgb_ctx c) {
+  for (size_t i = 0; i < c->pending_slot.size(); ++i) {
+    OOCGB_CK(cudaEventSynchronize(c->pending_b[i]));
+    float ms = 0.f;
+    OOCGB_CK(cudaEventElapsedTime(&ms, c->pending_a[i], c->pending_b[i]));
+    c->timings[c->pending_slot[i]] += ms;
+    if (c->pending_slot[i] == 0) c->timings[7] += 1.0;  // histogram launches
+    c->ev_pool.push_back(c->pending_a[i]);
+    c->ev_pool.push_back(c->pending_b[i]);
+  }
+  c->pending_slot.clear();
+  c->pending_a.clear();
+  c->pending_b.clear();
+}
+
+void ensure_staging(oocgb_data d) {
+  if (d->d_stage[0]) return;
+  d->stage_rows = d->rows_per_page;
+  for (int i = 0; i < kStages; ++i)
+    d->d_stage[i] = (uint8_t *)dmalloc((size_t)std::max<int64_t>(1, d->stage_rows) * d->stride);
+}
+
+}  // namespace oocgb
+
+using namespace oocgb;
+
+#define API_BEGIN try {
+#define API_END                                  \
+  return OOCGB_OK;                               \
+  }                                              \
+  catch (const oocgb::Error &e) {                \
+    set_last_error(e.what());                    \
+    return e.status;                             \
+  }                                              \
+  catch (const std::bad_alloc &) {               \
+    set_last_error("host allocation failed");    \
+    return OOCGB_ERR_NOMEM;                      \
+  }                                              \
+  catch (const std::exception &e) {              \
+    set_last_error(e.what());                    \
+    return OOCGB_ERR_DEVICE;                     \
+  }
+
+static void bind(oocgb_ctx c) { OOCGB_CK(cudaSetDevice(c->device)); }
+
+// Copy a caller array (host or device) to a fresh device buffer; returns {ptr, owned}.
+struct DevView {
+  const void *ptr = nullptr;
+  void *owned = nullptr;
+  ~DevView() { dfree(owned); }
+};
+static void view_on_device(oocgb_ctx c, const void *src, size_t bytes, DevView &v) {
+  if (is_device_ptr(src)) { v.ptr = src; return; }
+  v.owned = dmalloc(bytes);
+  OOCGB_CK(cudaMemcpyAsync(v.owned, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  v.ptr = v.owned;
+}
+
+static oocgb_data new_data(oocgb_ctx c, int64_t n_local, int64_t row0, int64_t n_global, int m,
+                           int max_bin, int64_t page_bytes, int placement, uint64_t seed) {
+  OOCGB_REQUIRE(m >= 1, OOCGB_ERR_ARG, "n_features must be >= 1");
+  OOCGB_REQUIRE(max_bin >= 2 && max_bin <= 256, OOCGB_ERR_ARG, "max_bin must be in [2, 256] (uint8 symbols)");
+  OOCGB_REQUIRE(n_local >= 0 && row0 >= 0 && n_global >= n_local && row0 + n_local <= n_global,
+                OOCGB_ERR_ARG, "row counts: need 0 <= row0, row0 + n_rows <= n_rows_global");
+  OOCGB_REQUIRE(n_local < (1LL << 31) - kPartTile, OOCGB_ERR_ARG, "at most 2^31 - 2048 rows per GPU");
+  OOCGB_REQUIRE(placement == OOCGB_PLACE_DEVICE || placement == OOCGB_PLACE_PINNED_HOST, OOCGB_ERR_ARG,
+                "placement must be DEVICE or PINNED_HOST");
+  OOCGB_REQUIRE(page_bytes >= 0, OOCGB_ERR_ARG, "page_bytes must be >= 0");
+  oocgb_data d = new oocgb_data_s();
+  d->ctx = c;
+  d->n_local = n_local;
+  d->row0 = row0;
+  d->n_global = n_global;
+  d->m = m;
+  d->stride = (m + 15) / 16 * 16;
+  d->max_bin = max_bin;
+  d->placement = placement;
+  d->seed = seed;
+  d->rows_per_page = page_bytes > 0 ? std::max<int64_t>(1, page_bytes / d->stride) : std::max<int64_t>(1, n_local);
+  d->n_pages = std::max<int64_t>(1, (n_local + d->rows_per_page - 1) / d->rows_per_page);
+  c->live_data++;
+  return d;
+}
+
+static void free_data(oocgb_data d) {
+  free_work(d);
+  dfree(d->d_cut_values); dfree(d->d_cut_ptrs); dfree(d->d_bins); dfree(d->d_sketch);
+  dfree(d->d_sketch_count); dfree(d->d_g); dfree(d->d_h); dfree(d->d_sel_rows); dfree(d->d_q);
+  dfree(d->d_sampled_page); dfree(d->d_gs); dfree(d->d_hs); dfree(d->d_tmp64);
+  for (int i = 0; i < 3; ++i) dfree(d->d_stage[i]);
+  if (d->h_pages) cudaFreeHost(d->h_pages);
+  d->ctx->live_data--;
+  delete d;
+}
+
+static void alloc_pages(oocgb_data d) {
+  const size_t bytes = (size_t)std::max<int64_t>(1, d->n_local) * d->stride;
+  if (d->placement == OOCGB_PLACE_DEVICE) {
+    d->d_bins = (uint8_t *)dmalloc(bytes);
+  } else {
+    cudaError_t e = cudaHostAlloc((void **)&d->h_pages, bytes, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(OOCGB_ERR_NOMEM, "pinned host allocation of " + std::to_string(bytes) + " bytes failed");
+    }
+  }
+}
+
+// Bin rows [row_local0, row_local0 + n) of X (device) into the pages.
+static void write_pages(oocgb_data d, const float *dX, int64_t row_local0, int64_t n) {
+  oocgb_ctx c = d->ctx;
+  int *d_err = (int *)((char *)c->d_small + 4096);
+  OOCGB_CK(cudaMemsetAsync(d_err, 0, sizeof(int), c->stream));
+  if (d->placement == OOCGB_PLACE_DEVICE) {
+    bin_rows(d, dX, n, d->d_bins + row_local0 * d->stride, d_err);
+  } else {
+    ensure_staging(d);
+    for (int64_t r = 0; r < n; r += d->stage_rows) {
+      int64_t nr = std::min<int64_t>(d->stage_rows, n - r);
+      bin_rows(d, dX + r * d->m, nr, d->d_stage[0], d_err);
+      OOCGB_CK(cudaMemcpyAsync(d->h_pages + (row_local0 + r) * d->stride, d->d_stage[0], (size_t)nr * d->stride,
+                               cudaMemcpyDeviceToHost, c->stream));
+      OOCGB_CK(cudaStreamSynchronize(c->stream));
+    }
+  }
+  int herr = 0;
+  OOCGB_CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  OOCGB_REQUIRE(herr == 0, OOCGB_ERR_ARG, "quantise: non-finite value in X (dense path, R4)");
+}
+
+// Run fn(dX_batch, row_offset, n_batch) over X (host or device) in device batches.
+template <class F>
+static void over_batches(oocgb_ctx c, const float *X, int64_t n, int m, F fn) {
+  if (n <= 0) return;
+  if (is_device_ptr(X)) { fn(X, 0, n); return; }
+  const int64_t batch = std::max<int64_t>(1, (256LL << 20) / ((int64_t)m * 4));
+  float *buf = (float *)dmalloc(sizeof(float) * (size_t)std::min(batch, n) * m);
+  try {
+    for (int64_t r = 0; r < n; r += batch) {
+      int64_t nr = std::min(batch, n - r);
+      OOCGB_CK(cudaMemcpyAsync(buf, X + r * m, sizeof(float) * (size_t)nr * m, cudaMemcpyHostToDevice, c->stream));
+      fn(buf, r, nr);
+      OOCGB_CK(cudaStreamSynchronize(c->stream));
+    }
+  } catch (...) {
+    dfree(buf);
+    throw;
+  }
+  dfree(buf);
+}
+
+extern "C" {
+
+const char *oocgb_last_error(void) { return g_last_error.c_str(); }
+int32_t oocgb_abi_version(void) { return 1; }
+
+int oocgb_nccl_unique_id(uint8_t out[128]) {
+  API_BEGIN
+  OOCGB_REQUIRE(out, OOCGB_ERR_ARG, "out is NULL");
+  ncclUniqueId id;
+  OOCGB_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out, &id, 128);
+  API_END
+}
+
+int oocgb_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t *nccl_id,
+                     uint64_t cuda_stream, oocgb_ctx *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(out, OOCGB_ERR_ARG, "out is NULL");
+  OOCGB_REQUIRE(world >= 1 && rank >= 0 && rank < world, OOCGB_ERR_ARG, "need 0 <= rank < world");
+  OOCGB_REQUIRE(world == 1 || nccl_id, OOCGB_ERR_ARG, "nccl_id required when world > 1");
+  int ndev = 0;
+  OOCGB_CK(cudaGetDeviceCount(&ndev));
+  OOCGB_REQUIRE(device >= 0 && device < ndev, OOCGB_ERR_ARG, "device out of range");
+  OOCGB_CK(cudaSetDevice(device));
+  oocgb_ctx c = new oocgb_ctx_s();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  try {
+    cudaDeviceProp p;
+    OOCGB_CK(cudaGetDeviceProperties(&p, device));
+    c->num_sms = p.multiProcessorCount;
+    if (cuda_stream) {
+      c->stream = (cudaStream_t)cuda_stream;
+    } else {
+      OOCGB_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    OOCGB_CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    OOCGB_CK(cudaMalloc(&c->d_small, 1 << 20));
+    OOCGB_CK(cudaMallocHost(&c->h_small, 1 << 20));
+    if (world > 1) {
+      ncclUniqueId id;
+      memcpy(&id, nccl_id, 128);
+      OOCGB_NCCL(ncclCommInitRank(&c->comm, world, id, rank));
+    }
+  } catch (...) {
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->d_small) cudaFree(c->d_small);
+    if (c->h_small) cudaFreeHost(c->h_small);
+    delete c;
+    throw;
+  }
+  *out = c;
+  API_END
+}
+
+int oocgb_ctx_destroy(oocgb_ctx c) {
+  API_BEGIN
+  OOCGB_REQUIRE(c, OOCGB_ERR_ARG, "ctx is NULL");
+  OOCGB_REQUIRE(c->live_data == 0, OOCGB_ERR_STATE, "ctx_destroy: data handles are still alive");
+  bind(c);
+  cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto e : c->pending_a) cudaEventDestroy(e);
+  for (auto e : c->pending_b) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->copy_stream);
+  cudaFree(c->d_small);
+  cudaFreeHost(c->h_small);
+  delete c;
+  API_END
+}
+
+int oocgb_quantise(oocgb_ctx c, const float *X, int64_t n_rows, int64_t row0_global, int64_t n_rows_global,
+                   int32_t n_features, int32_t max_bin, int64_t page_bytes, int32_t placement, uint64_t seed,
+                   oocgb_data *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(c && out, OOCGB_ERR_ARG, "ctx/out is NULL");
+  OOCGB_REQUIRE(X || n_rows == 0, OOCGB_ERR_ARG, "X is NULL");
+  bind(c);
+  oocgb_data d = new_data(c, n_rows, row0_global, n_rows_global, n_features, max_bin, page_bytes, placement, seed);
+  try {
+    // Alg. 2 (sketch) then Alg. 4/5 (ELLPACK pages)
+    over_batches(c, X, n_rows, n_features, [&](const float *dX, int64_t r, int64_t nr) {
+      sketch_append(d, dX, row0_global + r, nr);
+    });
+    cuts_finalize(d);
+    alloc_pages(d);
+    over_batches(c, X, n_rows, n_features, [&](const float *dX, int64_t r, int64_t nr) {
+      write_pages(d, dX, r, nr);
+    });
+    d->rows_written = n_rows;
+  } catch (...) {
+    free_data(d);
+    throw;
+  }
+  *out = d;
+  API_END
+}
+
+int oocgb_sketch_begin(oocgb_ctx c, int32_t n_features, int32_t max_bin, int64_t n_rows, int64_t row0_global,
+                       int64_t n_rows_global, int64_t page_bytes, int32_t placement, uint64_t seed,
+                       oocgb_data *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(c && out, OOCGB_ERR_ARG, "ctx/out is NULL");
+  bind(c);
+  oocgb_data d = new_data(c, n_rows, row0_global, n_rows_global, n_features, max_bin, page_bytes, placement, seed);
+  *out = d;
+  API_END
+}
+
+int oocgb_sketch_push(oocgb_data d, const float *X, int64_t row0_global, int64_t n) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && (X || n == 0), OOCGB_ERR_ARG, "data/X is NULL");
+  OOCGB_REQUIRE(!d->cuts_ready, OOCGB_ERR_STATE, "sketch_push after cuts_finalize");
+  OOCGB_REQUIRE(row0_global >= d->row0 && row0_global + n <= d->row0 + d->n_local, OOCGB_ERR_ARG,
+                "sketch_push: rows outside this rank's range");
+  bind(d->ctx);
+  over_batches(d->ctx, X, n, d->m, [&](const float *dX, int64_t r, int64_t nr) {
+    sketch_append(d, dX, row0_global + r, nr);
+  });
+  API_END
+}
+
+int oocgb_cuts_finalize(oocgb_data d) {
+  API_BEGIN
+  OOCGB_REQUIRE(d, OOCGB_ERR_ARG, "data is NULL");
+  OOCGB_REQUIRE(!d->cuts_ready, OOCGB_ERR_STATE, "cuts already finalized");
+  bind(d->ctx);
+  cuts_finalize(d);
+  alloc_pages(d);
+  API_END
+}
+
+int oocgb_pages_push(oocgb_data d, const float *X, int64_t row0_global, int64_t n) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && (X || n == 0), OOCGB_ERR_ARG, "data/X is NULL");
+  OOCGB_REQUIRE(d->cuts_ready, OOCGB_ERR_STATE, "pages_push before cuts_finalize");
+  OOCGB_REQUIRE(row0_global == d->row0 + d->rows_written && d->rows_written + n <= d->n_local, OOCGB_ERR_ARG,
+                "pages_push: rows must arrive in ascending global order, each once");
+  bind(d->ctx);
+  const int64_t base = d->rows_written;
+  over_batches(d->ctx, X, n, d->m, [&](const float *dX, int64_t r, int64_t nr) {
+    write_pages(d, dX, base + r, nr);
+  });
+  d->rows_written += n;
+  API_END
+}
+
+int oocgb_quantise_like(oocgb_data ref, const float *X, int64_t n_rows, int32_t placement, oocgb_data *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(ref && out && (X || n_rows == 0), OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(ref->cuts_ready, OOCGB_ERR_STATE, "reference data has no cuts");
+  oocgb_ctx c = ref->ctx;
+  bind(c);
+  oocgb_data d = new_data(c, n_rows, 0, n_rows, ref->m, ref->max_bin,
+                          ref->rows_per_page * (int64_t)ref->stride, placement, ref->seed);
+  try {
+    d->h_cut_values = ref->h_cut_values;
+    d->h_cut_ptrs = ref->h_cut_ptrs;
+    d->d_cut_values = (float *)dmalloc(sizeof(float) * std::max<size_t>(1, d->h_cut_values.size()));
+    d->d_cut_ptrs = (int32_t *)dmalloc(sizeof(int32_t) * (d->m + 1));
+    OOCGB_CK(cudaMemcpyAsync(d->d_cut_values, d->h_cut_values.data(), sizeof(float) * d->h_cut_values.size(),
+                             cudaMemcpyHostToDevice, c->stream));
+    OOCGB_CK(cudaMemcpyAsync(d->d_cut_ptrs, d->h_cut_ptrs.data(), sizeof(int32_t) * (d->m + 1),
+                             cudaMemcpyHostToDevice, c->stream));
+    d->cuts_ready = true;
+    alloc_pages(d);
+    over_batches(c, X, n_rows, d->m, [&](const float *dX, int64_t r, int64_t nr) { write_pages(d, dX, r, nr); });
+    d->rows_written = n_rows;
+  } catch (...) {
+    free_data(d);
+    throw;
+  }
+  *out = d;
+  API_END
+}
+
+int oocgb_data_info(oocgb_data d, oocgb_info *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && out, OOCGB_ERR_ARG, "NULL argument");
+  out->n_rows_local = d->n_local;
+  out->n_rows_global = d->n_global;
+  out->row0_global = d->row0;
+  out->n_features = d->m;
+  out->row_stride = d->stride;
+  out->max_bin = d->max_bin;
+  out->placement = d->placement;
+  out->n_pages = d->n_pages;
+  out->rows_per_page = d->rows_per_page;
+  out->total_cuts = (int64_t)d->h_cut_values.size();
+  API_END
+}
+
+int oocgb_data_destroy(oocgb_data d) {
+  API_BEGIN
+  OOCGB_REQUIRE(d, OOCGB_ERR_ARG, "data is NULL");
+  bind(d->ctx);
+  cudaStreamSynchronize(d->ctx->stream);
+  free_data(d);
+  API_END
+}
+
+static void ensure_grad(oocgb_data d) {
+  if (!d->d_g) {
+    d->d_g = (float *)dmalloc(sizeof(float) * std::max<int64_t>(1, d->n_local));
+    d->d_h = (float *)dmalloc(sizeof(float) * std::max<int64_t>(1, d->n_local));
+  }
+}
+
+int oocgb_set_gradients(oocgb_data d, const float *g, const float *h, int64_t n_local) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && ((g && h) || n_local == 0), OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(n_local == d->n_local, OOCGB_ERR_ARG, "set_gradients: length != n_rows_local");
+  oocgb_ctx c = d->ctx;
+  bind(c);
+  ensure_grad(d);
+  if (n_local > 0) {
+    OOCGB_CK(cudaMemcpyAsync(d->d_g, g, sizeof(float) * n_local, cudaMemcpyDefault, c->stream));
+    OOCGB_CK(cudaMemcpyAsync(d->d_h, h, sizeof(float) * n_local, cudaMemcpyDefault, c->stream));
+  }
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  d->has_grad = true;
+  d->has_sample = false;
+  API_END
+}
+
+int oocgb_set_logistic_gradients(oocgb_data d, const float *margin, const float *labels, int64_t n_local) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && ((margin && labels) || n_local == 0), OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(n_local == d->n_local, OOCGB_ERR_ARG, "set_logistic_gradients: length != n_rows_local");
+  oocgb_ctx c = d->ctx;
+  bind(c);
+  ensure_grad(d);
+  DevView vm, vy;
+  if (n_local > 0) {
+    view_on_device(c, margin, sizeof(float) * n_local, vm);
+    view_on_device(c, labels, sizeof(float) * n_local, vy);
+    logistic_gradients(d, (const float *)vm.ptr, (const float *)vy.ptr);
+  }
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  d->has_grad = true;
+  d->has_sample = false;
+  API_END
+}
+
+int oocgb_sample(oocgb_data d, int32_t mode, double ratio, double mvs_lambda, uint64_t seed, uint64_t round,
+                 int32_t quant_bits, oocgb_sample_info *info) {
+  API_BEGIN
+  OOCGB_REQUIRE(d, OOCGB_ERR_ARG, "data is NULL");
+  OOCGB_REQUIRE(mode >= 0 && mode <= 2, OOCGB_ERR_ARG, "mode must be NONE, UNIFORM or MVS");
+  OOCGB_REQUIRE(ratio > 0.0 && ratio <= 1.0, OOCGB_ERR_ARG, "ratio must be in (0, 1] (S:L302)");
+  OOCGB_REQUIRE(mvs_lambda >= 0.0 && std::isfinite(mvs_lambda), OOCGB_ERR_ARG, "mvs_lambda must be >= 0");
+  OOCGB_REQUIRE(quant_bits >= 8 && quant_bits <= 20, OOCGB_ERR_ARG, "quant_bits must be in [8, 20] (R12)");
+  OOCGB_REQUIRE(d->cuts_ready && d->rows_written == d->n_local, OOCGB_ERR_STATE, "sample: pages not complete");
+  OOCGB_REQUIRE(d->has_grad, OOCGB_ERR_STATE, "sample before set_gradients");
+  bind(d->ctx);
+  sample_rows(d, mode, ratio, mvs_lambda, seed, round, quant_bits, info);
+  API_END
+}
+
+int oocgb_build_tree(oocgb_data d, int32_t max_depth, double lambda, double gamma, double min_child_weight,
+                     double eta, int32_t keep_debug, oocgb_tree *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && out, OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(max_depth >= 0 && max_depth <= 16, OOCGB_ERR_ARG, "max_depth must be in [0, 16]");
+  OOCGB_REQUIRE(lambda >= 0.0 && std::isfinite(lambda) && std::isfinite(gamma) && std::isfinite(eta) &&
+                    std::isfinite(min_child_weight),
+                OOCGB_ERR_ARG, "lambda >= 0 and finite gamma / eta / min_child_weight required");
+  OOCGB_REQUIRE(d->has_sample, OOCGB_ERR_STATE, "build_tree before sample");
+  bind(d->ctx);
+  *out = build_tree(d, max_depth, lambda, gamma, min_child_weight, eta, keep_debug != 0);
+  API_END
+}
+
+int oocgb_tree_export(oocgb_tree t, oocgb_node *nodes, int32_t capacity, int32_t *n_nodes) {
+  API_BEGIN
+  OOCGB_REQUIRE(t && n_nodes, OOCGB_ERR_ARG, "NULL argument");
+  *n_nodes = (int32_t)t->nodes.size();
+  if (nodes) {
+    OOCGB_REQUIRE(capacity >= (int32_t)t->nodes.size(), OOCGB_ERR_ARG, "tree_export: capacity too small");
+    memcpy(nodes, t->nodes.data(), sizeof(oocgb_node) * t->nodes.size());
+  }
+  API_END
+}
+
+int oocgb_tree_destroy(oocgb_tree t) {
+  API_BEGIN
+  OOCGB_REQUIRE(t, OOCGB_ERR_ARG, "tree is NULL");
+  dfree(t->d_pnodes);
+  delete t;
+  API_END
+}
+
+int oocgb_predict(oocgb_data d, const oocgb_tree *trees, int32_t n_trees, float *margin) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && (trees || n_trees == 0) && (margin || d->n_local == 0), OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(d->cuts_ready && d->rows_written == d->n_local, OOCGB_ERR_STATE, "predict: pages not complete");
+  for (int t = 0; t < n_trees; ++t) OOCGB_REQUIRE(trees[t], OOCGB_ERR_ARG, "NULL tree");
+  oocgb_ctx c = d->ctx;
+  bind(c);
+  PhaseTimer timer(c, 4);
+  if (d->n_local == 0 || n_trees == 0) return OOCGB_OK;
+  const bool dev = is_device_ptr(margin);
+  float *dm = margin;
+  if (!dev) {
+    dm = (float *)dmalloc(sizeof(float) * d->n_local);
+    OOCGB_CK(cudaMemcpyAsync(dm, margin, sizeof(float) * d->n_local, cudaMemcpyHostToDevice, c->stream));
+  }
+  try {
+    for (int t0 = 0; t0 < n_trees; t0 += 4096) {
+      int nt = std::min(4096, n_trees - t0);
+      if (d->placement == OOCGB_PLACE_DEVICE) {
+        predict_device(d, d->d_bins, d->n_local, 0, trees + t0, nt, dm);
+      } else {
+        for_each_page(d, [&](const uint8_t *page, int64_t r0, int64_t nr) {
+          predict_device(d, page, nr, r0, trees + t0, nt, dm);
+        });
+      }
+    }
+    if (!dev) {
+      OOCGB_CK(cudaMemcpyAsync(margin, dm, sizeof(float) * d->n_local, cudaMemcpyDeviceToHost, c->stream));
+      OOCGB_CK(cudaStreamSynchronize(c->stream));
+      dfree(dm);
+    }
+  } catch (...) {
+    if (!dev) dfree(dm);
+    throw;
+  }
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  API_END
+}
+
+int oocgb_update_margin(oocgb_data d, oocgb_tree t, float *margin) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && t && (margin || d->n_local == 0), OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(t->owner == d, OOCGB_ERR_STATE, "update_margin: tree built from another data handle");
+  oocgb_ctx c = d->ctx;
+  bind(c);
+  PhaseTimer timer(c, 4);
+  if (d->n_local == 0) return OOCGB_OK;
+  DevView v;
+  const bool dev = is_device_ptr(margin);
+  float *dm = margin;
+  if (!dev) {
+    dm = (float *)dmalloc(sizeof(float) * d->n_local);
+    v.owned = dm;
+    OOCGB_CK(cudaMemcpyAsync(dm, margin, sizeof(float) * d->n_local, cudaMemcpyHostToDevice, c->stream));
+  }
+  update_margin(d, t, dm);
+  if (!dev) {
+    OOCGB_CK(cudaMemcpyAsync(margin, dm, sizeof(float) * d->n_local, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+  }
+  API_END
+}
+
+int oocgb_get_cuts(oocgb_data d, float *values, int32_t *offsets) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && values && offsets, OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(d->cuts_ready, OOCGB_ERR_STATE, "no cuts yet");
+  memcpy(values, d->h_cut_values.data(), sizeof(float) * d->h_cut_values.size());
+  memcpy(offsets, d->h_cut_ptrs.data(), sizeof(int32_t) * d->h_cut_ptrs.size());
+  API_END
+}
+
+int oocgb_get_bins(oocgb_data d, int64_t row0_local, int64_t n, uint8_t *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(d && (out || n == 0), OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(row0_local >= 0 && n >= 0 && row0_local + n <= d->rows_written, OOCGB_ERR_ARG,
+                "get_bins: row range outside the written pages");
+  bind(d->ctx);
+  if (n == 0) return OOCGB_OK;
+  if (d->placement == OOCGB_PLACE_DEVICE)
+    OOCGB_CK(cudaMemcpy(out, d->d_bins + row0_local * d->stride, (size_t)n * d->stride, cudaMemcpyDeviceToHost));
+  else
+    memcpy(out, d->h_pages + row0_local * d->stride, (size_t)n * d->stride);
+  API_END
+}
+
+int oocgb_get_sample(oocgb_data d, int64_t *gid, int64_t *q_g, int64_t *q_h) {
+  API_BEGIN
+  OOCGB_REQUIRE(d, OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(d->has_sample, OOCGB_ERR_STATE, "get_sample before sample");
+  bind(d->ctx);
+  const int64_t n = d->n_sel;
+  std::vector<int2> q(n);
+  std::vector<int32_t> rows(n);
+  if (n) {
+    OOCGB_CK(cudaMemcpy(q.data(), d->d_q, sizeof(int2) * n, cudaMemcpyDeviceToHost));
+    if (!d->all_selected) OOCGB_CK(cudaMemcpy(rows.data(), d->d_sel_rows, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (gid) gid[i] = d->row0 + (d->all_selected ? i : rows[i]);
+    if (q_g) q_g[i] = q[i].x;
+    if (q_h) q_h[i] = q[i].y;
+  }
+  API_END
+}
+
+int oocgb_get_histogram(oocgb_tree t, int32_t node, int64_t *gh) {
+  API_BEGIN
+  OOCGB_REQUIRE(t && gh, OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(t->debug, OOCGB_ERR_STATE, "get_histogram needs build_tree(keep_debug=1)");
+  OOCGB_REQUIRE(node >= 0 && node < (1 << t->max_depth) - 1, OOCGB_ERR_ARG, "node must have depth < max_depth");
+  const size_t hsz = (size_t)t->owner->m * kBins * 2;
+  memcpy(gh, t->hist.data() + hsz * node, sizeof(int64_t) * hsz);
+  API_END
+}
+
+int oocgb_get_partition(oocgb_tree t, int32_t *leaf_of_row) {
+  API_BEGIN
+  OOCGB_REQUIRE(t && leaf_of_row, OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(t->debug, OOCGB_ERR_STATE, "get_partition needs build_tree(keep_debug=1)");
+  memcpy(leaf_of_row, t->leaf_of_row.data(), sizeof(int32_t) * t->leaf_of_row.size());
+  API_END
+}
+
+int oocgb_get_timings(oocgb_ctx c, double *out, int32_t n) {
+  API_BEGIN
+  OOCGB_REQUIRE(c && out, OOCGB_ERR_ARG, "NULL argument");
+  bind(c);
+  drain_timers(c);
+  for (int i = 0; i < n && i < 16; ++i) out[i] = c->timings[i];
+  for (int i = 0; i < 16; ++i) c->timings[i] = 0.0;
+  API_END
+}
+
+int oocgb_set_profiling(oocgb_ctx c, int32_t enable) {
+  API_BEGIN
+  OOCGB_REQUIRE(c, OOCGB_ERR_ARG, "NULL argument");
+  bind(c);
+  drain_timers(c);
+  c->profiling = enable != 0;
+  for (int i = 0; i < 16; ++i) c->timings[i] = 0.0;
+  API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+// Internal declarations of liboocgb (B200 / sm_100a).  Not part of the ABI (include/oocgb.h).
+// Citations: "P:Lx" = PAPER.md line, "Rk" = reading k in DESIGN.md §3.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/oocgb.h"
+
+namespace oocgb {
+
+// ---------------------------------------------------------------------------------------------
+// Errors: thrown inside the library, turned into a status code + thread-local message at the
+// C-ABI boundary (api.cu).
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string &m) : std::runtime_error(m), status(s) {}
+};
+
+#define OOCGB_CK(call)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      int st_ = (e_ == cudaErrorMemoryAllocation) ? OOCGB_ERR_NOMEM : OOCGB_ERR_DEVICE;      \
+      throw ::oocgb::Error(st_, std::string(#call) + ": " + cudaGetErrorString(e_) + " @" + \
+                                    __FILE__ + ":" + std::to_string(__LINE__));             \
+    }                                                                                        \
+  } while (0)
+
+#define OOCGB_NCCL(call)                                                                     \
+  do {                                                                                       \
+    ncclResult_t r_ = (call);                                                                \
+    if (r_ != ncclSuccess)                                                                   \
+      throw ::oocgb::Error(OOCGB_ERR_DEVICE, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+#define OOCGB_REQUIRE(cond, status, msg)                                                     \
+  do {                                                                                       \
+    if (!(cond)) throw ::oocgb::Error((status), (msg));                                      \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------------
+// Tuning constants.
+constexpr int kFG = 32;              // features per histogram feature-group (one 32 B sector)
+constexpr int kBins = 256;           // uint8 symbols (R5, R7)
+constexpr int kHistThreads = 256;    // histogram CTA
+constexpr int kHistSmem = 2 * kBins * kFG * 4;  // g and h s32 planes [bin][32 features]
+constexpr int kPartTile = 2048;      // positions per partition tile
+constexpr int kPartThreads = 256;
+
+// Device node record (heap order).  G/H keep the exact fixed-point sums.
+struct DNode {
+  int32_t feature;     // -2 absent, -1 leaf, >= 0 split feature
+  int32_t split_bin;
+  float split_value;
+  float leaf_value;
+  double gain;
+  double sum_g, sum_h;
+  long long n_rows;    // global sampled rows
+  long long Gq, Hq;    // fixed-point sums (global)
+};
+
+// Row segment of the partition at one depth (pass-through segments carry leaves).
+struct Seg {
+  int32_t begin, count;  // local positions
+  int32_t node;          // heap index
+  int32_t pad;
+};
+
+// Sibling pair built at a level: `built` gets a histogram from rows, `derived` = parent - built.
+struct Pair {
+  int32_t parent;      // heap id (-1 at the root level)
+  int32_t built;       // heap id
+  int32_t derived;     // heap id (-1 at the root level)
+  int32_t begin;       // local positions of the built child's rows
+  int32_t count;
+  int32_t chunk_base;  // first global chunk of this pair
+  int32_t n_chunks;
+  int32_t chunk_rows;
+};
+
+// Best split candidate of one (node, feature).
+struct Cand {
+  double gain;
+  int32_t bin;
+  int32_t valid;
+  long long GL, HL;
+};
+
+struct LevelCtl {       // device-resident control block of one build
+  int n_pairs;
+  int n_items;
+  int n_segs;
+  int n_splits;         // splits decided at the current level
+  int error;            // 1: H + lambda <= 0 at a node
+  int pad[3];
+};
+
+struct PNode {          // compact node for predict
+  int32_t feature;
+  int32_t split_bin;
+  float leaf;
+  int32_t pad;
+};
+
+}  // namespace oocgb
+
+// ---------------------------------------------------------------------------------------------
+// Opaque handle structs.
+struct oocgb_ctx_s {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t copy_stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int live_data = 0;
+  int num_sms = 148;
+  bool profiling = false;
+  double timings[16] = {0};
+  std::vector<cudaEvent_t> ev_pool;          // recycled events
+  std::vector<int> pending_slot;             // (slot, event a, event b) recorded, not yet read
+  std::vector<cudaEvent_t> pending_a, pending_b;
+  // scratch for small host<->device exchanges
+  void *d_small = nullptr;   // 1 MB device scratch
+  void *h_small = nullptr;   // 1 MB pinned scratch
+};
+
+struct oocgb_data_s {
+  oocgb_ctx ctx = nullptr;
+  int64_t n_local = 0, n_global = 0, row0 = 0;
+  int32_t m = 0, stride = 0, max_bin = 256, placement = OOCGB_PLACE_DEVICE;
+  int64_t rows_per_page = 0, n_pages = 1;
+  uint64_t seed = 0;
+  // cuts (R1-R4)
+  float *d_cut_values = nullptr;
+  int32_t *d_cut_ptrs = nullptr;
+  std::vector<float> h_cut_values;
+  std::vector<int32_t> h_cut_ptrs;
+  bool cuts_ready = false;
+  // ELLPACK (R5-R6)
+  uint8_t *d_bins = nullptr;    // DEVICE placement: [n_local][stride]
+  uint8_t *h_pages = nullptr;   // PINNED_HOST placement: [n_local][stride] (pages are row ranges)
+  int64_t rows_written = 0;     // streamed pages_push progress
+  // streamed sketch state
+  uint32_t *d_sketch = nullptr; // column-major ordered keys [m][cap]
+  int64_t sketch_cap = 0;
+  unsigned long long *d_sketch_count = nullptr;
+  bool sketch_all_rows = true;
+  // gradients
+  float *d_g = nullptr, *d_h = nullptr;
+  bool has_grad = false;
+  // sample
+  bool has_sample = false;
+  bool all_selected = false;
+  int64_t n_sel = 0, n_sel_global = 0;
+  int32_t *d_sel_rows = nullptr;   // local row ids, ascending
+  int2 *d_q = nullptr;             // (q_g, q_h), |q| <= 2^quant_bits
+  int32_t e_g = 0, e_h = 0, quant_bits = 16;
+  long long G_root = 0, H_root = 0;
+  uint8_t *d_sampled_page = nullptr;  // PINNED_HOST: compacted selected rows (Alg. 7)
+  int64_t sampled_cap = 0;
+  int64_t sel_cap = 0;
+  double *d_gs = nullptr, *d_hs = nullptr;  // scaled g', h' of the selected rows
+  long long *d_tmp64 = nullptr;             // MVS g_hat / q64 [n_local]
+  int64_t tmp_cap = 0;
+  // tree workspace (lazy, sized for (n_sel cap, depth))
+  struct Work *work = nullptr;
+  uint64_t tree_serial = 0;
+  // staging for streamed pages
+  uint8_t *d_stage[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t stage_ev[3] = {};
+  int64_t stage_rows = 0;
+};
+
+struct oocgb_tree_s {
+  oocgb_data owner = nullptr;
+  uint64_t serial = 0;
+  int32_t max_depth = 0;
+  std::vector<oocgb_node> nodes;
+  oocgb::PNode *d_pnodes = nullptr;  // device copy for predict
+  bool debug = false;
+  std::vector<long long> hist;       // [2^D - 1][m][256][2]
+  std::vector<int32_t> leaf_of_row;  // selected order
+};
+
+namespace oocgb {
+
+// ---------------------------------------------------------------------------------------------
+// Host-side launchers, one per kernel family (quantise.cu, sample.cu, tree.cu).
+void set_last_error(const std::string &msg);
+void *dmalloc(size_t bytes);
+void dfree(void *p);
+bool is_device_ptr(const void *p);
+
+// quantise.cu
+void sketch_append(oocgb_data d, const float *dX, int64_t row0_global, int64_t n);
+void cuts_finalize(oocgb_data d);
+void bin_rows(oocgb_data d, const float *dX, int64_t n, uint8_t *d_out, int *d_err);
+
+// sample.cu
+void logistic_gradients(oocgb_data d, const float *d_margin, const float *d_labels);
+void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64_t seed,
+                 uint64_t round, int quant_bits, oocgb_sample_info *info);
+
+// tree.cu
+oocgb_tree build_tree(oocgb_data d, int max_depth, double lambda, double gamma, double mcw,
+                      double eta, bool keep_debug);
+void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t n_rows, int64_t row_offset,
+                    const oocgb_tree *trees, int n_trees, float *d_margin);
+void update_margin(oocgb_data d, oocgb_tree t, float *d_margin);
+void free_work(oocgb_data d);
+
+
+// NCCL helpers (no-ops when world == 1)
+void allreduce_sum_i64(oocgb_ctx c, long long *d_buf, size_t count);
+void allreduce_max_u64(oocgb_ctx c, unsigned long long *d_buf, size_t count);
+
+// profiling: when ctx->profiling, records an event pair around a phase on the ctx stream
+// (no synchronisation); oocgb_get_timings() later sums the elapsed times into timings[slot].
+struct PhaseTimer {
+  oocgb_ctx c;
+  int slot;
+  cudaEvent_t a = nullptr;
+  PhaseTimer(oocgb_ctx c_, int s);
+  ~PhaseTimer();
+};
+void drain_timers(oocgb_ctx c);
+
+}  // namespace oocgb

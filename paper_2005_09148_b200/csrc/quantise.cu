@@ -1,0 +1,342 @@
+// Quantile sketch (Alg. 2-3) and ELLPACK page writer (Alg. 4-5)
+// for sm_100a.  One-time preprocessing ("should only be done once at the beginning of
+// training") — not in sec/round.
+//
+// Cuts (R1-R4): a global-row-keyed Philox Bernoulli sample of <= 2^20 rows (all rows when
+// n_global <= 2^20) is gathered as order-preserving uint32 keys, sorted per feature with a
+// segmented radix sort (CUB, a library sort primitive), and the cut of rank ceil(b N / B) is
+// read for b = 1..B (or every distinct value when there are <= B of them).
+// Bins (R3, R5): bin = lower_bound(cuts_j, x) clamped to B_j - 1, one byte per (row, feature).
+#include <cub/device/device_segmented_radix_sort.cuh>
+
+#include "internal.cuh"
+#include "philox.cuh"
+
+namespace oocgb {
+
+// Order-preserving float -> uint32 key, -0.0 canonicalised to +0.0 (R4).
+__device__ __forceinline__ uint32_t float_key(float x) {
+  if (x == 0.0f) x = 0.0f;
+  uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_float(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k ^ 0x80000000u) : ~k;
+  return __uint_as_float(u);
+}
+
+// One warp per row: Philox selection (stream 1, round 2^64-1, R2), then the row's m keys are
+// appended row-major at an atomically claimed slot (slot order is irrelevant: keys are sorted).
+__global__ void k_sketch_append(const float *__restrict__ X, int64_t n, int m, int64_t row0_global,
+                                int64_t n_global, uint64_t seed, bool all_rows, uint32_t *sample,
+                                int64_t cap, unsigned long long *count, int *err) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const double p = (double)(1 << 20) / (double)n_global;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    bool sel = true;
+    if (!all_rows) sel = philox_uniform(seed, ~0ull, (uint64_t)(row0_global + r), 1) < p;
+    if (!sel) continue;
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd(count, 1ull);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if ((int64_t)slot >= cap) {
+      if (lane == 0) atomicExch(err, 3);
+      continue;
+    }
+    const float *xr = X + r * (int64_t)m;
+    uint32_t *out = sample + (int64_t)slot * m;
+    for (int j = lane; j < m; j += 32) {
+      float x = xr[j];
+      if (!isfinite(x)) atomicExch(err, 2);
+      out[j] = float_key(x);
+    }
+  }
+}
+
+// Row-major [N][m] -> column-major [m][N] through a padded 32x32 shared tile.
+__global__ void k_transpose_keys(const uint32_t *__restrict__ in, int64_t N, int m,
+                                 uint32_t *__restrict__ out) {
+  __shared__ uint32_t t[32][33];
+  int64_t r0 = (int64_t)blockIdx.x * 32;
+  int c0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t r = r0 + i;
+    int c = c0 + threadIdx.x;
+    if (r < N && c < m) t[i][threadIdx.x] = in[r * m + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int c = c0 + i;
+    int64_t r = r0 + threadIdx.x;
+    if (r < N && c < m) out[(int64_t)c * N + r] = t[threadIdx.x][i];
+  }
+}
+
+// One block per feature over its sorted keys s[0..N): O1 steps 3-5.
+__global__ void k_extract_cuts(const uint32_t *__restrict__ sorted, int64_t N, int B,
+                               float *cuts_out /*[m][256]*/, int *cnt_out /*[m]*/) {
+  int j = blockIdx.x;
+  const uint32_t *s = sorted + (int64_t)j * N;
+  __shared__ unsigned long long distinct;
+  __shared__ uint32_t vals[256];
+  __shared__ int nvals;
+  __shared__ int keep[257];
+  if (threadIdx.x == 0) { distinct = 0; nvals = 0; }
+  __syncthreads();
+  if (N == 0) {  // step 5: no observed values -> one cut 0.0
+    if (threadIdx.x == 0) { cuts_out[j * 256] = 0.0f; cnt_out[j] = 1; }
+    return;
+  }
+  unsigned long long dl = 0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) dl += (i == 0 || s[i] != s[i - 1]);
+  for (int o = 16; o; o >>= 1) dl += __shfl_down_sync(0xffffffffu, dl, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&distinct, dl);
+  __syncthreads();
+  if (distinct <= (unsigned long long)B) {
+    // step 3: every distinct value is a cut (collected, then ordered by rank)
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x)
+      if (i == 0 || s[i] != s[i - 1]) vals[atomicAdd(&nvals, 1)] = s[i];
+    __syncthreads();
+    int D = nvals;
+    if (threadIdx.x < D) {
+      uint32_t v = vals[threadIdx.x];
+      int rank = 0;
+      for (int u = 0; u < D; ++u) rank += vals[u] < v;
+      cuts_out[j * 256 + rank] = key_float(v);
+    }
+    if (threadIdx.x == 0) cnt_out[j] = D;
+  } else {
+    // step 4: c_b = v[ceil(b N / B)] (1-based), repeats dropped
+    int b = threadIdx.x + 1;
+    uint32_t v = 0;
+    if (b <= B) {
+      int64_t idx = ((int64_t)b * N + B - 1) / B;
+      v = s[idx - 1];
+      vals[threadIdx.x] = v;
+    }
+    __syncthreads();
+    int k = (b <= B) && (b == 1 || v > vals[threadIdx.x - 1]);
+    keep[threadIdx.x] = k;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // B <= 256: a sequential scan is fine
+      int acc = 0;
+      for (int t = 0; t < B; ++t) { int kk = keep[t]; keep[t] = acc; acc += kk; }
+      keep[256] = acc;
+    }
+    __syncthreads();
+    if (k) cuts_out[j * 256 + keep[threadIdx.x]] = key_float(v);
+    if (threadIdx.x == 0) cnt_out[j] = keep[256];
+  }
+}
+
+// LookupBin + Write (Alg. 4): thread per (row, 4 features) -> one 32-bit store.
+__global__ void k_bin_rows(const float *__restrict__ X, int64_t n, int m, int stride,
+                           const float *__restrict__ cuts, const int *__restrict__ ptrs,
+                           uint8_t *__restrict__ out, int *err) {
+  int quads = stride >> 2;
+  int64_t total = n * quads;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / quads;
+    int q = (int)(t - r * quads);
+    uint32_t word = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int j = q * 4 + c;
+      if (j >= m) break;
+      float x = X[r * m + j];
+      if (!isfinite(x)) { atomicExch(err, 2); continue; }
+      int lo = __ldg(ptrs + j), hi = __ldg(ptrs + j + 1);
+      int B = hi - lo;
+      int a = 0, bnd = B;  // lower_bound: smallest b with x <= c_b
+      while (a < bnd) {
+        int mid = (a + bnd) >> 1;
+        if (x <= __ldg(cuts + lo + mid)) bnd = mid; else a = mid + 1;
+      }
+      if (a > B - 1) a = B - 1;  // clamp above the last cut (R3)
+      word |= (uint32_t)a << (8 * c);
+    }
+    reinterpret_cast<uint32_t *>(out + r * stride)[q] = word;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+static int64_t sketch_capacity(oocgb_data d) {
+  if (d->n_global <= (1 << 20)) return d->n_local;
+  double mu = (double)d->n_local * ((double)(1 << 20) / (double)d->n_global);
+  return (int64_t)(mu + 8.0 * sqrt(mu) + 1024.0);
+}
+
+void sketch_append(oocgb_data d, const float *dX, int64_t row0_global, int64_t n) {
+  oocgb_ctx c = d->ctx;
+  if (!d->d_sketch) {
+    d->sketch_cap = sketch_capacity(d);
+    d->d_sketch = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, d->sketch_cap) * d->m);
+    d->d_sketch_count = (unsigned long long *)dmalloc(sizeof(unsigned long long));
+    OOCGB_CK(cudaMemsetAsync(d->d_sketch_count, 0, sizeof(unsigned long long), c->stream));
+    d->sketch_all_rows = d->n_global <= (1 << 20);
+  }
+  if (n <= 0) return;
+  int *d_err = (int *)c->d_small;
+  OOCGB_CK(cudaMemsetAsync(d_err, 0, sizeof(int), c->stream));
+  int blocks = (int)std::min<int64_t>((n + 7) / 8, (int64_t)c->num_sms * 16);
+  k_sketch_append<<<blocks, 256, 0, c->stream>>>(dX, n, d->m, row0_global, d->n_global, d->seed,
+                                                 d->sketch_all_rows, d->d_sketch, d->sketch_cap,
+                                                 d->d_sketch_count, d_err);
+  OOCGB_CK(cudaGetLastError());
+  int herr = 0;
+  OOCGB_CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  OOCGB_REQUIRE(herr != 2, OOCGB_ERR_ARG, "quantise: non-finite value in X (dense path, R4)");
+  OOCGB_REQUIRE(herr != 3, OOCGB_ERR_NOMEM, "quantise: sketch sample exceeded its capacity");
+}
+
+void cuts_finalize(oocgb_data d) {
+  oocgb_ctx c = d->ctx;
+  if (!d->d_sketch) sketch_append(d, nullptr, 0, 0);
+  unsigned long long n_local_sample = 0;
+  OOCGB_CK(cudaMemcpyAsync(&n_local_sample, d->d_sketch_count, sizeof(n_local_sample),
+                           cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  const int m = d->m;
+  uint32_t *rowmajor = d->d_sketch;
+  int64_t N = (int64_t)n_local_sample;
+  uint32_t *gathered = nullptr;
+  if (c->world > 1) {
+    // allgather the sketch sample: pad every rank to the max count with
+    // 0xFFFFFFFF keys (sort after every finite key) and drop them after sorting.
+    unsigned long long *d_cnt = (unsigned long long *)c->d_small;
+    OOCGB_CK(cudaMemcpyAsync(d_cnt, &n_local_sample, 8, cudaMemcpyHostToDevice, c->stream));
+    allreduce_max_u64(c, d_cnt, 1);
+    unsigned long long maxc = 0;
+    OOCGB_CK(cudaMemcpyAsync(&maxc, d_cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+    long long tot = (long long)n_local_sample;
+    long long *d_tot = (long long *)((char *)c->d_small + 64);
+    OOCGB_CK(cudaMemcpyAsync(d_tot, &tot, 8, cudaMemcpyHostToDevice, c->stream));
+    allreduce_sum_i64(c, d_tot, 1);
+    OOCGB_CK(cudaMemcpyAsync(&tot, d_tot, 8, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    uint32_t *padded = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<unsigned long long>(1, maxc) * m);
+    OOCGB_CK(cudaMemsetAsync(padded, 0xFF, sizeof(uint32_t) * (size_t)maxc * m, c->stream));
+    OOCGB_CK(cudaMemcpyAsync(padded, rowmajor, sizeof(uint32_t) * (size_t)n_local_sample * m,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    gathered = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<unsigned long long>(1, maxc) * m * c->world);
+    OOCGB_NCCL(ncclAllGather(padded, gathered, (size_t)maxc * m, ncclUint32, c->comm, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    dfree(padded);
+    rowmajor = gathered;
+    N = (int64_t)maxc * c->world;  // includes padding rows; trimmed per feature below
+    d->n_global = d->n_global;     // unchanged
+    // padding rows sort last; the true count per feature is `tot`
+    int64_t Ntrue = tot;
+    uint32_t *colmajor = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, N) * m);
+    dim3 tb(32, 8), tg((unsigned)((N + 31) / 32), (unsigned)((m + 31) / 32));
+    if (N > 0) k_transpose_keys<<<tg, tb, 0, c->stream>>>(rowmajor, N, m, colmajor);
+    OOCGB_CK(cudaGetLastError());
+    dfree(gathered);
+    // sort per feature, then extract with the true count (padding keys sit at the end)
+    uint32_t *sorted = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, N) * m);
+    std::vector<int> offs(m + 1);
+    for (int j = 0; j <= m; ++j) offs[j] = (int)(j * N);
+    int *d_offs = (int *)dmalloc(sizeof(int) * (m + 1));
+    OOCGB_CK(cudaMemcpyAsync(d_offs, offs.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice, c->stream));
+    size_t tmp = 0;
+    OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, colmajor, sorted, (int)(N * m), m,
+                                                     d_offs, d_offs + 1, 0, 32, c->stream));
+    void *d_tmp = dmalloc(std::max<size_t>(tmp, 16));
+    OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tmp, colmajor, sorted, (int)(N * m), m,
+                                                     d_offs, d_offs + 1, 0, 32, c->stream));
+    dfree(d_tmp);
+    dfree(colmajor);
+    // compact each feature's first Ntrue keys into [m][Ntrue]
+    uint32_t *trimmed = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, Ntrue) * m);
+    for (int j = 0; j < m; ++j)
+      OOCGB_CK(cudaMemcpyAsync(trimmed + (int64_t)j * Ntrue, sorted + (int64_t)j * N,
+                               sizeof(uint32_t) * (size_t)Ntrue, cudaMemcpyDeviceToDevice, c->stream));
+    dfree(sorted);
+    dfree(d_offs);
+    rowmajor = nullptr;
+    N = Ntrue;
+    // fall through to extraction with `trimmed` as the sorted column-major keys
+    float *d_cuts = (float *)dmalloc(sizeof(float) * (size_t)m * 256);
+    int *d_cnt2 = (int *)dmalloc(sizeof(int) * m);
+    k_extract_cuts<<<m, 256, 0, c->stream>>>(trimmed, N, d->max_bin, d_cuts, d_cnt2);
+    OOCGB_CK(cudaGetLastError());
+    std::vector<float> hc((size_t)m * 256);
+    std::vector<int> hn(m);
+    OOCGB_CK(cudaMemcpyAsync(hc.data(), d_cuts, sizeof(float) * hc.size(), cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaMemcpyAsync(hn.data(), d_cnt2, sizeof(int) * m, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    dfree(trimmed); dfree(d_cuts); dfree(d_cnt2);
+    d->h_cut_ptrs.assign(m + 1, 0);
+    d->h_cut_values.clear();
+    for (int j = 0; j < m; ++j) {
+      for (int k = 0; k < hn[j]; ++k) d->h_cut_values.push_back(hc[(size_t)j * 256 + k]);
+      d->h_cut_ptrs[j + 1] = (int)d->h_cut_values.size();
+    }
+  } else {
+    uint32_t *colmajor = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, N) * m);
+    dim3 tb(32, 8), tg((unsigned)((N + 31) / 32), (unsigned)((m + 31) / 32));
+    if (N > 0) k_transpose_keys<<<tg, tb, 0, c->stream>>>(rowmajor, N, m, colmajor);
+    OOCGB_CK(cudaGetLastError());
+    uint32_t *sorted = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, N) * m);
+    std::vector<int> offs(m + 1);
+    for (int j = 0; j <= m; ++j) offs[j] = (int)(j * N);
+    int *d_offs = (int *)dmalloc(sizeof(int) * (m + 1));
+    OOCGB_CK(cudaMemcpyAsync(d_offs, offs.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice, c->stream));
+    if (N > 0) {
+      size_t tmp = 0;
+      OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, colmajor, sorted, (int)(N * m), m,
+                                                       d_offs, d_offs + 1, 0, 32, c->stream));
+      void *d_tmp = dmalloc(std::max<size_t>(tmp, 16));
+      OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tmp, colmajor, sorted, (int)(N * m), m,
+                                                       d_offs, d_offs + 1, 0, 32, c->stream));
+      OOCGB_CK(cudaStreamSynchronize(c->stream));
+      dfree(d_tmp);
+    }
+    dfree(colmajor);
+    dfree(d_offs);
+    float *d_cuts = (float *)dmalloc(sizeof(float) * (size_t)m * 256);
+    int *d_cnt2 = (int *)dmalloc(sizeof(int) * m);
+    k_extract_cuts<<<m, 256, 0, c->stream>>>(sorted, N, d->max_bin, d_cuts, d_cnt2);
+    OOCGB_CK(cudaGetLastError());
+    std::vector<float> hc((size_t)m * 256);
+    std::vector<int> hn(m);
+    OOCGB_CK(cudaMemcpyAsync(hc.data(), d_cuts, sizeof(float) * hc.size(), cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaMemcpyAsync(hn.data(), d_cnt2, sizeof(int) * m, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    dfree(sorted); dfree(d_cuts); dfree(d_cnt2);
+    d->h_cut_ptrs.assign(m + 1, 0);
+    d->h_cut_values.clear();
+    for (int j = 0; j < m; ++j) {
+      for (int k = 0; k < hn[j]; ++k) d->h_cut_values.push_back(hc[(size_t)j * 256 + k]);
+      d->h_cut_ptrs[j + 1] = (int)d->h_cut_values.size();
+    }
+  }
+  dfree(d->d_sketch);
+  d->d_sketch = nullptr;
+  dfree(d->d_sketch_count);
+  d->d_sketch_count = nullptr;
+  d->d_cut_values = (float *)dmalloc(sizeof(float) * std::max<size_t>(1, d->h_cut_values.size()));
+  d->d_cut_ptrs = (int32_t *)dmalloc(sizeof(int32_t) * (m + 1));
+  OOCGB_CK(cudaMemcpyAsync(d->d_cut_values, d->h_cut_values.data(), sizeof(float) * d->h_cut_values.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+  OOCGB_CK(cudaMemcpyAsync(d->d_cut_ptrs, d->h_cut_ptrs.data(), sizeof(int32_t) * (m + 1),
+                           cudaMemcpyHostToDevice, c->stream));
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  d->cuts_ready = true;
+}
+
+void bin_rows(oocgb_data d, const float *dX, int64_t n, uint8_t *d_out, int *d_err) {
+  oocgb_ctx c = d->ctx;
+  if (n <= 0) return;
+  int64_t total = n * (d->stride / 4);
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)c->num_sms * 32);
+  k_bin_rows<<<blocks, 256, 0, c->stream>>>(dX, n, d->m, d->stride, d->d_cut_values, d->d_cut_ptrs,
+                                            d_out, d_err);
+  OOCGB_CK(cudaGetLastError());
+}
+
+}  // namespace oocgb

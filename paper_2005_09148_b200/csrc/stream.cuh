@@ -1,0 +1,52 @@
+// Out-of-core page streamer ("streamed ... via a multi-threaded
+// pre-fetcher", here pinned host -> HBM over PCIe): pages of the ELLPACK matrix live in pinned
+// host memory; fn(page_device_ptr, first_row, n_rows) consumes them on the ctx stream while the
+// next pages are copied on the copy stream into a ring of kStages device staging buffers.
+// Copy and compute are chained by events only — no host synchronisation inside the loop.
+#pragma once
+#include "internal.cuh"
+
+namespace oocgb {
+
+constexpr int kStages = 3;
+
+void ensure_staging(oocgb_data d);
+void record_copy_timing(oocgb_ctx c, cudaEvent_t a, cudaEvent_t b);
+cudaEvent_t pool_event(oocgb_ctx c);
+
+template <class F>
+void for_each_page(oocgb_data d, F fn) {
+  oocgb_ctx c = d->ctx;
+  ensure_staging(d);
+  static thread_local cudaEvent_t copy_done[kStages] = {}, consumed[kStages] = {};
+  static thread_local int inited = 0;
+  if (!inited) {
+    for (int i = 0; i < kStages; ++i) {
+      OOCGB_CK(cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming));
+      OOCGB_CK(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
+    }
+    inited = 1;
+  }
+  // the copy stream must not overwrite staging still used by earlier work on the ctx stream
+  OOCGB_CK(cudaEventRecord(consumed[0], c->stream));
+  for (int i = 0; i < kStages; ++i) OOCGB_CK(cudaStreamWaitEvent(c->copy_stream, consumed[0], 0));
+  for (int i = 1; i < kStages; ++i) OOCGB_CK(cudaEventRecord(consumed[i], c->stream));
+  const int64_t rpp = d->rows_per_page;
+  for (int64_t p = 0; p < d->n_pages; ++p) {
+    const int slot = (int)(p % kStages);
+    const int64_t r0 = p * rpp;
+    const int64_t nr = std::min<int64_t>(rpp, d->n_local - r0);
+    OOCGB_CK(cudaStreamWaitEvent(c->copy_stream, consumed[slot], 0));
+    cudaEvent_t ta = nullptr, tb = nullptr;
+    if (c->profiling) { ta = pool_event(c); tb = pool_event(c); OOCGB_CK(cudaEventRecord(ta, c->copy_stream)); }
+    OOCGB_CK(cudaMemcpyAsync(d->d_stage[slot], d->h_pages + r0 * d->stride, (size_t)nr * d->stride,
+                             cudaMemcpyHostToDevice, c->copy_stream));
+    if (c->profiling) { OOCGB_CK(cudaEventRecord(tb, c->copy_stream)); record_copy_timing(c, ta, tb); }
+    OOCGB_CK(cudaEventRecord(copy_done[slot], c->copy_stream));
+    OOCGB_CK(cudaStreamWaitEvent(c->stream, copy_done[slot], 0));
+    fn((const uint8_t *)d->d_stage[slot], r0, nr);
+    OOCGB_CK(cudaEventRecord(consumed[slot], c->stream));
+  }
+}
+
+}  // namespace oocgb

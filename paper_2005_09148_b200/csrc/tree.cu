@@ -1,0 +1,918 @@
+// Tree construction (Alg. 1) for sm_100a, depth-wise (R16):
+//   per level d:  k_hist (BuildHistograms, L174-175)      -> s32 partial histograms
+//                 [multi-GPU: k_reduce_partials + ncclAllReduce(int64), P:L188-190]
+//                 k_eval  (EvaluateSplit, L176-178; Eq. 8) -> per-(node, feature) best split,
+//                          sibling = parent - built (R17), parents kept for the next level
+//                 k_finalize (argmax over features, Eq. 6 leaf values, R13-R15)
+//                 k_part_flags / k_part_plan / k_part_scatter (RepartitionInstances, L172-173):
+//                          stable partition by one global scan; gradient pairs travel with rows
+// Everything stays on the device: one host sync per tree (the export).
+//
+// Histogram kernel design (measured in tools/microbench):
+//  * s32 shared accumulators in a bin-major layout [bin][32 features] (g plane, h plane), so
+//    the bank of (bin, f) is f.  Each lane owns one row and visits its 32 features rotated by
+//    its lane id (feature (lane + s) & 31 at step s): the 32 lanes of every atomic hit 32
+//    distinct banks -> conflict-free ATOMS at 1 warp-instruction/clk/SM (microbench: 4.57 T
+//    symbols/s on B200, vs 0.15 T with bin-driven random banks).
+//  * non-returning atomics: a chunk holds <= (2^31-1) >> quant_bits rows, so no s32 sum can
+//    overflow (|q| <= 2^quant_bits) and no carry handling is needed.
+//  * each (chunk, feature-group) item writes its s32 partial once (no zero-fill, no global
+//    atomics, deterministic); k_eval sums the partials of a node in int64.
+#include "internal.cuh"
+#include "stream.cuh"
+
+struct Work {
+  int64_t cap_rows = 0;
+  int max_depth = -1, m = 0, n_fg = 0;
+  int64_t items_cap = 0;
+  int32_t *ridx[2] = {nullptr, nullptr};
+  int2 *q[2] = {nullptr, nullptr};
+  uint32_t *flagbits = nullptr;
+  int *tile_cnt = nullptr;
+  int *tile_off = nullptr;
+  oocgb::Seg *segs[2] = {nullptr, nullptr};
+  int *bpart = nullptr, *seg_nr = nullptr, *seg_grb = nullptr;
+  long long *seg_cnt = nullptr;
+  oocgb::Pair *pairs = nullptr;
+  int *partial = nullptr;
+  long long *phist[2] = {nullptr, nullptr};
+  long long *built64 = nullptr;
+  oocgb::Cand *cand = nullptr;
+  oocgb::DNode *dnodes = nullptr;
+  oocgb::LevelCtl *ctl = nullptr;
+  long long *dbg = nullptr;
+  size_t dbg_bytes = 0;
+  int final_cur = 0;  // which ridx / segs buffer holds the final partition
+  int hist_grid = 0;
+};
+
+namespace oocgb {
+
+__device__ __forceinline__ int level_first(int d) { return (1 << d) - 1; }
+
+// Leaf weight (Eq. 6) and dequantised sums of a node from its exact fixed-point sums (R15).
+__device__ void node_fill(DNode &nd, long long Gq, long long Hq, double sg_inv, double sh_inv,
+                          double lambda, double eta, int *err) {
+  double g = __dmul_rn((double)Gq, sg_inv), h = __dmul_rn((double)Hq, sh_inv);
+  nd.Gq = Gq;
+  nd.Hq = Hq;
+  nd.sum_g = g;
+  nd.sum_h = h;
+  double den = __dadd_rn(h, lambda);
+  if (!(den > 0.0)) atomicExch(err, 1);
+  double w = __ddiv_rn(-g, den);
+  nd.leaf_value = __double2float_rn(__dmul_rn(eta, w));
+}
+
+__global__ void k_init_build(DNode *dn, int n_nodes, long long G, long long H, long long n_rows_global,
+                             double sg_inv, double sh_inv, double lambda, double eta, Seg *segs,
+                             Pair *pairs, LevelCtl *ctl, int n_sel, int n_fg, int target_items,
+                             int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
+                             const int2 *q_in, int2 *q_out, int ridx_mode) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  int nth = gridDim.x * blockDim.x;
+  for (int v = tid; v < n_nodes; v += nth) {
+    DNode nd{};
+    nd.feature = -2;
+    dn[v] = nd;
+  }
+  for (int i = tid; i < n_sel; i += nth) {
+    ridx[i] = (ridx_mode == 1) ? sel_rows[i] : i;  // 1: in-core sampled (bins of the full page)
+    q_out[i] = q_in[i];
+  }
+  if (tid == 0) {
+    DNode r{};
+    r.feature = -1;
+    r.n_rows = n_rows_global;
+    node_fill(r, G, H, sg_inv, sh_inv, lambda, eta, &ctl->error);
+    dn[0] = r;
+    segs[0] = Seg{0, n_sel, 0, 0};
+    long long cr = ((long long)n_sel * n_fg + target_items - 1) / target_items;
+    if (cr < 1024) cr = 1024;
+    if (cr > kmax) cr = kmax;
+    int nch = (int)((n_sel + cr - 1) / cr);
+    pairs[0] = Pair{-1, 0, -1, 0, n_sel, 0, nch, (int)cr};
+    ctl->n_pairs = max_depth > 0 ? 1 : 0;
+    ctl->n_items = max_depth > 0 ? nch * n_fg : 0;
+    ctl->n_segs = 1;
+    ctl->n_splits = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// BuildHistograms.  Persistent CTAs over items = (global chunk, feature group).
+__global__ void __launch_bounds__(kHistThreads, 3)
+k_hist(const uint8_t *__restrict__ bins, int stride, int m, int n_fg, const int32_t *__restrict__ ridx,
+       const int2 *__restrict__ q, const Pair *__restrict__ pairs, const LevelCtl *__restrict__ ctl,
+       int *__restrict__ partial) {
+  extern __shared__ int4 smem4[];
+  int *Gp = reinterpret_cast<int *>(smem4);
+  int *Hp = Gp + kBins * kFG;
+  const int n_items = ctl->n_items, n_pairs = ctl->n_pairs;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wq = lane >> 2, bq = (lane & 3) * 8;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int fg = item % n_fg, cg = item / n_fg;
+    int lo = 0, hi = n_pairs - 1;  // largest p with chunk_base <= cg
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (pairs[mid].chunk_base <= cg) lo = mid; else hi = mid - 1;
+    }
+    const Pair P = pairs[lo];
+    const int c = cg - P.chunk_base;
+    const int r0 = P.begin + c * P.chunk_rows;
+    const int r1 = min(P.begin + P.count, r0 + P.chunk_rows);
+    for (int i = threadIdx.x; i < 2 * kBins * kFG / 4; i += kHistThreads) smem4[i] = make_int4(0, 0, 0, 0);
+    __syncthreads();
+    const uint8_t *base = bins + fg * kFG;
+    const bool two = (fg * kFG + 16) < stride;
+    int k = r0 + threadIdx.x;
+    uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+    int2 qq = make_int2(0, 0);
+    if (k < r1) {
+      const uint4 *p4 = reinterpret_cast<const uint4 *>(base + (size_t)ridx[k] * stride);
+      a = __ldg(p4);
+      if (two) b = __ldg(p4 + 1);
+      qq = q[k];
+    }
+    while (k < r1) {
+      // prefetch the next row of this thread
+      const int kn = k + kHistThreads;
+      uint4 an = make_uint4(0, 0, 0, 0), bn = make_uint4(0, 0, 0, 0);
+      int2 qn = make_int2(0, 0);
+      if (kn < r1) {
+        const uint4 *p4 = reinterpret_cast<const uint4 *>(base + (size_t)ridx[kn] * stride);
+        an = __ldg(p4);
+        if (two) bn = __ldg(p4 + 1);
+        qn = q[kn];
+      }
+      // rotate the 32 symbols right by `lane` bytes: R byte s = symbol of feature (s + lane) & 31
+      uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t t[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = (wq & 1) ? w[(i + 1) & 7] : w[i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = (wq & 2) ? t[(i + 2) & 7] : t[i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = (wq & 4) ? w[(i + 4) & 7] : w[i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = __funnelshift_r(t[i], t[(i + 1) & 7], bq);
+#pragma unroll
+      for (int s = 0; s < 32; ++s) {
+        const uint32_t bin = (w[s >> 2] >> ((s & 3) * 8)) & 0xffu;
+        const uint32_t idx = (bin << 5) | ((uint32_t)(lane + s) & 31u);
+        atomicAdd(Gp + idx, qq.x);
+        atomicAdd(Hp + idx, qq.y);
+      }
+      a = an; b = bn; qq = qn; k = kn;
+    }
+    __syncthreads();
+    // flush: warp w owns bins [32w, 32w+32); lane l = feature l -> conflict-free reads; each lane
+    // writes its feature's 32 (g, h) pairs = 256 contiguous bytes of the [32][256][2] partial.
+    const int f = fg * kFG + lane;
+    for (int bb = warp; bb < kBins / 32; bb += kHistThreads / 32) {
+      int4 *dst = reinterpret_cast<int4 *>(partial + (((size_t)item * kFG + lane) * kBins + bb * 32) * 2);
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const int i0 = (bb * 32 + i) * kFG + lane, i1 = i0 + kFG;
+        int4 v = make_int4(Gp[i0], Hp[i0], Gp[i1], Hp[i1]);
+        if (f < m) dst[i >> 1] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Multi-GPU: sum a pair's s32 chunk partials into an int64 [pair][m][256][2] buffer that is
+// then all-reduced.  Thread per (pair, feature, bin).
+__global__ void k_reduce_partials(const int *__restrict__ partial, const Pair *__restrict__ pairs,
+                                  const LevelCtl *__restrict__ ctl, int m, int n_fg,
+                                  long long *__restrict__ out) {
+  const int n_pairs = ctl->n_pairs;
+  int64_t total = (int64_t)n_pairs * m * kBins;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int b = (int)(t % kBins);
+    int j = (int)((t / kBins) % m);
+    int p = (int)(t / ((int64_t)kBins * m));
+    const Pair P = pairs[p];
+    long long g = 0, h = 0;
+    for (int c = 0; c < P.n_chunks; ++c) {
+      size_t item = (size_t)(P.chunk_base + c) * n_fg + j / kFG;
+      const int2 v = reinterpret_cast<const int2 *>(partial)[(item * kFG + (j % kFG)) * kBins + b];
+      g += v.x;
+      h += v.y;
+    }
+    out[t * 2] = g;
+    out[t * 2 + 1] = h;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// EvaluateSplit: one warp per (pair, feature j); lane owns bins [8 lane, 8 lane + 8).
+struct EvalArgs {
+  int d, D, m, n_fg;
+  const Pair *pairs;
+  const LevelCtl *ctl;
+  const int *partial;
+  const long long *built64;   // non-null: multi-GPU all-reduced built histograms
+  const long long *phist_prev;
+  long long *phist_next;
+  long long *dbg;
+  const int *cut_ptrs;
+  DNode *dn;
+  Cand *cand;
+  double lambda, gamma, mcw, sg_inv, sh_inv;
+};
+
+__device__ __forceinline__ long long warp_excl_scan_ll(long long v, int lane, long long &total) {
+  long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  total = __shfl_sync(0xffffffffu, incl, 31);
+  return incl - v;
+}
+
+__device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const long long (&g)[8],
+                          const long long (&h)[8]) {
+  const int B = A.cut_ptrs[j + 1] - A.cut_ptrs[j];
+  const long long G = A.dn[node].Gq, H = A.dn[node].Hq;
+  long long lg = 0, lh = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { lg += g[i]; lh += h[i]; }
+  long long tg, th;
+  long long eg = warp_excl_scan_ll(lg, lane, tg);
+  long long eh = warp_excl_scan_ll(lh, lane, th);
+  const double gP = __dmul_rn((double)G, A.sg_inv), hP = __dmul_rn((double)H, A.sh_inv);
+  const double tP = __ddiv_rn(__dmul_rn(gP, gP), __dadd_rn(hP, A.lambda));
+  double best = 0.0;
+  int bbin = 0x7fffffff, have = 0;
+  long long bGL = 0, bHL = 0;
+  long long GL = eg, HL = eh;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    GL += g[i];
+    HL += h[i];
+    const int b = lane * 8 + i;
+    if (b <= B - 2) {
+      const long long GR = G - GL, HR = H - HL;
+      const double gl = __dmul_rn((double)GL, A.sg_inv), hl = __dmul_rn((double)HL, A.sh_inv);
+      const double gr = __dmul_rn((double)GR, A.sg_inv), hr = __dmul_rn((double)HR, A.sh_inv);
+      const double dl = __dadd_rn(hl, A.lambda), dr = __dadd_rn(hr, A.lambda);
+      if (hl >= A.mcw && hr >= A.mcw && dl > 0.0 && dr > 0.0) {
+        const double tL = __ddiv_rn(__dmul_rn(gl, gl), dl);
+        const double tR = __ddiv_rn(__dmul_rn(gr, gr), dr);
+        const double gain = __dsub_rn(__dmul_rn(0.5, __dsub_rn(__dadd_rn(tL, tR), tP)), A.gamma);
+        if (!have || gain > best) { have = 1; best = gain; bbin = b; bGL = GL; bHL = HL; }
+      }
+    }
+  }
+  // warp argmax: larger gain, then lower bin
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    double ob = __shfl_down_sync(0xffffffffu, best, o);
+    int obin = __shfl_down_sync(0xffffffffu, bbin, o);
+    int ohave = __shfl_down_sync(0xffffffffu, have, o);
+    long long oGL = __shfl_down_sync(0xffffffffu, bGL, o);
+    long long oHL = __shfl_down_sync(0xffffffffu, bHL, o);
+    bool take = ohave && (!have || ob > best || (ob == best && obin < bbin));
+    if (take) { best = ob; bbin = obin; have = ohave; bGL = oGL; bHL = oHL; }
+  }
+  if (lane == 0) {
+    const int slot = node - level_first(A.d);
+    Cand cd;
+    cd.gain = best;
+    cd.bin = bbin;
+    cd.valid = have;
+    cd.GL = bGL;
+    cd.HL = bHL;
+    A.cand[(size_t)slot * A.m + j] = cd;
+  }
+}
+
+__device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)[8], const long long (&h)[8]) {
+  longlong2 *d2 = reinterpret_cast<longlong2 *>(dst);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) d2[i] = make_longlong2(g[i], h[i]);
+}
+
+__global__ void __launch_bounds__(256) k_eval(EvalArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int p = (int)(wid / A.m), j = (int)(wid % A.m);
+  if (p >= A.ctl->n_pairs) return;
+  const Pair P = A.pairs[p];
+  long long g[8], h[8];
+  const size_t hsz = (size_t)A.m * kBins * 2;
+  if (A.built64) {
+    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.built64 + (size_t)p * hsz + ((size_t)j * kBins + lane * 8) * 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { longlong2 v = src[i]; g[i] = v.x; h[i] = v.y; }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { g[i] = 0; h[i] = 0; }
+    for (int c = 0; c < P.n_chunks; ++c) {
+      const size_t item = (size_t)(P.chunk_base + c) * A.n_fg + j / kFG;
+      const int4 *src = reinterpret_cast<const int4 *>(A.partial + ((item * kFG + (j % kFG)) * kBins + lane * 8) * 2);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int4 v = __ldg(src + i);
+        g[2 * i] += v.x; h[2 * i] += v.y; g[2 * i + 1] += v.z; h[2 * i + 1] += v.w;
+      }
+    }
+  }
+  const bool keep = A.d <= A.D - 2;
+  const int f_d = level_first(A.d);
+  if (keep) store_hist8(A.phist_next + (size_t)(P.built - f_d) * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
+  if (A.dbg) store_hist8(A.dbg + (size_t)P.built * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
+  eval_node(A, P.built, j, lane, g, h);
+  if (P.derived >= 0) {
+    const int ps = P.parent - level_first(A.d - 1);
+    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + ((size_t)j * kBins + lane * 8) * 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { longlong2 v = src[i]; g[i] = v.x - g[i]; h[i] = v.y - h[i]; }
+    if (keep) store_hist8(A.phist_next + (size_t)(P.derived - f_d) * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
+    if (A.dbg) store_hist8(A.dbg + (size_t)P.derived * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
+    eval_node(A, P.derived, j, lane, g, h);
+  }
+}
+
+// Split decision per node at depth d: argmax over features (ties: lowest feature, R13),
+// split iff gain > 0; children get their exact sums and Eq. 6 leaf values.
+__global__ void k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl,
+                           const Cand *__restrict__ cand, DNode *dn, const float *__restrict__ cut_values,
+                           const int *__restrict__ cut_ptrs, double sg_inv, double sh_inv,
+                           double lambda, double eta) {
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int p = wid >> 1;
+  if (p >= ctl->n_pairs) return;
+  const Pair P = pairs[p];
+  const int node = (wid & 1) ? P.derived : P.built;
+  if (node < 0) return;
+  const int slot = node - level_first(d);
+  double best = 0.0;
+  int have = 0, bj = 0x7fffffff, bb = 0;
+  long long GL = 0, HL = 0;
+  for (int j = lane; j < m; j += 32) {
+    const Cand cd = cand[(size_t)slot * m + j];
+    if (cd.valid && (!have || cd.gain > best)) { have = 1; best = cd.gain; bj = j; bb = cd.bin; GL = cd.GL; HL = cd.HL; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    double ob = __shfl_down_sync(0xffffffffu, best, o);
+    int oj = __shfl_down_sync(0xffffffffu, bj, o);
+    int obb = __shfl_down_sync(0xffffffffu, bb, o);
+    int oh = __shfl_down_sync(0xffffffffu, have, o);
+    long long oGL = __shfl_down_sync(0xffffffffu, GL, o);
+    long long oHL = __shfl_down_sync(0xffffffffu, HL, o);
+    bool take = oh && (!have || ob > best || (ob == best && oj < bj));
+    if (take) { best = ob; bj = oj; bb = obb; have = oh; GL = oGL; HL = oHL; }
+  }
+  if (lane == 0 && have && best > 0.0) {
+    DNode &nd = dn[node];
+    nd.feature = bj;
+    nd.split_bin = bb;
+    nd.split_value = cut_values[cut_ptrs[bj] + bb];
+    nd.gain = best;
+    DNode L{}, R{};
+    L.feature = -1;
+    R.feature = -1;
+    node_fill(L, GL, HL, sg_inv, sh_inv, lambda, eta, &ctl->error);
+    node_fill(R, nd.Gq - GL, nd.Hq - HL, sg_inv, sh_inv, lambda, eta, &ctl->error);
+    dn[2 * node + 1] = L;
+    dn[2 * node + 2] = R;
+    atomicAdd(&ctl->n_splits, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// RepartitionInstances: stable partition of every split segment, by one global scan of the
+// "goes right" flags (bin > split_bin).  For position i in segment s:
+//   rr  = #right in [begin_s, i)            left  -> i - rr
+//   nL  = count_s - #right in s             right -> begin_s + nL + rr
+__device__ __forceinline__ int seg_of(const Seg *segs, int n_segs, int i) {
+  int lo = 0, hi = n_segs - 1;  // last segment with begin <= i (non-empty one containing i)
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].begin <= i) lo = mid; else hi = mid - 1;
+  }
+  while (lo < n_segs - 1 && segs[lo].begin + segs[lo].count <= i) ++lo;
+  return lo;
+}
+
+__global__ void __launch_bounds__(kPartThreads)
+k_part_flags(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
+             const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, int stride,
+             const int32_t *__restrict__ ridx, uint32_t *__restrict__ flagbits, int *__restrict__ tile_cnt,
+             int *__restrict__ bpart) {
+  __shared__ uint32_t s_words[kPartTile / 32];
+  const int n_segs = ctl->n_segs;
+  const int t0 = blockIdx.x * kPartTile;
+  const int p0 = t0 + threadIdx.x * 8;
+  uint32_t bits = 0;
+  if (p0 < n) {
+    int s = seg_of(segs, n_segs, p0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = p0 + k;
+      if (i >= n) break;
+      while (segs[s].begin + segs[s].count <= i) ++s;
+      const DNode &nd = dn[segs[s].node];
+      if (nd.feature >= 0) {
+        const uint8_t b = bins[(size_t)ridx[i] * stride + nd.feature];
+        bits |= (uint32_t)(b > nd.split_bin) << k;
+      }
+    }
+  }
+  reinterpret_cast<uint8_t *>(s_words)[threadIdx.x] = (uint8_t)bits;
+  __syncthreads();
+  const int nw = kPartTile / 32;
+  if (threadIdx.x < nw) flagbits[(size_t)blockIdx.x * nw + threadIdx.x] = s_words[threadIdx.x];
+  int c = __popc(bits);
+  for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  __shared__ int s_red[kPartThreads / 32];
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kPartThreads / 32; ++w) t += s_red[w];
+    tile_cnt[blockIdx.x] = t;
+  }
+  // boundary partials for segments beginning inside this tile
+  const int t1 = min(n, t0 + kPartTile);
+  int lo = 0, hi = n_segs;  // first segment with begin >= t0
+  while (lo < hi) { int mid = (lo + hi) >> 1; if (segs[mid].begin < t0) lo = mid + 1; else hi = mid; }
+  for (int s = lo + threadIdx.x; s < n_segs && segs[s].begin < t1; s += blockDim.x) {
+    const int off = segs[s].begin - t0;
+    int r = 0;
+    for (int w = 0; w < (off >> 5); ++w) r += __popc(s_words[w]);
+    if (off & 31) r += __popc(s_words[off >> 5] & ((1u << (off & 31)) - 1u));
+    bpart[s] = r;
+  }
+}
+
+// Block-wide exclusive scan (blockDim.x == 1024).  Returns the exclusive prefix of v and
+// writes the block total to *total.  Contains __syncthreads(); call from all threads.
+__device__ int block_excl_scan(int v, int *total) {
+  __shared__ int s_w[32];
+  __shared__ int s_tot;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) s_w[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    int x = lane < nw ? s_w[lane] : 0, xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += u;
+    }
+    if (lane < nw) s_w[lane] = xi - x;
+    if (lane == 31) s_tot = xi;
+  }
+  __syncthreads();
+  const int r = s_w[w] + incl - v;
+  *total = s_tot;
+  __syncthreads();
+  return r;
+}
+
+// Single block, phase 1: tile scan, per-segment right counts (local), children row counts.
+// seg_cnt[2s], seg_cnt[2s+1] = (left, right) rows of segment s; all-reduced across ranks
+// between phase 1 and phase 2 when world > 1 (so every rank picks the same built child).
+__global__ void __launch_bounds__(1024)
+k_part_plan1(int n, int n_tiles, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
+             const int *__restrict__ tile_cnt, int *__restrict__ tile_off, const int *__restrict__ bpart,
+             int *__restrict__ seg_nr, int *__restrict__ seg_grb, long long *__restrict__ seg_cnt) {
+  const int T = blockDim.x;
+  int carry = 0;
+  for (int base = 0; base < n_tiles; base += T) {
+    const int i = base + threadIdx.x;
+    const int v = i < n_tiles ? tile_cnt[i] : 0;
+    int tot;
+    const int e = block_excl_scan(v, &tot);
+    if (i < n_tiles) tile_off[i] = carry + e;
+    carry += tot;
+  }
+  const int total_right = carry;
+  const int n_segs = ctl->n_segs;
+  for (int s = threadIdx.x; s < n_segs; s += T) {
+    const int b = segs[s].begin;
+    seg_grb[s] = (b >= n) ? total_right : (tile_off[b / kPartTile] + bpart[s]);
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < n_segs; s += T) {
+    const int e = (s + 1 < n_segs) ? seg_grb[s + 1] : total_right;
+    const int nr = e - seg_grb[s];
+    seg_nr[s] = nr;
+    seg_cnt[2 * s] = segs[s].count - nr;
+    seg_cnt[2 * s + 1] = nr;
+  }
+}
+
+// Single block, phase 2: children n_rows (global counts), next level's segments (split -> 2,
+// leaf -> pass-through 1) and sibling pairs (built = child with fewer global rows, ties
+// left, R17), histogram chunking.  Saves the old segment count for k_part_scatter.
+__global__ void __launch_bounds__(1024)
+k_part_plan2(const Seg *__restrict__ segs, Seg *__restrict__ segs_next, LevelCtl *ctl, DNode *dn,
+             const int *__restrict__ seg_nr, const long long *__restrict__ seg_cnt, Pair *__restrict__ pairs,
+             int n_fg, int target_items, int kmax) {
+  const int T = blockDim.x;
+  const int n_segs = ctl->n_segs;
+  int nseg_carry = 0, npair_carry = 0;
+  long long rows_local = 0;
+  for (int base = 0; base < n_segs; base += T) {
+    const int s = base + threadIdx.x;
+    int split = 0;
+    if (s < n_segs) split = dn[segs[s].node].feature >= 0;
+    int tot_s, tot_p;
+    const int es = block_excl_scan(s < n_segs ? 1 + split : 0, &tot_s);
+    const int ep = block_excl_scan(split, &tot_p);
+    if (s < n_segs) {
+      const Seg S = segs[s];
+      const int ns = nseg_carry + es, np = npair_carry + ep;
+      if (split) {
+        const int nr = seg_nr[s], nl = S.count - nr;
+        const long long gl = seg_cnt[2 * s], gr = seg_cnt[2 * s + 1];
+        dn[2 * S.node + 1].n_rows = gl;
+        dn[2 * S.node + 2].n_rows = gr;
+        segs_next[ns] = Seg{S.begin, nl, 2 * S.node + 1, 0};
+        segs_next[ns + 1] = Seg{S.begin + nl, nr, 2 * S.node + 2, 0};
+        Pair pr;
+        pr.parent = S.node;
+        if (gl <= gr) { pr.built = 2 * S.node + 1; pr.derived = 2 * S.node + 2; pr.begin = S.begin; pr.count = nl; }
+        else { pr.built = 2 * S.node + 2; pr.derived = 2 * S.node + 1; pr.begin = S.begin + nl; pr.count = nr; }
+        pr.chunk_base = 0; pr.n_chunks = 0; pr.chunk_rows = 0;
+        pairs[np] = pr;
+        rows_local += pr.count;
+      } else {
+        segs_next[ns] = S;
+      }
+    }
+    nseg_carry += tot_s;
+    npair_carry += tot_p;
+  }
+  // chunk size: about target_items items per level, within [1024, kmax] rows (s32 bound)
+  __shared__ unsigned long long s_rows;
+  if (threadIdx.x == 0) s_rows = 0;
+  __syncthreads();
+  atomicAdd(&s_rows, (unsigned long long)rows_local);
+  __syncthreads();
+  long long cr = ((long long)s_rows * n_fg + target_items - 1) / target_items;
+  if (cr < 1024) cr = 1024;
+  if (cr > kmax) cr = kmax;
+  const int n_pairs = npair_carry;
+  int chunk_carry = 0;
+  for (int base = 0; base < n_pairs; base += T) {
+    const int p = base + threadIdx.x;
+    const int nch = p < n_pairs ? (int)((pairs[p].count + cr - 1) / cr) : 0;
+    int tot;
+    const int e = block_excl_scan(nch, &tot);
+    if (p < n_pairs) {
+      pairs[p].chunk_base = chunk_carry + e;
+      pairs[p].n_chunks = nch;
+      pairs[p].chunk_rows = (int)cr;
+    }
+    chunk_carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    ctl->pad[0] = n_segs;  // segment count of the level being scattered
+    ctl->n_pairs = n_pairs;
+    ctl->n_items = chunk_carry * n_fg;
+    ctl->n_segs = nseg_carry;
+    ctl->n_splits = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kPartThreads)
+k_part_scatter(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
+               const uint32_t *__restrict__ flagbits, const int *__restrict__ tile_off,
+               const int *__restrict__ seg_nr, const int *__restrict__ seg_grb,
+               const int32_t *__restrict__ ridx, const int2 *__restrict__ q, int32_t *__restrict__ ridx_out,
+               int2 *__restrict__ q_out) {
+  __shared__ uint32_t s_words[kPartTile / 32];
+  const int nw = kPartTile / 32;
+  const int t0 = blockIdx.x * kPartTile;
+  if (threadIdx.x < nw) s_words[threadIdx.x] = flagbits[(size_t)blockIdx.x * nw + threadIdx.x];
+  __syncthreads();
+  const int n_segs = ctl->pad[0];
+  const int p0 = t0 + threadIdx.x * 8;
+  if (p0 >= n) return;
+  // rights in this tile before p0
+  const int off = threadIdx.x * 8;
+  int r = 0;
+  for (int w = 0; w < (off >> 5); ++w) r += __popc(s_words[w]);
+  if (off & 31) r += __popc(s_words[off >> 5] & ((1u << (off & 31)) - 1u));
+  const uint32_t bits = (s_words[off >> 5] >> (off & 31)) & 0xffu;
+  int gr = tile_off[blockIdx.x] + r;  // global right rank at p0
+  int s = seg_of(segs, n_segs, p0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = p0 + k;
+    if (i >= n) break;
+    while (segs[s].begin + segs[s].count <= i) ++s;
+    const Seg S = segs[s];
+    const int rr = gr - seg_grb[s];
+    const int right = (bits >> k) & 1;
+    int pos;
+    if (right) pos = S.begin + (S.count - seg_nr[s]) + rr;
+    else pos = i - rr;
+    ridx_out[pos] = ridx[i];
+    q_out[pos] = q[i];
+    gr += right;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Prediction (Eq. 1): margin[row] += leaf(tree, bins_row), binned traversal, per tree in order.
+__global__ void k_predict(const uint8_t *__restrict__ bins, int stride, int64_t n,
+                          const PNode *const *__restrict__ trees, int n_trees, float *__restrict__ margin) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float mg = margin[i];
+    const uint8_t *row = bins + i * stride;
+    for (int t = 0; t < n_trees; ++t) {
+      const PNode *nd = trees[t];
+      int v = 0;
+      while (nd[v].feature >= 0) v = (row[nd[v].feature] <= nd[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
+      mg = mg + nd[v].leaf;
+    }
+    margin[i] = mg;
+  }
+}
+
+// margin[row] += leaf of the row's final segment (in-core, all rows selected).
+__global__ void k_update_margin(int n, const Seg *__restrict__ segs, int n_segs, const DNode *__restrict__ dn,
+                                const int32_t *__restrict__ ridx, float *__restrict__ margin) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = seg_of(segs, n_segs, i);
+  margin[ridx[i]] = margin[ridx[i]] + dn[segs[s].node].leaf_value;
+}
+
+__global__ void k_leaf_of_pos(int n, const Seg *__restrict__ segs, int n_segs, const int32_t *__restrict__ ridx,
+                              int32_t *__restrict__ out_row, int32_t *__restrict__ out_leaf) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int s = seg_of(segs, n_segs, i);
+  out_row[i] = ridx[i];
+  out_leaf[i] = segs[s].node;
+}
+
+// ---------------------------------------------------------------------------------------------
+static void ensure_work(oocgb_data d, int D) {
+  oocgb_ctx c = d->ctx;
+  Work *&w = d->work;
+  const int m = d->m;
+  const int n_fg = (m + kFG - 1) / kFG;
+  const int64_t n = std::max<int64_t>(1, d->n_sel);
+  const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
+  const int hist_grid = c->num_sms * 3;
+  const int target = 2 * hist_grid;
+  const int64_t max_pairs = D > 0 ? (1LL << (D - 1)) : 1;
+  int64_t items = std::max<int64_t>(target, (int64_t)n_fg * ((n + kmax - 1) / kmax)) + (int64_t)n_fg * (1 + max_pairs) + n_fg;
+  if (w && w->cap_rows >= n && w->max_depth >= D && w->m == m && w->items_cap >= items) return;
+  free_work(d);
+  w = new Work();
+  w->cap_rows = n;
+  w->max_depth = D;
+  w->m = m;
+  w->n_fg = n_fg;
+  w->items_cap = items;
+  w->hist_grid = hist_grid;
+  const int64_t tiles = (n + kPartTile - 1) / kPartTile;
+  const int64_t max_segs = 1LL << std::max(D, 1);
+  for (int i = 0; i < 2; ++i) {
+    w->ridx[i] = (int32_t *)dmalloc(sizeof(int32_t) * n);
+    w->q[i] = (int2 *)dmalloc(sizeof(int2) * n);
+    w->segs[i] = (Seg *)dmalloc(sizeof(Seg) * max_segs);
+  }
+  w->flagbits = (uint32_t *)dmalloc(sizeof(uint32_t) * tiles * (kPartTile / 32));
+  w->tile_cnt = (int *)dmalloc(sizeof(int) * tiles);
+  w->tile_off = (int *)dmalloc(sizeof(int) * tiles);
+  w->bpart = (int *)dmalloc(sizeof(int) * max_segs);
+  w->seg_nr = (int *)dmalloc(sizeof(int) * max_segs);
+  w->seg_grb = (int *)dmalloc(sizeof(int) * max_segs);
+  w->seg_cnt = (long long *)dmalloc(sizeof(long long) * 2 * max_segs);
+  w->pairs = (Pair *)dmalloc(sizeof(Pair) * max_pairs);
+  w->partial = (int *)dmalloc((size_t)items * kFG * kBins * 2 * sizeof(int));
+  const size_t hsz = (size_t)m * kBins * 2;
+  const int64_t pslots = D >= 2 ? (1LL << (D - 2)) : 1;
+  for (int i = 0; i < 2; ++i) w->phist[i] = (long long *)dmalloc(sizeof(long long) * hsz * pslots);
+  if (c->world > 1) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * max_pairs);
+  w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)max_pairs * 2 * m);
+  w->dnodes = (DNode *)dmalloc(sizeof(DNode) * ((1LL << (D + 1)) - 1));
+  w->ctl = (LevelCtl *)dmalloc(sizeof(LevelCtl));
+  OOCGB_CK(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem));
+}
+
+void free_work(oocgb_data d) {
+  Work *w = d->work;
+  if (!w) return;
+  for (int i = 0; i < 2; ++i) { dfree(w->ridx[i]); dfree(w->q[i]); dfree(w->segs[i]); dfree(w->phist[i]); }
+  dfree(w->flagbits); dfree(w->tile_cnt); dfree(w->tile_off); dfree(w->bpart); dfree(w->seg_nr);
+  dfree(w->seg_grb); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
+  dfree(w->cand); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg);
+  delete w;
+  d->work = nullptr;
+}
+
+oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double mcw, double eta,
+                      bool keep_debug) {
+  oocgb_ctx c = d->ctx;
+  PhaseTimer whole(c, 6);
+  ensure_work(d, D);
+  Work *w = d->work;
+  const int m = d->m, n_fg = w->n_fg;
+  const int n = (int)d->n_sel;
+  const int n_nodes = (1 << (D + 1)) - 1;
+  const double sg_inv = ldexp(1.0, -d->e_g), sh_inv = ldexp(1.0, -d->e_h);
+  const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
+  const int target = 2 * w->hist_grid;
+  const size_t hsz = (size_t)m * kBins * 2;
+  const uint8_t *bins;
+  int ridx_mode;
+  if (d->placement == OOCGB_PLACE_PINNED_HOST) { bins = d->d_sampled_page; ridx_mode = 0; }
+  else { bins = d->d_bins; ridx_mode = d->all_selected ? 0 : 1; }
+  if (keep_debug) {
+    size_t need = sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1);
+    if (w->dbg_bytes < need) { dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
+    OOCGB_CK(cudaMemsetAsync(w->dbg, 0, need, c->stream));
+  }
+  OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
+  k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
+      w->dnodes, n_nodes, d->G_root, d->H_root, d->n_sel_global, sg_inv, sh_inv, lambda, eta,
+      w->segs[0], w->pairs, w->ctl, n, n_fg, target, kmax, D, d->d_sel_rows, w->ridx[0], d->d_q,
+      w->q[0], ridx_mode);
+  OOCGB_CK(cudaGetLastError());
+  int cur = 0;
+  const int tiles = (n + kPartTile - 1) / kPartTile;
+  double hist_bytes = 0.0;
+  for (int lv = 0; lv < D; ++lv) {
+    const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
+    {
+      PhaseTimer t(c, 0);
+      k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, d->stride, m, n_fg, w->ridx[cur],
+                                                                   w->q[cur], w->pairs, w->ctl, w->partial);
+      OOCGB_CK(cudaGetLastError());
+    }
+    if (c->world > 1) {
+      int64_t tot = (int64_t)max_pairs * m * kBins;
+      k_reduce_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
+          w->partial, w->pairs, w->ctl, m, n_fg, w->built64);
+      allreduce_sum_i64(c, w->built64, hsz * max_pairs);
+    }
+    {
+      PhaseTimer t(c, 1);
+      EvalArgs A;
+      A.d = lv; A.D = D; A.m = m; A.n_fg = n_fg;
+      A.pairs = w->pairs; A.ctl = w->ctl; A.partial = w->partial;
+      A.built64 = c->world > 1 ? w->built64 : nullptr;
+      A.phist_prev = w->phist[(lv + 1) & 1];
+      A.phist_next = w->phist[lv & 1];
+      A.dbg = keep_debug ? w->dbg : nullptr;
+      A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
+      A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.sg_inv = sg_inv; A.sh_inv = sh_inv;
+      int64_t warps = (int64_t)max_pairs * m;
+      k_eval<<<(unsigned)((warps + 7) / 8), 256, 0, c->stream>>>(A);
+      OOCGB_CK(cudaGetLastError());
+      k_finalize<<<(unsigned)((max_pairs * 2 + 7) / 8), 256, 0, c->stream>>>(
+          lv, m, w->pairs, w->ctl, w->cand, w->dnodes, d->d_cut_values, d->d_cut_ptrs, sg_inv, sh_inv,
+          lambda, eta);
+      OOCGB_CK(cudaGetLastError());
+    }
+    {
+      PhaseTimer t(c, 2);
+      if (n > 0) {
+        k_part_flags<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, d->stride,
+                                                            w->ridx[cur], w->flagbits, w->tile_cnt, w->bpart);
+        OOCGB_CK(cudaGetLastError());
+      }
+      k_part_plan1<<<1, 1024, 0, c->stream>>>(n, tiles, w->segs[cur], w->ctl, w->tile_cnt, w->tile_off,
+                                              w->bpart, w->seg_nr, w->seg_grb, w->seg_cnt);
+      OOCGB_CK(cudaGetLastError());
+      if (c->world > 1) allreduce_sum_i64(c, w->seg_cnt, 2 * (size_t)(1 << lv));
+      k_part_plan2<<<1, 1024, 0, c->stream>>>(w->segs[cur], w->segs[cur ^ 1], w->ctl, w->dnodes, w->seg_nr,
+                                              w->seg_cnt, w->pairs, n_fg, target, kmax);
+      OOCGB_CK(cudaGetLastError());
+      if (n > 0) {
+        k_part_scatter<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->flagbits,
+                                                              w->tile_off, w->seg_nr, w->seg_grb,
+                                                              w->ridx[cur], w->q[cur], w->ridx[cur ^ 1],
+                                                              w->q[cur ^ 1]);
+        OOCGB_CK(cudaGetLastError());
+      }
+    }
+    cur ^= 1;
+  }
+  w->final_cur = cur;
+  // export
+  std::vector<DNode> hn(n_nodes);
+  LevelCtl hctl;
+  OOCGB_CK(cudaMemcpyAsync(hn.data(), w->dnodes, sizeof(DNode) * n_nodes, cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaMemcpyAsync(&hctl, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  OOCGB_REQUIRE(hctl.error == 0, OOCGB_ERR_ARG, "build_tree: H + lambda <= 0 at a node (S:L406)");
+  oocgb_tree t = new oocgb_tree_s();
+  t->owner = d;
+  t->serial = ++d->tree_serial;
+  t->max_depth = D;
+  t->nodes.resize(n_nodes);
+  std::vector<PNode> pn(n_nodes);
+  for (int v = 0; v < n_nodes; ++v) {
+    oocgb_node &o = t->nodes[v];
+    o.feature = hn[v].feature;
+    o.split_bin = hn[v].split_bin;
+    o.split_value = hn[v].split_value;
+    o.leaf_value = hn[v].leaf_value;
+    o.gain = hn[v].gain;
+    o.sum_g = hn[v].sum_g;
+    o.sum_h = hn[v].sum_h;
+    o.n_rows = hn[v].n_rows;
+    if (o.feature == -2) { o.split_bin = 0; o.split_value = 0; o.leaf_value = 0; o.gain = 0; o.sum_g = 0; o.sum_h = 0; o.n_rows = 0; }
+    if (o.feature == -1) { o.split_bin = 0; o.split_value = 0; o.gain = 0; }
+    pn[v] = PNode{o.feature, o.split_bin, o.leaf_value, 0};
+  }
+  t->d_pnodes = (PNode *)dmalloc(sizeof(PNode) * n_nodes);
+  OOCGB_CK(cudaMemcpyAsync(t->d_pnodes, pn.data(), sizeof(PNode) * n_nodes, cudaMemcpyHostToDevice, c->stream));
+  if (keep_debug) {
+    t->debug = true;
+    size_t cnt = hsz * (size_t)std::max(0, (1 << D) - 1);
+    t->hist.resize(cnt);
+    if (cnt) OOCGB_CK(cudaMemcpyAsync(t->hist.data(), w->dbg, sizeof(long long) * cnt, cudaMemcpyDeviceToHost, c->stream));
+    // final partition: position -> (row index, leaf)
+    LevelCtl h2;
+    OOCGB_CK(cudaMemcpyAsync(&h2, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    int32_t *d_rows = (int32_t *)dmalloc(sizeof(int32_t) * std::max(1, n));
+    int32_t *d_leaf = (int32_t *)dmalloc(sizeof(int32_t) * std::max(1, n));
+    if (n > 0)
+      k_leaf_of_pos<<<(n + 255) / 256, 256, 0, c->stream>>>(n, w->segs[cur], D > 0 ? h2.n_segs : 1, w->ridx[cur],
+                                                             d_rows, d_leaf);
+    std::vector<int32_t> rows(n), leaf(n);
+    if (n > 0) {
+      OOCGB_CK(cudaMemcpyAsync(rows.data(), d_rows, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+      OOCGB_CK(cudaMemcpyAsync(leaf.data(), d_leaf, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    }
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    dfree(d_rows);
+    dfree(d_leaf);
+    // row index -> selected order
+    t->leaf_of_row.assign(n, -1);
+    if (ridx_mode == 1) {
+      std::vector<int32_t> sel(n);
+      if (n) OOCGB_CK(cudaMemcpy(sel.data(), d->d_sel_rows, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) {
+        int k = (int)(std::lower_bound(sel.begin(), sel.end(), rows[i]) - sel.begin());
+        t->leaf_of_row[k] = leaf[i];
+      }
+    } else {
+      for (int i = 0; i < n; ++i) t->leaf_of_row[rows[i]] = leaf[i];
+    }
+  }
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  return t;
+}
+
+void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t n_rows, int64_t row_offset,
+                    const oocgb_tree *trees, int n_trees, float *d_margin) {
+  oocgb_ctx c = d->ctx;
+  if (n_rows <= 0 || n_trees <= 0) return;
+  std::vector<const PNode *> ptrs(n_trees);
+  for (int t = 0; t < n_trees; ++t) ptrs[t] = trees[t]->d_pnodes;
+  const PNode **d_ptrs = (const PNode **)((char *)c->d_small + (768 << 10));
+  OOCGB_REQUIRE(n_trees <= 4096, OOCGB_ERR_ARG, "predict: at most 4096 trees per call");
+  OOCGB_CK(cudaMemcpyAsync(d_ptrs, ptrs.data(), sizeof(void *) * n_trees, cudaMemcpyHostToDevice, c->stream));
+  int blocks = (int)std::min<int64_t>((n_rows + 255) / 256, (int64_t)c->num_sms * 16);
+  k_predict<<<blocks, 256, 0, c->stream>>>(d_bins, d->stride, n_rows, d_ptrs, n_trees, d_margin + row_offset);
+  OOCGB_CK(cudaGetLastError());
+}
+
+void update_margin(oocgb_data d, oocgb_tree t, float *d_margin) {
+  oocgb_ctx c = d->ctx;
+  Work *w = d->work;
+  OOCGB_REQUIRE(w && t->serial == d->tree_serial && d->all_selected && d->placement == OOCGB_PLACE_DEVICE,
+                OOCGB_ERR_STATE, "update_margin: needs the latest tree of an in-core, f = 1 sample");
+  const int n = (int)d->n_sel;
+  LevelCtl h;
+  OOCGB_CK(cudaMemcpyAsync(&h, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  const int n_segs = t->max_depth > 0 ? h.n_segs : 1;
+  if (n > 0)
+    k_update_margin<<<(n + 255) / 256, 256, 0, c->stream>>>(n, w->segs[w->final_cur], n_segs, w->dnodes,
+                                                            w->ridx[w->final_cur], d_margin);
+  OOCGB_CK(cudaGetLastError());
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace oocgb

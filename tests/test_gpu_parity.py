@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star): bit-exact cut points, bin indices, sampled row sets and their
+fixed-point gradients, histograms, partitions and chosen splits; gains and leaf weights are
+in fact bit-exact too (same IEEE operation order, R14) and are checked with == and, as the
+stated bar, rel. error <= 1e-6; AUC after training within 1e-3 relative.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ob = pytest.importorskip("paper_2005_09148_b200")
+
+
+def _oracle_cuts_bins(X, max_bin, seed=2):
+    cv, cp = oracle.cuts(X, max_bin, seed=seed)
+    return cv, cp, oracle.bins(X, cv, cp)
+
+
+SHAPES = [
+    (1, 1, 256), (7, 3, 2), (100, 17, 16), (1000, 33, 256), (2049, 20, 256), (5000, 64, 64),
+    (10000, 20, 256),  # config 1 shape
+]
+
+
+@pytest.mark.parametrize("n,m,max_bin", SHAPES)
+@pytest.mark.parametrize("stress", [False, True])
+def test_cuts_and_bins_bit_exact(ctx, n, m, max_bin, stress):
+    if m < 4 and stress:
+        pytest.skip("stress needs >= 4 features")
+    if n >= 50 and m >= 2:
+        X, _ = synth.make_classification(n, m, seed=n + m, stress=stress)
+    else:
+        X = np.random.default_rng(0).normal(size=(n, m)).astype(np.float32)
+    cv, cp, B = _oracle_cuts_bins(X, max_bin)
+    d = ctx.quantise(X, max_bin)
+    gv, gp = d.get_cuts()
+    np.testing.assert_array_equal(gp, cp)
+    assert gv.tobytes() == cv.tobytes()
+    np.testing.assert_array_equal(d.get_bins(), B)
+    d.close()
+
+
+def test_cuts_negative_zero_and_ties(ctx):
+    X = np.array([[-0.0, 1.0], [0.0, 1.0], [2.0, 1.0], [-1.0, 1.0]] * 10, np.float32)
+    cv, cp, B = _oracle_cuts_bins(X, 256)
+    d = ctx.quantise(X, 256)
+    gv, gp = d.get_cuts()
+    assert gv.tobytes() == cv.tobytes()
+    np.testing.assert_array_equal(d.get_bins(), B)
+    d.close()
+
+
+def test_nonfinite_rejected(ctx):
+    X = np.ones((10, 3), np.float32)
+    X[4, 1] = np.nan
+    with pytest.raises(ob.OocgbError) as e:
+        ctx.quantise(X, 256)
+    assert e.value.status == ob.ERR_ARG
+
+
+def test_sketch_sample_large_n(ctx):
+    """n_global > 2^20: the sketch is the Philox row sample (R2), independent of pushing order."""
+    n, m = (1 << 20) + 4096, 4
+    rng = np.random.default_rng(5)
+    X = rng.normal(size=(n, m)).astype(np.float32)
+    X[:, 3] = np.round(X[:, 3] * 3)  # few distinct values
+    cv, cp = oracle.cuts(X, 256, seed=9)
+    d = ctx.sketch_begin(m, 256, n, seed=9)
+    half = n // 2
+    d.sketch_push(X[half:], half)  # reverse order on purpose
+    d.sketch_push(X[:half], 0)
+    d.cuts_finalize()
+    d.pages_push(X[:half], 0)
+    d.pages_push(X[half:], half)
+    gv, gp = d.get_cuts()
+    np.testing.assert_array_equal(gp, cp)
+    assert gv.tobytes() == cv.tobytes()
+    idx = rng.integers(0, n, size=5000)
+    np.testing.assert_array_equal(d.get_bins()[idx], oracle.bins(X[idx], cv, cp))
+    d.close()
+
+
+# ------------------------------------------------------------------------------------------ sampling
+@pytest.mark.parametrize("mode,ratio", [(0, 1.0), (1, 0.5), (1, 0.1), (2, 0.1), (2, 0.3), (2, 0.5), (2, 1.0)])
+@pytest.mark.parametrize("kind", ["logistic", "wide", "ties"])
+@pytest.mark.parametrize("n", [1, 777, 20000])
+def test_sample_bit_exact(ctx, mode, ratio, kind, n):
+    X = np.zeros((n, 2), np.float32)
+    X[:, 0] = np.arange(n)
+    g, h = synth.gradient_pairs(n, seed=n + mode, kind=kind)
+    d = ctx.quantise(X, 16)
+    d.set_gradients(g, h)
+    info = d.sample(mode, ratio, mvs_lambda=1.0, seed=11, round=3, quant_bits=16)
+    s = oracle.sample(g, h, mode, ratio, 1.0, 11, 3)
+    sel = s["selected"].astype(bool)
+    qg, e_g = oracle.quantise(s["gs"][sel], 16)
+    qh, e_h = oracle.quantise(s["hs"][sel], 16)
+    assert info["n_selected_local"] == s["n_selected"]
+    gid, gq, hq = d.get_sample(info["n_selected_local"])
+    np.testing.assert_array_equal(gid, np.nonzero(sel)[0])
+    assert (info["e_g"], info["e_h"]) == (e_g, e_h)
+    np.testing.assert_array_equal(gq, qg)
+    np.testing.assert_array_equal(hq, qh)
+    if mode == 2 and not info["fallback_uniform"]:
+        assert info["k_star"] == s["k_star"]
+        assert info["mu"] == s["mu"]
+    d.close()
+
+
+# ------------------------------------------------------------------------------------------ trees
+def _oracle_tree(B, m, cv, cp, g, h, mode, ratio, depth, quant_bits=16, lam=1.0, gamma=0.0, mcw=1.0,
+                 eta=0.1, seed=1, round_=0):
+    s = oracle.sample(g, h, mode, ratio, 1.0, seed, round_)
+    sel = s["selected"].astype(bool)
+    qg, e_g = oracle.quantise(s["gs"][sel], quant_bits)
+    qh, e_h = oracle.quantise(s["hs"][sel], quant_bits)
+    nodes, lor, hist = oracle.build_tree(B[sel], m, cv, cp, qg, qh, e_g, e_h, depth, lam, gamma, mcw, eta,
+                                         want_hist=True)
+    return nodes, lor, hist, sel
+
+
+def _compare_trees(gn, on):
+    assert gn.shape == on.shape
+    for f in ("feature", "split_bin", "n_rows"):
+        np.testing.assert_array_equal(gn[f], on[f], err_msg=f)
+    pres = on["feature"] != -2
+    sp = on["feature"] >= 0
+    np.testing.assert_array_equal(gn["split_value"][sp], on["split_value"][sp])
+    np.testing.assert_array_equal(gn["leaf_value"][pres], on["leaf_value"][pres])
+    # bars: rel <= 1e-6 (north_star); in fact bit-exact by construction (R14)
+    np.testing.assert_allclose(gn["gain"][sp], on["gain"][sp], rtol=1e-6)
+    np.testing.assert_array_equal(gn["gain"][sp], on["gain"][sp])
+    np.testing.assert_array_equal(gn["sum_g"][pres], on["sum_g"][pres])
+    np.testing.assert_array_equal(gn["sum_h"][pres], on["sum_h"][pres])
+
+
+TREE_CASES = [
+    # n, m, max_bin, depth, mode, ratio, stress
+    (1, 1, 256, 3, 0, 1.0, False),
+    (50, 3, 8, 4, 0, 1.0, False),
+    (3000, 20, 256, 6, 0, 1.0, False),
+    (10000, 20, 256, 6, 0, 1.0, False),   # config 1
+    (10000, 20, 256, 6, 0, 1.0, True),
+    (12345, 45, 64, 7, 2, 0.3, False),
+    (20000, 33, 256, 8, 1, 0.5, True),
+    (20000, 70, 256, 5, 2, 0.1, False),
+    (4096, 8, 256, 0, 0, 1.0, False),
+    (5000, 10, 256, 10, 0, 1.0, False),
+]
+
+
+@pytest.mark.parametrize("n,m,max_bin,depth,mode,ratio,stress", TREE_CASES)
+def test_tree_bit_exact(ctx, n, m, max_bin, depth, mode, ratio, stress):
+    if n >= 50:
+        X, y = synth.make_classification(n, max(m, 2), seed=7 + n, stress=stress and m >= 4)
+        X = np.ascontiguousarray(X[:, :m])
+    else:
+        rng = np.random.default_rng(n)
+        X = rng.normal(size=(n, m)).astype(np.float32)
+        y = (rng.random(n) < 0.5).astype(np.float32)
+    cv, cp, B = _oracle_cuts_bins(X, max_bin)
+    margin = np.random.default_rng(n).normal(scale=0.5, size=n).astype(np.float32)
+    g, h = oracle.logistic_grad(margin, y)
+    on, olor, ohist, sel = _oracle_tree(B, m, cv, cp, g, h, mode, ratio, depth)
+    d = ctx.quantise(X, max_bin)
+    d.set_gradients(g, h)
+    info = d.sample(mode, ratio, 1.0, 1, 0, 16)
+    t = d.build_tree(depth, 1.0, 0.0, 1.0, 0.1, keep_debug=True)
+    gn = t.export()
+    _compare_trees(gn, on)
+    # histograms of every present node with depth < D: bit-exact
+    for v in range((1 << depth) - 1):
+        if on["feature"][v] == -2:
+            continue
+        np.testing.assert_array_equal(t.get_histogram(v), ohist[v], err_msg=f"node {v}")
+    # partition: final node of every selected row, bit-exact
+    np.testing.assert_array_equal(t.get_partition(info["n_selected_local"]), olor)
+    # predict (binned traversal) == oracle predict, bit-exact float32
+    m0 = np.random.default_rng(1).normal(size=n).astype(np.float32)
+    gm = d.predict([t], m0.copy())
+    om = oracle.predict(B, on, m0)
+    np.testing.assert_array_equal(gm, om)
+    if mode == 0:
+        um = d.update_margin(t, m0.copy())
+        np.testing.assert_array_equal(um, om)
+    t.close()
+    d.close()
+
+
+def test_logistic_gradients_close(ctx):
+    n = 5000
+    rng = np.random.default_rng(3)
+    margin = rng.normal(scale=3, size=n).astype(np.float32)
+    y = (rng.random(n) < 0.5).astype(np.float32)
+    X = rng.normal(size=(n, 2)).astype(np.float32)
+    d = ctx.quantise(X, 16)
+    d.set_logistic_gradients(margin, y)
+    d.sample(0, 1.0)
+    _, qg, qh = d.get_sample(n)
+    g, h = oracle.logistic_grad(margin, y)
+    og, _ = oracle.quantise(g.astype(np.float64), 16)
+    oh, _ = oracle.quantise(h.astype(np.float64), 16)
+    assert np.max(np.abs(qg - og)) <= 1 and np.max(np.abs(qh - oh)) <= 1
+    d.close()
+
+
+def test_out_of_core_equals_in_core(ctx):
+    """without sampling the out-of-core algorithm equals the in-core one (bit-exact)."""
+    n, m = 30000, 40
+    X, y = synth.make_classification(n, m, seed=3)
+    g, h = oracle.logistic_grad(np.zeros(n, np.float32), y)
+    trees = []
+    for placement, page in [(ob.PLACE_DEVICE, 0), (ob.PLACE_PINNED_HOST, 4096 * 48)]:
+        d = ctx.quantise(X, 256, page_bytes=page, placement=placement)
+        assert d.info()["n_pages"] == (1 if page == 0 else -(-n // (page // 48)))
+        d.set_gradients(g, h)
+        d.sample(0, 1.0)
+        t = d.build_tree(6)
+        trees.append((d, t, t.export()))
+    _compare_trees(trees[0][2], trees[1][2])
+    m0 = np.zeros(n, np.float32)
+    p0 = trees[0][0].predict([trees[0][1]], m0.copy())
+    p1 = trees[1][0].predict([trees[1][1]], m0.copy())
+    np.testing.assert_array_equal(p0, p1)
+    for d, t, _ in trees:
+        t.close()
+        d.close()
+
+
+@pytest.mark.parametrize("mode,ratio", [(2, 0.1), (1, 0.3)])
+def test_out_of_core_sampled_matches_oracle(ctx, mode, ratio):
+    """Alg. 7: sample, compact the pinned pages into one device page, build in-core."""
+    n, m = 25000, 24
+    X, y = synth.make_classification(n, m, seed=4)
+    cv, cp, B = _oracle_cuts_bins(X, 256)
+    g, h = oracle.logistic_grad(np.random.default_rng(2).normal(size=n).astype(np.float32), y)
+    on, olor, _, sel = _oracle_tree(B, m, cv, cp, g, h, mode, ratio, 6, seed=5, round_=9)
+    d = ctx.quantise(X, 256, page_bytes=3000 * 32, placement=ob.PLACE_PINNED_HOST)
+    d.set_gradients(g, h)
+    info = d.sample(mode, ratio, 1.0, 5, 9, 16)
+    t = d.build_tree(6, keep_debug=True)
+    _compare_trees(t.export(), on)
+    np.testing.assert_array_equal(t.get_partition(info["n_selected_local"]), olor)
+    t.close()
+    d.close()
+
+
+def test_training_auc_config1(ctx):
+    """Config 1 (10k x 20, 256 bins, depth 6, 10 rounds, binary:logistic): AUC vs oracle <= 1e-3 rel."""
+    from sklearn.metrics import roc_auc_score
+    n, m = 10000, 20
+    X, y = synth.make_classification(n, m, seed=0)
+    cv, cp, B = _oracle_cuts_bins(X, 256)
+    d = ctx.quantise(X, 256)
+    gm = np.zeros(n, np.float32)
+    om = np.zeros(n, np.float32)
+    prev_o = None
+    for r in range(10):
+        d.set_logistic_gradients(gm, y)
+        d.sample(0, 1.0, round=r)
+        t = d.build_tree(6)
+        d.predict([t], gm)
+        t.close()
+        on, om, _ = oracle.boosting_round(B, m, cv, cp, om, y, max_depth=6, prev_tree=prev_o, round_=r)
+        prev_o = on
+    om = oracle.predict(B, prev_o, om)
+    a_gpu, a_orc = roc_auc_score(y, gm), roc_auc_score(y, om)
+    assert abs(a_gpu - a_orc) / a_orc <= 1e-3
+    assert a_gpu > 0.8
+    d.close()
+
+
+def test_state_errors(ctx):
+    X = np.random.default_rng(0).normal(size=(100, 3)).astype(np.float32)
+    d = ctx.quantise(X, 16)
+    with pytest.raises(ob.OocgbError) as e:
+        d.build_tree(3)
+    assert e.value.status == ob.ERR_STATE
+    with pytest.raises(ob.OocgbError) as e:
+        d.sample(0, 1.0)
+    assert e.value.status == ob.ERR_STATE
+    d.set_gradients(np.zeros(100, np.float32), np.ones(100, np.float32))
+    with pytest.raises(ob.OocgbError) as e:
+        d.sample(1, 0.0)
+    assert e.value.status == ob.ERR_ARG
+    with pytest.raises(ob.OocgbError) as e:
+        d.set_gradients(np.zeros(99, np.float32), np.ones(99, np.float32))
+    assert e.value.status == ob.ERR_ARG
+    d.close()
