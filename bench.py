@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py — seconds per boosting round (and histogram GB/s vs HBM peak) of the B200 hot path
+of "Out-of-Core GPU Gradient Boosting" (arXiv 2005.09148), BASELINE.json config 2:
+1M rows x 500 features make_classification-style, 256 bins, depth 8, in-core, binary:logistic.
+
+A step = one boosting round through the library's public API, exactly the north_star's calls:
+  update margin with tree t-1 (Eq. 1) -> logistic gradients (Eq. 5) -> sample(NONE, f = 1)
+  -> build_tree(depth 8, lambda 1, gamma 0)   (histograms, evaluation, partition, leaves)
+Timing: W untimed warm-up rounds, then K rounds between CUDA events on the stream the library
+launches on (torch's current stream is handed to the library), barrier + synchronize on both
+sides, max over ranks.  Inputs (512 MB of ELLPACK) are larger than L2 (126 MB).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (row-sharded, weak scaling: 1M rows/GPU)
+
+--impl reference times the CPU oracle (oracle/, as it stands) on a bounded sample of the same
+workload and extrapolates to the config (it is the deliberately slow reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ROWS, N_FEAT, MAX_BIN, DEPTH = 1_000_000, 500, 256, 8
+LAMBDA, GAMMA, MCW, ETA, QBITS = 1.0, 0.0, 1.0, 0.1, 16
+METRIC = "sec/boosting round"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=N_ROWS, help="rows per GPU (config 2: 1M)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON line)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        for k in ("hbm_gbs", "hbm_GBps", "hbm"):
+            if k in d:
+                return float(d[k]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        pass
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        self.path = f"/tmp/oocgb_clocks_{os.getpid()}.csv"
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def hist_rows(nodes: np.ndarray):
+    """(rows of built nodes summed over levels, number of built nodes) of one tree."""
+    D = int(np.log2(len(nodes) + 1)) - 1
+    rows, built = 0, 0
+    for v in range((1 << D) - 1):
+        if v == 0:
+            rows += int(nodes["n_rows"][0])
+            built += 1
+            continue
+        p = (v - 1) // 2
+        if nodes["feature"][p] < 0 or v != 2 * p + 1:
+            continue
+        rows += min(int(nodes["n_rows"][v]), int(nodes["n_rows"][v + 1]))
+        built += 1
+    return rows, built
+
+
+def hist_algorithmic_bytes(nodes: np.ndarray, m: int) -> float:
+    """per built node, 1 B per (row, feature) symbol + 8 B (q_g, q_h int32)
+    + 4 B row index per row, + the node's int64 histogram (m x 256 x 16 B) written.  Built nodes:
+    the root, then the child with fewer rows of every split (ties: left), levels 0..D-1."""
+    rows, built = hist_rows(nodes)
+    return rows * (m + 8 + 4) + built * m * 256 * 16.0
+
+
+def launches_per_round(D: int) -> int:
+    # update_margin 1 + logistic 1 + sample(NONE): absmax 1 + quantise 1
+    # build_tree: init 1 + per level (hist, eval, finalize, part_flags, plan1, plan2, scatter) 7
+    return 4 + 1 + 7 * D
+
+
+def make_data(rows, rank):
+    import synth
+    X, y = synth.fast_classification(rows, N_FEAT, seed=1000 + rank)
+    return X, y
+
+
+def cpu_baseline_leg(sample_rows=200_000, rounds=3):
+    """Oracle (as it stands, single thread) on a bounded sample of config 2: `rounds` boosting
+    rounds on sample_rows x 500, depth 8; sec/round extrapolated linearly in rows (the oracle is
+    O(rows x features x depth)) to 1M rows.  Setup (cuts, bins) untimed."""
+    import oracle
+    import synth
+    X, y = synth.fast_classification(sample_rows, N_FEAT, seed=77)
+    cv, cp = oracle.cuts(X, MAX_BIN)
+    B = oracle.bins(X, cv, cp)
+    margin = np.zeros(sample_rows, np.float32)
+    prev = None
+    ts = []
+    for r in range(rounds):
+        t0 = time.perf_counter()
+        prev, margin, _ = oracle.boosting_round(B, N_FEAT, cv, cp, margin, y, max_depth=DEPTH, lam=LAMBDA,
+                                                gamma=GAMMA, mcw=MCW, eta=ETA, quant_bits=QBITS,
+                                                prev_tree=prev, round_=r)
+        ts.append(time.perf_counter() - t0)
+    per_round = statistics.median(ts) * (N_ROWS / sample_rows)
+    return {"value": per_round, "unit": "s", "cores": 1, "kind": "oracle",
+            "sample": f"{rounds} rounds on {sample_rows} x {N_FEAT} rows (depth {DEPTH}), median sec/round "
+                      f"x {N_ROWS // sample_rows} (linear in rows) -> 1M x 500; single thread, "
+                      f"host {os.cpu_count()} cores"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    sample_rows = 100_000
+    X, y = synth.fast_classification(sample_rows, N_FEAT, seed=77)
+    cv, cp = oracle.cuts(X, MAX_BIN)
+    B = oracle.bins(X, cv, cp)
+    margin = np.zeros(sample_rows, np.float32)
+    prev = None
+    ts = []
+    for r in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        prev, margin, _ = oracle.boosting_round(B, N_FEAT, cv, cp, margin, y, max_depth=DEPTH, lam=LAMBDA,
+                                                gamma=GAMMA, mcw=MCW, eta=ETA, quant_bits=QBITS,
+                                                prev_tree=prev, round_=r)
+        if r >= args.warmup:
+            ts.append(time.perf_counter() - t0)
+    scale = N_ROWS / sample_rows
+    v = sum(ts) / len(ts) * scale
+    sample = (f"each step = 1 boosting round on {sample_rows} x {N_FEAT} (depth {DEPTH}); sec/round x {scale:.0f}"
+              f" (linear in rows) -> config 2 (1M x 500); single thread")
+    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64 fixed-point histograms, f64 gains", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "config 2: 1M x 500 make_classification, 256 bins, depth 8, in-core, f=1",
+                       "rows_per_gpu": N_ROWS, "n_features": N_FEAT, "max_bin": MAX_BIN, "max_depth": DEPTH},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import paper_2005_09148_b200 as ob
+    from paper_2005_09148_b200 import build as obuild
+    if rank == 0:
+        obuild.build()
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    nid = None
+    if world > 1:
+        import torch.distributed as tdist
+        idl = [ob.nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(idl, src=0)
+        nid = idl[0]
+    ctx = ob.Context(local, rank, world, nid, stream=stream.cuda_stream)
+    rows = args.rows
+    X, y = make_data(rows, rank)
+    Xd = torch.from_numpy(X).cuda()
+    yd = torch.from_numpy(y).cuda()
+    d = ctx.quantise(Xd, MAX_BIN, row0_global=rank * rows, n_rows_global=world * rows)
+    del Xd
+    torch.cuda.synchronize()
+    margin = torch.zeros(rows, dtype=torch.float32, device="cuda")
+
+    def round_device(prev_tree, r):
+        if prev_tree is not None:
+            d.update_margin(prev_tree, margin)
+            prev_tree.close()
+        d.set_logistic_gradients(margin, yd)
+        d.sample(ob.SAMPLE_NONE, 1.0, round=r, quant_bits=QBITS)
+        return d.build_tree(DEPTH, LAMBDA, GAMMA, MCW, ETA)
+
+    tree = None
+    r = 0
+    for _ in range(args.warmup):
+        tree = round_device(tree, r)
+        r += 1
+    if args.profile_only:
+        for _ in range(args.steps):
+            tree = round_device(tree, r)
+            r += 1
+        torch.cuda.synchronize()
+        return
+    clocks = ClockSampler(local)
+    ctx.set_profiling(True)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    hist_bytes = 0.0
+    hist_rowfeat = 0.0
+    for _ in range(args.steps):
+        tree = round_device(tree, r)
+        nodes = tree.export()
+        hist_bytes += hist_algorithmic_bytes(nodes, N_FEAT)
+        hist_rowfeat += hist_rows(nodes)[0] * N_FEAT
+        r += 1
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    tm = ctx.get_timings()
+    ctx.set_profiling(False)
+    ck = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t[0])
+    ms_step = ms / args.steps
+    hist_ms = tm["hist_ms"]
+    n_hist = max(1, int(tm["hist_launches"]))
+    achieved = (hist_bytes / n_hist) / (hist_ms / n_hist * 1e-3) / 1e9  # GB/s per launch average
+    peak, peak_src = hbm_peak()
+
+    # ---- e2e: the same round through the public API with HOST buffers (pinned), H2D/D2H inside
+    m_host = torch.zeros(rows, dtype=torch.float32).pin_memory()
+    y_host = torch.from_numpy(y).pin_memory()
+    e2e_tree = None
+    rr = r
+
+    def round_host(prev_tree, r_):
+        if prev_tree is not None:
+            d.update_margin(prev_tree, m_host)      # H2D + D2H of the margin
+            prev_tree.close()
+        d.set_logistic_gradients(m_host, y_host)    # H2D of margin + labels
+        d.sample(ob.SAMPLE_NONE, 1.0, round=r_, quant_bits=QBITS)
+        t = d.build_tree(DEPTH, LAMBDA, GAMMA, MCW, ETA)
+        t.export()                                  # D2H of the tree
+        return t
+
+    for _ in range(2):
+        e2e_tree = round_host(e2e_tree, rr)
+        rr += 1
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_tree = round_host(e2e_tree, rr)
+        rr += 1
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    n_nodes = (1 << (DEPTH + 1)) - 1
+    h2d = rows * 4 * 3
+    d2h = rows * 4 + n_nodes * 48
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8 symbols, int32/int64 fixed-point sums, f64 gains",
+            "data": "synthetic (make_classification-style, seeded)",
+            "config": {"workload": "config 2: 1M x 500 make_classification, 256 bins, depth 8, in-core, f=1",
+                       "rows_per_gpu": rows, "rows_global": rows * world, "n_features": N_FEAT,
+                       "max_bin": MAX_BIN, "max_depth": DEPTH, "quant_bits": QBITS,
+                       "parallelism": f"row-sharded dp{world}",
+                       "l2": "inputs larger than L2 (512 MB ELLPACK per GPU vs 126 MB L2), no flush"},
+            "gpu_launches": launches_per_round(DEPTH) * args.steps,
+            "rows_rounds_per_s": rows * world / (ms_step / 1e3),
+            "histogram": {"row_features_per_s": hist_rowfeat / (hist_ms * 1e-3), "ms_per_round": hist_ms / args.steps,
+                          "launches": n_hist, "algorithmic_bytes_per_round": hist_bytes / args.steps},
+            "phases_ms_per_round": {k: v / args.steps for k, v in tm.items() if k.endswith("_ms")},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "k_hist",
+                         "peak_source": peak_src},
+            "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "clocks": ck,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    for t in (tree, e2e_tree):
+        if t is not None:
+            t.close()
+    d.close()
+    ctx.close()
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,8 +1,8 @@
 """Build liboocgb.so in-tree for sm_100a (nvcc, -gencode arch=compute_100a,code=sm_100a).
 
 Flags: -O3 -lineinfo (ncu source view), -fmad=false and host -ffp-contract=off (no FMA
-contraction anywhere in the split/sampling arithmetic, DESIGN.md §3 R14), links NCCL for the
-multi-GPU histogram all-reduce.
+contraction anywhere in the split/sampling arithmetic, DESIGN.md §3 R14).  NCCL (multi-GPU
+histogram all-reduce) is dlopen'ed at run time, not linked.
 """
 from __future__ import annotations
 
@@ -31,7 +31,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
     tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *SRC, "-lnccl"]
+    cmd = [NVCC, *FLAGS, "-o", tmp, *SRC, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -2,6 +2,7 @@
 // marshalling, NCCL plumbing and the page streamer.  The arithmetic of the method lives in
 // quantise.cu, sample.cu and tree.cu.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -39,13 +40,35 @@ bool is_device_ptr(const void *p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+const NcclApi &nccl_api() {
+  static NcclApi api{};
+  static bool loaded = false;
+  if (loaded) return api;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) throw Error(OOCGB_ERR_DEVICE, std::string("cannot load NCCL: ") + dlerror());
+  auto sym = [&](const char *n) {
+    void *p = dlsym(h, n);
+    if (!p) throw Error(OOCGB_ERR_DEVICE, std::string("NCCL symbol missing: ") + n);
+    return p;
+  };
+  api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+  api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+  api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+  api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+  loaded = true;
+  return api;
+}
+
 void allreduce_sum_i64(oocgb_ctx c, long long *d_buf, size_t count) {
   if (c->world <= 1 || count == 0) return;
-  OOCGB_NCCL(ncclAllReduce(d_buf, d_buf, count, ncclInt64, ncclSum, c->comm, c->stream));
+  OOCGB_NCCL(nccl_api().AllReduce(d_buf, d_buf, count, ncclInt64, ncclSum, c->comm, c->stream));
 }
 void allreduce_max_u64(oocgb_ctx c, unsigned long long *d_buf, size_t count) {
   if (c->world <= 1 || count == 0) return;
-  OOCGB_NCCL(ncclAllReduce(d_buf, d_buf, count, ncclUint64, ncclMax, c->comm, c->stream));
+  OOCGB_NCCL(nccl_api().AllReduce(d_buf, d_buf, count, ncclUint64, ncclMax, c->comm, c->stream));
 }
 
 cudaEvent_t pool_event(oocgb_ctx c) {
@@ -238,7 +261,7 @@ int oocgb_nccl_unique_id(uint8_t out[128]) {
   API_BEGIN
   OOCGB_REQUIRE(out, OOCGB_ERR_ARG, "out is NULL");
   ncclUniqueId id;
-  OOCGB_NCCL(ncclGetUniqueId(&id));
+  OOCGB_NCCL(nccl_api().GetUniqueId(&id));
   static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
   memcpy(out, &id, 128);
   API_END
@@ -274,7 +297,7 @@ int oocgb_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t 
     if (world > 1) {
       ncclUniqueId id;
       memcpy(&id, nccl_id, 128);
-      OOCGB_NCCL(ncclCommInitRank(&c->comm, world, id, rank));
+      OOCGB_NCCL(nccl_api().CommInitRank(&c->comm, world, id, rank));
     }
   } catch (...) {
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -294,7 +317,7 @@ int oocgb_ctx_destroy(oocgb_ctx c) {
   OOCGB_REQUIRE(c->live_data == 0, OOCGB_ERR_STATE, "ctx_destroy: data handles are still alive");
   bind(c);
   cudaStreamSynchronize(c->stream);
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm) nccl_api().CommDestroy(c->comm);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto e : c->pending_a) cudaEventDestroy(e);
   for (auto e : c->pending_b) cudaEventDestroy(e);

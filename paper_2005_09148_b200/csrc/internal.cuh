@@ -32,11 +32,24 @@ struct Error : std::runtime_error {
     }                                                                                        \
   } while (0)
 
+// NCCL is loaded lazily with dlopen("libnccl.so.2") (nccl_api() in api.cu) so that a process
+// that never goes multi-GPU never loads it, and a process that imported torch first binds to
+// torch's NCCL instead of a second copy.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  const char *(*GetErrorString)(ncclResult_t);
+};
+const NcclApi &nccl_api();
+
 #define OOCGB_NCCL(call)                                                                     \
   do {                                                                                       \
     ncclResult_t r_ = (call);                                                                \
     if (r_ != ncclSuccess)                                                                   \
-      throw ::oocgb::Error(OOCGB_ERR_DEVICE, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+      throw ::oocgb::Error(OOCGB_ERR_DEVICE, std::string(#call) + ": " + ::oocgb::nccl_api().GetErrorString(r_)); \
   } while (0)
 
 #define OOCGB_REQUIRE(cond, status, msg)                                                     \
