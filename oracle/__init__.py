@@ -137,7 +137,8 @@ def cuts(X: np.ndarray, max_bin: int = 256, seed: int = 2, row0: int = 0, n_glob
 
 
 def stride_of(m: int) -> int:
-    return (m + 15) // 16 * 16
+    """R5: bytes per ELLPACK row = 32 * ceil(m / 32) (feature groups of 32), pad bytes 0."""
+    return (m + 31) // 32 * 32
 
 
 # ---------------------------------------------------------------------------------------- O2

@@ -174,11 +174,16 @@ static oocgb_data new_data(oocgb_ctx c, int64_t n_local, int64_t row0, int64_t n
   d->row0 = row0;
   d->n_global = n_global;
   d->m = m;
-  d->stride = (m + 15) / 16 * 16;
+  d->n_fg = (m + 31) / 32;
+  d->stride = 32 * d->n_fg;  // bytes per row summed over the group planes (R5)
   d->max_bin = max_bin;
   d->placement = placement;
   d->seed = seed;
-  d->rows_per_page = page_bytes > 0 ? std::max<int64_t>(1, page_bytes / d->stride) : std::max<int64_t>(1, n_local);
+  // DEVICE placement keeps one page (the device-resident ELLPACK matrix, Alg. 4); PINNED_HOST
+  // pages hold floor(page_bytes / stride) rows (R6)
+  d->rows_per_page = (page_bytes > 0 && placement == OOCGB_PLACE_PINNED_HOST)
+                         ? std::max<int64_t>(1, page_bytes / d->stride)
+                         : std::max<int64_t>(1, n_local);
   d->n_pages = std::max<int64_t>(1, (n_local + d->rows_per_page - 1) / d->rows_per_page);
   c->live_data++;
   return d;
@@ -196,7 +201,7 @@ static void free_data(oocgb_data d) {
 }
 
 static void alloc_pages(oocgb_data d) {
-  const size_t bytes = (size_t)std::max<int64_t>(1, d->n_local) * d->stride;
+  const size_t bytes = (size_t)d->n_pages * (size_t)d->rows_per_page * d->stride;
   if (d->placement == OOCGB_PLACE_DEVICE) {
     d->d_bins = (uint8_t *)dmalloc(bytes);
   } else {
@@ -208,23 +213,14 @@ static void alloc_pages(oocgb_data d) {
   }
 }
 
-// Bin rows [row_local0, row_local0 + n) of X (device) into the pages.
+// Bin rows [row_local0, row_local0 + n) of X (device) straight into the tiled pages: device
+// memory, or pinned host memory written zero-copy (mapped, UVA) by the binning kernel.
 static void write_pages(oocgb_data d, const float *dX, int64_t row_local0, int64_t n) {
   oocgb_ctx c = d->ctx;
   int *d_err = (int *)((char *)c->d_small + 4096);
   OOCGB_CK(cudaMemsetAsync(d_err, 0, sizeof(int), c->stream));
-  if (d->placement == OOCGB_PLACE_DEVICE) {
-    bin_rows(d, dX, n, d->d_bins + row_local0 * d->stride, d_err);
-  } else {
-    ensure_staging(d);
-    for (int64_t r = 0; r < n; r += d->stage_rows) {
-      int64_t nr = std::min<int64_t>(d->stage_rows, n - r);
-      bin_rows(d, dX + r * d->m, nr, d->d_stage[0], d_err);
-      OOCGB_CK(cudaMemcpyAsync(d->h_pages + (row_local0 + r) * d->stride, d->d_stage[0], (size_t)nr * d->stride,
-                               cudaMemcpyDeviceToHost, c->stream));
-      OOCGB_CK(cudaStreamSynchronize(c->stream));
-    }
-  }
+  uint8_t *base = d->placement == OOCGB_PLACE_DEVICE ? d->d_bins : d->h_pages;
+  bin_rows(d, dX, n, row_local0, base, d_err);
   int herr = 0;
   OOCGB_CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   OOCGB_CK(cudaStreamSynchronize(c->stream));
@@ -569,10 +565,10 @@ int oocgb_predict(oocgb_data d, const oocgb_tree *trees, int32_t n_trees, float 
     for (int t0 = 0; t0 < n_trees; t0 += 4096) {
       int nt = std::min(4096, n_trees - t0);
       if (d->placement == OOCGB_PLACE_DEVICE) {
-        predict_device(d, d->d_bins, d->n_local, 0, trees + t0, nt, dm);
+        predict_device(d, d->d_bins, d->rows_per_page, d->n_local, 0, trees + t0, nt, dm);
       } else {
         for_each_page(d, [&](const uint8_t *page, int64_t r0, int64_t nr) {
-          predict_device(d, page, nr, r0, trees + t0, nt, dm);
+          predict_device(d, page, d->rows_per_page, nr, r0, trees + t0, nt, dm);
         });
       }
     }
@@ -629,10 +625,27 @@ int oocgb_get_bins(oocgb_data d, int64_t row0_local, int64_t n, uint8_t *out) {
                 "get_bins: row range outside the written pages");
   bind(d->ctx);
   if (n == 0) return OOCGB_OK;
-  if (d->placement == OOCGB_PLACE_DEVICE)
-    OOCGB_CK(cudaMemcpy(out, d->d_bins + row0_local * d->stride, (size_t)n * d->stride, cudaMemcpyDeviceToHost));
-  else
-    memcpy(out, d->h_pages + row0_local * d->stride, (size_t)n * d->stride);
+  // tiled pages -> row-major [n][stride] (ABI order: row i, feature j at out[i * stride + j])
+  const int64_t rpp = d->rows_per_page;
+  std::vector<uint8_t> page_buf;
+  for (int64_t r = row0_local; r < row0_local + n;) {
+    const int64_t p = r / rpp, r_in = r - p * rpp;
+    const int64_t cnt = std::min<int64_t>(rpp - r_in, row0_local + n - r);
+    for (int g = 0; g < d->n_fg; ++g) {
+      const size_t off = ell_off(r, 32 * g, rpp, d->n_fg);
+      const uint8_t *src;
+      if (d->placement == OOCGB_PLACE_DEVICE) {
+        page_buf.resize((size_t)cnt * 32);
+        OOCGB_CK(cudaMemcpy(page_buf.data(), d->d_bins + off, (size_t)cnt * 32, cudaMemcpyDeviceToHost));
+        src = page_buf.data();
+      } else {
+        src = d->h_pages + off;
+      }
+      for (int64_t i = 0; i < cnt; ++i)
+        memcpy(out + (size_t)(r - row0_local + i) * d->stride + 32 * g, src + (size_t)i * 32, 32);
+    }
+    r += cnt;
+  }
   API_END
 }
 

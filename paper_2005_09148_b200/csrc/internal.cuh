@@ -61,7 +61,7 @@ const NcclApi &nccl_api();
 // Tuning constants.
 constexpr int kFG = 32;              // features per histogram feature-group (one 32 B sector)
 constexpr int kBins = 256;           // uint8 symbols (R5, R7)
-constexpr int kHistThreads = 256;    // histogram CTA
+constexpr int kHistThreads = 384;    // histogram CTA
 constexpr int kHistSmem = 2 * kBins * kFG * 4;  // g and h s32 planes [bin][32 features]
 constexpr int kPartTile = 2048;      // positions per partition tile
 constexpr int kPartThreads = 256;
@@ -114,6 +114,12 @@ struct LevelCtl {       // device-resident control block of one build
   int pad[3];
 };
 
+// byte offset of symbol (row, f) in a tiled ELLPACK buffer of pages of rpp rows
+__host__ __device__ __forceinline__ size_t ell_off(int64_t row, int f, int64_t rpp, int n_fg) {
+  const int64_t p = row / rpp, r = row - p * rpp;
+  return ((size_t)p * n_fg + (size_t)(f >> 5)) * (size_t)rpp * 32 + (size_t)r * 32 + (size_t)(f & 31);
+}
+
 struct PNode {          // compact node for predict
   int32_t feature;
   int32_t split_bin;
@@ -147,6 +153,7 @@ struct oocgb_data_s {
   oocgb_ctx ctx = nullptr;
   int64_t n_local = 0, n_global = 0, row0 = 0;
   int32_t m = 0, stride = 0, max_bin = 256, placement = OOCGB_PLACE_DEVICE;
+  int32_t n_fg = 0;                // feature groups of 32 (stride = 32 n_fg bytes per row)
   int64_t rows_per_page = 0, n_pages = 1;
   uint64_t seed = 0;
   // cuts (R1-R4)
@@ -156,8 +163,11 @@ struct oocgb_data_s {
   std::vector<int32_t> h_cut_ptrs;
   bool cuts_ready = false;
   // ELLPACK (R5-R6)
-  uint8_t *d_bins = nullptr;    // DEVICE placement: [n_local][stride]
-  uint8_t *h_pages = nullptr;   // PINNED_HOST placement: [n_local][stride] (pages are row ranges)
+  // Tiled ELLPACK (R5): pages of rows_per_page rows; inside a page the symbols of
+  // feature group g (features 32g..32g+31) of all the page's rows are contiguous:
+  //   offset(row, f) = page * (rpp * stride) + (f / 32) * (rpp * 32) + (row % rpp) * 32 + f % 32
+  uint8_t *d_bins = nullptr;    // DEVICE placement: one page, rpp = n_local
+  uint8_t *h_pages = nullptr;   // PINNED_HOST placement: n_pages pages (last one padded)
   int64_t rows_written = 0;     // streamed pages_push progress
   // streamed sketch state
   uint32_t *d_sketch = nullptr; // column-major ordered keys [m][cap]
@@ -213,7 +223,7 @@ bool is_device_ptr(const void *p);
 // quantise.cu
 void sketch_append(oocgb_data d, const float *dX, int64_t row0_global, int64_t n);
 void cuts_finalize(oocgb_data d);
-void bin_rows(oocgb_data d, const float *dX, int64_t n, uint8_t *d_out, int *d_err);
+void bin_rows(oocgb_data d, const float *dX, int64_t n, int64_t row_local0, uint8_t *out_base, int *d_err);
 
 // sample.cu
 void logistic_gradients(oocgb_data d, const float *d_margin, const float *d_labels);
@@ -223,7 +233,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
 // tree.cu
 oocgb_tree build_tree(oocgb_data d, int max_depth, double lambda, double gamma, double mcw,
                       double eta, bool keep_debug);
-void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t n_rows, int64_t row_offset,
+void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t rpp, int64_t n_rows, int64_t row_offset,
                     const oocgb_tree *trees, int n_trees, float *d_margin);
 void update_margin(oocgb_data d, oocgb_tree t, float *d_margin);
 void free_work(oocgb_data d);

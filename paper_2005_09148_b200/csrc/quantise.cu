@@ -131,34 +131,37 @@ __global__ void k_extract_cuts(const uint32_t *__restrict__ sorted, int64_t N, i
   }
 }
 
-// LookupBin + Write (Alg. 4): thread per (row, 4 features) -> one 32-bit store.
-__global__ void k_bin_rows(const float *__restrict__ X, int64_t n, int m, int stride,
-                           const float *__restrict__ cuts, const int *__restrict__ ptrs,
+// LookupBin + Write (Alg. 4) into the tiled page layout.  Thread per (feature group g,
+// row r, quad u): consecutive threads write consecutive 32-bit words of a group plane, so the
+// output is fully coalesced (device pages, or pinned host pages written zero-copy over PCIe).
+__global__ void k_bin_rows(const float *__restrict__ X, int64_t n, int m, int n_fg, int64_t row_local0,
+                           int64_t rpp, const float *__restrict__ cuts, const int *__restrict__ ptrs,
                            uint8_t *__restrict__ out, int *err) {
-  int quads = stride >> 2;
-  int64_t total = n * quads;
+  const int64_t total = (int64_t)n_fg * n * 8;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = t / quads;
-    int q = (int)(t - r * quads);
+    const int u = (int)(t & 7);
+    const int64_t gr = t >> 3;
+    const int g = (int)(gr / n);
+    const int64_t r = gr - (int64_t)g * n;
     uint32_t word = 0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      int j = q * 4 + c;
+      const int j = g * 32 + u * 4 + c;
       if (j >= m) break;
-      float x = X[r * m + j];
+      const float x = X[r * m + j];
       if (!isfinite(x)) { atomicExch(err, 2); continue; }
-      int lo = __ldg(ptrs + j), hi = __ldg(ptrs + j + 1);
-      int B = hi - lo;
+      const int lo = __ldg(ptrs + j), hi = __ldg(ptrs + j + 1);
+      const int B = hi - lo;
       int a = 0, bnd = B;  // lower_bound: smallest b with x <= c_b
       while (a < bnd) {
-        int mid = (a + bnd) >> 1;
+        const int mid = (a + bnd) >> 1;
         if (x <= __ldg(cuts + lo + mid)) bnd = mid; else a = mid + 1;
       }
       if (a > B - 1) a = B - 1;  // clamp above the last cut (R3)
       word |= (uint32_t)a << (8 * c);
     }
-    reinterpret_cast<uint32_t *>(out + r * stride)[q] = word;
+    *reinterpret_cast<uint32_t *>(out + ell_off(row_local0 + r, g * 32 + u * 4, rpp, n_fg)) = word;
   }
 }
 
@@ -329,13 +332,13 @@ void cuts_finalize(oocgb_data d) {
   d->cuts_ready = true;
 }
 
-void bin_rows(oocgb_data d, const float *dX, int64_t n, uint8_t *d_out, int *d_err) {
+void bin_rows(oocgb_data d, const float *dX, int64_t n, int64_t row_local0, uint8_t *out_base, int *d_err) {
   oocgb_ctx c = d->ctx;
   if (n <= 0) return;
-  int64_t total = n * (d->stride / 4);
-  int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)c->num_sms * 32);
-  k_bin_rows<<<blocks, 256, 0, c->stream>>>(dX, n, d->m, d->stride, d->d_cut_values, d->d_cut_ptrs,
-                                            d_out, d_err);
+  const int64_t total = (int64_t)d->n_fg * n * 8;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)c->num_sms * 32);
+  k_bin_rows<<<blocks, 256, 0, c->stream>>>(dX, n, d->m, d->n_fg, row_local0, d->rows_per_page, d->d_cut_values,
+                                            d->d_cut_ptrs, out_base, d_err);
   OOCGB_CK(cudaGetLastError());
 }
 

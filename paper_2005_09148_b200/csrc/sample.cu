@@ -271,19 +271,20 @@ __global__ void k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, i
   }
 }
 
-// Compact (Alg. 7): copy the selected rows of one staged page into the sampled page.
-__global__ void k_compact_page(const uint8_t *__restrict__ page, int64_t page_row0, int stride,
-                               const int32_t *__restrict__ sel_rows, int64_t k0, int64_t k1,
+// Compact (Alg. 7): copy the selected rows of one staged page (rpp-row group planes)
+// into the sampled page (cap-row group planes): thread per (selected row, group, 16-B half).
+__global__ void k_compact_page(const uint8_t *__restrict__ page, int64_t page_row0, int64_t rpp, int n_fg,
+                               const int32_t *__restrict__ sel_rows, int64_t k0, int64_t k1, int64_t cap,
                                uint8_t *__restrict__ out) {
-  int vec = stride / 16;
-  int64_t total = (k1 - k0) * vec;
+  const int64_t total = (k1 - k0) * n_fg * 2;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t k = k0 + t / vec;
-    int v = (int)(t % vec);
-    int64_t r = sel_rows[k] - page_row0;
-    reinterpret_cast<uint4 *>(out + k * stride)[v] =
-        reinterpret_cast<const uint4 *>(page + r * stride)[v];
+    const int h = (int)(t & 1);
+    const int g = (int)((t >> 1) % n_fg);
+    const int64_t k = k0 + (t >> 1) / n_fg;
+    const int64_t r = sel_rows[k] - page_row0;
+    *reinterpret_cast<uint4 *>(out + ((size_t)g * cap + k) * 32 + h * 16) =
+        *reinterpret_cast<const uint4 *>(page + ((size_t)g * rpp + r) * 32 + h * 16);
   }
 }
 
@@ -522,7 +523,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       dfree(d->d_sampled_page);
       d->d_sampled_page = nullptr;
       d->sampled_cap = 0;
-      d->d_sampled_page = (uint8_t *)dmalloc((size_t)std::max<int64_t>(1, d->n_sel) * d->stride);
+      d->d_sampled_page = (uint8_t *)dmalloc((size_t)std::max<int64_t>(1, d->n_sel) * d->stride);  // tiled, cap rows
       d->sampled_cap = std::max<int64_t>(1, d->n_sel);
     }
     std::vector<int32_t> hsel;
@@ -530,8 +531,9 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
     if (d->all_selected) {
       // identity selection: every page is copied whole
       for_each_page(d, [&](const uint8_t *page, int64_t r0, int64_t nr) {
-        OOCGB_CK(cudaMemcpyAsync(d->d_sampled_page + r0 * d->stride, page, (size_t)nr * d->stride,
-                                 cudaMemcpyDeviceToDevice, c->stream));
+        OOCGB_CK(cudaMemcpy2DAsync(d->d_sampled_page + r0 * 32, (size_t)d->sampled_cap * 32, page,
+                                   (size_t)d->rows_per_page * 32, (size_t)nr * 32, (size_t)d->n_fg,
+                                   cudaMemcpyDeviceToDevice, c->stream));
       });
     } else {
       // per-page ranges of sel_rows (ascending) via host binary search over a D2H copy
@@ -543,9 +545,9 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
         int64_t k0 = std::lower_bound(hsel.begin(), hsel.end(), (int32_t)r0) - hsel.begin();
         int64_t k1 = std::lower_bound(hsel.begin(), hsel.end(), (int32_t)(r0 + nr)) - hsel.begin();
         if (k1 > k0) {
-          int64_t tot = (k1 - k0) * (d->stride / 16);
-          k_compact_page<<<grid_for(c, tot), 256, 0, c->stream>>>(page, r0, d->stride, sel, k0, k1,
-                                                                    d->d_sampled_page);
+          int64_t tot = (k1 - k0) * d->n_fg * 2;
+          k_compact_page<<<grid_for(c, tot), 256, 0, c->stream>>>(page, r0, d->rows_per_page, d->n_fg, sel, k0, k1,
+                                                                    d->sampled_cap, d->d_sampled_page);
           OOCGB_CK(cudaGetLastError());
         }
       });

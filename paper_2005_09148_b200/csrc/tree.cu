@@ -101,16 +101,23 @@ __global__ void k_init_build(DNode *dn, int n_nodes, long long G, long long H, l
 
 // ---------------------------------------------------------------------------------------------
 // BuildHistograms.  Persistent CTAs over items = (global chunk, feature group).
+// Lane l of a warp works on row slot r = l >> 1 and half h = l & 1 of the 32-feature group
+// (features 16h .. 16h + 15): its 16 symbols are one 16-B load from the group plane (the two
+// lanes of a row read one 32-B sector; a warp's 16 consecutive rows are 512 contiguous bytes).
+// At step s the lane adds into feature 16h + ((r + s) & 15): for a fixed s the 32 lanes hit 32
+// distinct banks (h picks the bank half, the rotation a bank inside it) -> conflict-free ATOMS.
 __global__ void __launch_bounds__(kHistThreads, 3)
-k_hist(const uint8_t *__restrict__ bins, int stride, int m, int n_fg, const int32_t *__restrict__ ridx,
+k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
        const int2 *__restrict__ q, const Pair *__restrict__ pairs, const LevelCtl *__restrict__ ctl,
-       int *__restrict__ partial) {
+       int *__restrict__ partial, int identity, int opaque_zero) {
   extern __shared__ int4 smem4[];
   int *Gp = reinterpret_cast<int *>(smem4);
   int *Hp = Gp + kBins * kFG;
   const int n_items = ctl->n_items, n_pairs = ctl->n_pairs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wq = lane >> 2, bq = (lane & 3) * 8;
+  const int half = lane & 1, rslot = lane >> 1;
+  const int wq = rslot >> 2, bq = (rslot & 3) * 8;
+  constexpr int RT = kHistThreads / 2;  // rows per CTA step
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int fg = item % n_fg, cg = item / n_fg;
     int lo = 0, hi = n_pairs - 1;  // largest p with chunk_base <= cg
@@ -124,47 +131,65 @@ k_hist(const uint8_t *__restrict__ bins, int stride, int m, int n_fg, const int3
     const int r1 = min(P.begin + P.count, r0 + P.chunk_rows);
     for (int i = threadIdx.x; i < 2 * kBins * kFG / 4; i += kHistThreads) smem4[i] = make_int4(0, 0, 0, 0);
     __syncthreads();
-    const uint8_t *base = bins + fg * kFG;
-    const bool two = (fg * kFG + 16) < stride;
-    int k = r0 + threadIdx.x;
-    uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
-    int2 qq = make_int2(0, 0);
-    if (k < r1) {
-      const uint4 *p4 = reinterpret_cast<const uint4 *>(base + (size_t)ridx[k] * stride);
-      a = __ldg(p4);
-      if (two) b = __ldg(p4 + 1);
-      qq = q[k];
-    }
+    const uint8_t *base = bins + (size_t)fg * pitch + half * 16;
+    auto row_of = [&](int kk) -> int { return identity ? kk : __ldg(ridx + kk); };
+    auto load_row = [&](int kk, int row, uint4 &x, int2 &qv) {
+      if (kk < r1) {
+        x = __ldg(reinterpret_cast<const uint4 *>(base + (size_t)row * 32));
+        qv = __ldg(q + kk);
+      }
+    };
+    // rotate the lane's 16 symbols right by `rslot` bytes (byte s = feature 16h + ((rslot+s)&15))
+    // and return the 16 x 2 atomics as a closure, so the refill load can be issued in between.
+    auto accumulate = [&](const uint4 &x, const int2 qq, int kk) {
+      uint32_t w[4] = {x.x, x.y, x.z, x.w};
+      uint32_t t[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t[i] = (wq & 1) ? w[(i + 1) & 3] : w[i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = (wq & 2) ? t[(i + 2) & 3] : t[i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t[i] = __funnelshift_r(w[i], w[(i + 1) & 3], bq);
+      // row slot made opaque to ptxas so it cannot hoist 16 (rslot + s) & 15 registers
+      const uint32_t ln = (uint32_t)rslot + (uint32_t)(opaque_zero * kk);
+      const uint32_t hb = (uint32_t)half << 4;
+      return [=]() {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          const uint32_t bin = (t[s >> 2] >> ((s & 3) * 8)) & 0xffu;
+          const uint32_t idx = (bin << 5) | hb | ((ln + (uint32_t)s) & 15u);
+          atomicAdd(Gp + idx, qq.x);
+          atomicAdd(Hp + idx, qq.y);
+        }
+      };
+    };
+    // Software pipeline over rows k, k + RT, k + 2RT, ...: two register sets A and B alternate
+    // (loop unrolled by two, no in-flight register is ever copied); a set is refilled with the
+    // row two steps ahead right after its rotation consumed it, and the row id for that refill
+    // was loaded one step earlier still.
+    int k = r0 + (threadIdx.x >> 1);
+    uint4 xa = make_uint4(0, 0, 0, 0), xb = xa;
+    int2 qa = make_int2(0, 0), qb = qa;
+    int ra = 0, rb = 0;
+    if (k < r1) load_row(k, row_of(k), xa, qa);
+    if (k + RT < r1) load_row(k + RT, row_of(k + RT), xb, qb);
+    if (k + 2 * RT < r1) ra = row_of(k + 2 * RT);
+    if (k + 3 * RT < r1) rb = row_of(k + 3 * RT);
     while (k < r1) {
-      // prefetch the next row of this thread
-      const int kn = k + kHistThreads;
-      uint4 an = make_uint4(0, 0, 0, 0), bn = make_uint4(0, 0, 0, 0);
-      int2 qn = make_int2(0, 0);
-      if (kn < r1) {
-        const uint4 *p4 = reinterpret_cast<const uint4 *>(base + (size_t)ridx[kn] * stride);
-        an = __ldg(p4);
-        if (two) bn = __ldg(p4 + 1);
-        qn = q[kn];
+      {
+        auto run = accumulate(xa, qa, k);
+        load_row(k + 2 * RT, ra, xa, qa);
+        if (k + 4 * RT < r1) ra = row_of(k + 4 * RT);
+        run();
       }
-      // rotate the 32 symbols right by `lane` bytes: R byte s = symbol of feature (s + lane) & 31
-      uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      uint32_t t[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) t[i] = (wq & 1) ? w[(i + 1) & 7] : w[i];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = (wq & 2) ? t[(i + 2) & 7] : t[i];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) t[i] = (wq & 4) ? w[(i + 4) & 7] : w[i];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = __funnelshift_r(t[i], t[(i + 1) & 7], bq);
-#pragma unroll
-      for (int s = 0; s < 32; ++s) {
-        const uint32_t bin = (w[s >> 2] >> ((s & 3) * 8)) & 0xffu;
-        const uint32_t idx = (bin << 5) | ((uint32_t)(lane + s) & 31u);
-        atomicAdd(Gp + idx, qq.x);
-        atomicAdd(Hp + idx, qq.y);
+      if (k + RT >= r1) break;
+      {
+        auto run = accumulate(xb, qb, k + RT);
+        load_row(k + 3 * RT, rb, xb, qb);
+        if (k + 5 * RT < r1) rb = row_of(k + 5 * RT);
+        run();
       }
-      a = an; b = bn; qq = qn; k = kn;
+      k += 2 * RT;
     }
     __syncthreads();
     // flush: warp w owns bins [32w, 32w+32); lane l = feature l -> conflict-free reads; each lane
@@ -406,7 +431,7 @@ __device__ __forceinline__ int seg_of(const Seg *segs, int n_segs, int i) {
 
 __global__ void __launch_bounds__(kPartThreads)
 k_part_flags(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
-             const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, int stride,
+             const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, size_t pitch,
              const int32_t *__restrict__ ridx, uint32_t *__restrict__ flagbits, int *__restrict__ tile_cnt,
              int *__restrict__ bpart) {
   __shared__ uint32_t s_words[kPartTile / 32];
@@ -423,7 +448,7 @@ k_part_flags(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
       while (segs[s].begin + segs[s].count <= i) ++s;
       const DNode &nd = dn[segs[s].node];
       if (nd.feature >= 0) {
-        const uint8_t b = bins[(size_t)ridx[i] * stride + nd.feature];
+        const uint8_t b = bins[(size_t)(nd.feature >> 5) * pitch + (size_t)ridx[i] * 32 + (nd.feature & 31)];
         bits |= (uint32_t)(b > nd.split_bin) << k;
       }
     }
@@ -635,16 +660,19 @@ k_part_scatter(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__
 
 // ---------------------------------------------------------------------------------------------
 // Prediction (Eq. 1): margin[row] += leaf(tree, bins_row), binned traversal, per tree in order.
-__global__ void k_predict(const uint8_t *__restrict__ bins, int stride, int64_t n,
+__global__ void k_predict(const uint8_t *__restrict__ bins, size_t pitch, int64_t n,
                           const PNode *const *__restrict__ trees, int n_trees, float *__restrict__ margin) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float mg = margin[i];
-    const uint8_t *row = bins + i * stride;
+    const uint8_t *row = bins + i * 32;  // row i of group plane 0 (plane g at + g * pitch)
     for (int t = 0; t < n_trees; ++t) {
       const PNode *nd = trees[t];
       int v = 0;
-      while (nd[v].feature >= 0) v = (row[nd[v].feature] <= nd[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
+      while (nd[v].feature >= 0) {
+        const int f = nd[v].feature;
+        v = (row[(size_t)(f >> 5) * pitch + (f & 31)] <= nd[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
+      }
       mg = mg + nd[v].leaf;
     }
     margin[i] = mg;
@@ -742,8 +770,12 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   const size_t hsz = (size_t)m * kBins * 2;
   const uint8_t *bins;
   int ridx_mode;
-  if (d->placement == OOCGB_PLACE_PINNED_HOST) { bins = d->d_sampled_page; ridx_mode = 0; }
-  else { bins = d->d_bins; ridx_mode = d->all_selected ? 0 : 1; }
+  size_t pitch;  // bytes of one feature-group plane of the tiled page the tree reads
+  if (d->placement == OOCGB_PLACE_PINNED_HOST) {
+    bins = d->d_sampled_page; ridx_mode = 0; pitch = (size_t)d->sampled_cap * 32;
+  } else {
+    bins = d->d_bins; ridx_mode = d->all_selected ? 0 : 1; pitch = (size_t)d->rows_per_page * 32;
+  }
   if (keep_debug) {
     size_t need = sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1);
     if (w->dbg_bytes < need) { dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
@@ -762,8 +794,9 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
     {
       PhaseTimer t(c, 0);
-      k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, d->stride, m, n_fg, w->ridx[cur],
-                                                                   w->q[cur], w->pairs, w->ctl, w->partial);
+      k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur],
+                                                                   w->q[cur], w->pairs, w->ctl, w->partial,
+                                                                   (lv == 0 && ridx_mode == 0) ? 1 : 0, 0);
       OOCGB_CK(cudaGetLastError());
     }
     if (c->world > 1) {
@@ -794,7 +827,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     {
       PhaseTimer t(c, 2);
       if (n > 0) {
-        k_part_flags<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, d->stride,
+        k_part_flags<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
                                                             w->ridx[cur], w->flagbits, w->tile_cnt, w->bpart);
         OOCGB_CK(cudaGetLastError());
       }
@@ -884,7 +917,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   return t;
 }
 
-void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t n_rows, int64_t row_offset,
+void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t rpp, int64_t n_rows, int64_t row_offset,
                     const oocgb_tree *trees, int n_trees, float *d_margin) {
   oocgb_ctx c = d->ctx;
   if (n_rows <= 0 || n_trees <= 0) return;
@@ -894,7 +927,7 @@ void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t n_rows, int64_t
   OOCGB_REQUIRE(n_trees <= 4096, OOCGB_ERR_ARG, "predict: at most 4096 trees per call");
   OOCGB_CK(cudaMemcpyAsync(d_ptrs, ptrs.data(), sizeof(void *) * n_trees, cudaMemcpyHostToDevice, c->stream));
   int blocks = (int)std::min<int64_t>((n_rows + 255) / 256, (int64_t)c->num_sms * 16);
-  k_predict<<<blocks, 256, 0, c->stream>>>(d_bins, d->stride, n_rows, d_ptrs, n_trees, d_margin + row_offset);
+  k_predict<<<blocks, 256, 0, c->stream>>>(d_bins, (size_t)rpp * 32, n_rows, d_ptrs, n_trees, d_margin + row_offset);
   OOCGB_CK(cudaGetLastError());
 }
 

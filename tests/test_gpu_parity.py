@@ -215,9 +215,11 @@ def test_out_of_core_equals_in_core(ctx):
     X, y = synth.make_classification(n, m, seed=3)
     g, h = oracle.logistic_grad(np.zeros(n, np.float32), y)
     trees = []
-    for placement, page in [(ob.PLACE_DEVICE, 0), (ob.PLACE_PINNED_HOST, 4096 * 48)]:
+    for placement, page in [(ob.PLACE_DEVICE, 0), (ob.PLACE_PINNED_HOST, 4096 * 64)]:
         d = ctx.quantise(X, 256, page_bytes=page, placement=placement)
-        assert d.info()["n_pages"] == (1 if page == 0 else -(-n // (page // 48)))
+        st = d.info()["row_stride"]
+        assert st == 64
+        assert d.info()["n_pages"] == (1 if page == 0 else -(-n // (page // st)))
         d.set_gradients(g, h)
         d.sample(0, 1.0)
         t = d.build_tree(6)

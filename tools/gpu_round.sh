@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
 if [ -z "$SKIP_TESTS" ]; then
-  timeout 1200 python -m pytest tests -q -m gpu --tb=short --timeout 300 2>&1 | tail -40 > gpurun_out/parity.log
+  timeout 1200 python -m pytest tests -q -m gpu --tb=short --timeout 300 ${PYARGS} 2>&1 | tail -40 > gpurun_out/parity.log
   tail -5 gpurun_out/parity.log
 fi
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -3 gpurun_out/smoke.log
