@@ -101,23 +101,34 @@ __global__ void k_init_build(DNode *dn, int n_nodes, long long G, long long H, l
 
 // ---------------------------------------------------------------------------------------------
 // BuildHistograms.  Persistent CTAs over items = (global chunk, feature group).
+// Shared accumulators: s32 words [bin][g: 32 features | h: 32 features] -> word(bin, f) =
+// 64 bin + f for g and + 32 for h, so the bank of every accumulator is its feature f.
 // Lane l of a warp works on row slot r = l >> 1 and half h = l & 1 of the 32-feature group
 // (features 16h .. 16h + 15): its 16 symbols are one 16-B load from the group plane (the two
 // lanes of a row read one 32-B sector; a warp's 16 consecutive rows are 512 contiguous bytes).
 // At step s the lane adds into feature 16h + ((r + s) & 15): for a fixed s the 32 lanes hit 32
 // distinct banks (h picks the bank half, the rotation a bank inside it) -> conflict-free ATOMS.
+// Per symbol: one PRMT (bin * 256 straight from the packed word), one IADD3 (+ the lane's
+// precomputed feature offset and the shared base), two ATOMS.
 __global__ void __launch_bounds__(kHistThreads, 3)
 k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
        const int2 *__restrict__ q, const Pair *__restrict__ pairs, const LevelCtl *__restrict__ ctl,
        int *__restrict__ partial, int identity, int opaque_zero) {
   extern __shared__ int4 smem4[];
-  int *Gp = reinterpret_cast<int *>(smem4);
-  int *Hp = Gp + kBins * kFG;
+  int *S = reinterpret_cast<int *>(smem4);
+  char *Sb = reinterpret_cast<char *>(smem4);
   const int n_items = ctl->n_items, n_pairs = ctl->n_pairs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int half = lane & 1, rslot = lane >> 1;
   const int wq = rslot >> 2, bq = (rslot & 3) * 8;
+  // 32-bit shared address of feature 16h + ((rslot + s) & 15) in bin 0 (the shared base is folded
+  // in here once, so the inner loop never rematerialises it)
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem4);
+  uint32_t f4[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) f4[s] = sbase + 4u * (uint32_t)(16 * half + ((rslot + s) & 15));
   constexpr int RT = kHistThreads / 2;  // rows per CTA step
+  (void)opaque_zero;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int fg = item % n_fg, cg = item / n_fg;
     int lo = 0, hi = n_pairs - 1;  // largest p with chunk_base <= cg
@@ -139,9 +150,10 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
         qv = __ldg(q + kk);
       }
     };
-    // rotate the lane's 16 symbols right by `rslot` bytes (byte s = feature 16h + ((rslot+s)&15))
-    // and return the 16 x 2 atomics as a closure, so the refill load can be issued in between.
-    auto accumulate = [&](const uint4 &x, const int2 qq, int kk) {
+    // one row: rotate the lane's 16 symbols right by `rslot` bytes (byte s = feature
+    // 16h + ((rslot + s) & 15)), then 16 x 2 conflict-free shared reductions.  PRMT moves byte
+    // (s & 3) of a word to bits 8..15 with zeros elsewhere = bin * 256 (the bin's 256-B line).
+    auto accumulate = [&](const uint4 &x, const int2 qq) {
       uint32_t w[4] = {x.x, x.y, x.z, x.w};
       uint32_t t[4];
 #pragma unroll
@@ -150,46 +162,48 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
       for (int i = 0; i < 4; ++i) w[i] = (wq & 2) ? t[(i + 2) & 3] : t[i];
 #pragma unroll
       for (int i = 0; i < 4; ++i) t[i] = __funnelshift_r(w[i], w[(i + 1) & 3], bq);
-      // row slot made opaque to ptxas so it cannot hoist 16 (rslot + s) & 15 registers
-      const uint32_t ln = (uint32_t)rslot + (uint32_t)(opaque_zero * kk);
-      const uint32_t hb = (uint32_t)half << 4;
-      return [=]() {
 #pragma unroll
-        for (int s = 0; s < 16; ++s) {
-          const uint32_t bin = (t[s >> 2] >> ((s & 3) * 8)) & 0xffu;
-          const uint32_t idx = (bin << 5) | hb | ((ln + (uint32_t)s) & 15u);
-          atomicAdd(Gp + idx, qq.x);
-          atomicAdd(Hp + idx, qq.y);
-        }
-      };
+      for (int s = 0; s < 16; ++s) {
+        const uint32_t a = __byte_perm(t[s >> 2], 0u, 0x4404u | ((uint32_t)(s & 3) << 4)) + f4[s];
+        asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(qq.x));
+        asm volatile("red.shared.add.s32 [%0+128], %1;" ::"r"(a), "r"(qq.y));
+      }
     };
-    // Software pipeline over rows k, k + RT, k + 2RT, ...: two register sets A and B alternate
-    // (loop unrolled by two, no in-flight register is ever copied); a set is refilled with the
-    // row two steps ahead right after its rotation consumed it, and the row id for that refill
-    // was loaded one step earlier still.
+    // Software pipeline over rows k, k + RT, k + 2RT, ...: kDepth register sets rotate (the loop
+    // is unrolled by kDepth); a set is consumed (rotation + reductions) and only then refilled
+    // with the row kDepth steps ahead, so no in-flight register is ever copied; the row id for
+    // a refill is loaded one round earlier still.
+    constexpr int kDepth = 3;
     int k = r0 + (threadIdx.x >> 1);
-    uint4 xa = make_uint4(0, 0, 0, 0), xb = xa;
-    int2 qa = make_int2(0, 0), qb = qa;
-    int ra = 0, rb = 0;
-    if (k < r1) load_row(k, row_of(k), xa, qa);
-    if (k + RT < r1) load_row(k + RT, row_of(k + RT), xb, qb);
-    if (k + 2 * RT < r1) ra = row_of(k + 2 * RT);
-    if (k + 3 * RT < r1) rb = row_of(k + 3 * RT);
+    uint4 xs[kDepth];
+    int2 qs[kDepth];
+    int rs[kDepth];
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      xs[i] = make_uint4(0, 0, 0, 0);
+      qs[i] = make_int2(0, 0);
+      rs[i] = 0;
+      if (k + i * RT < r1) load_row(k + i * RT, row_of(k + i * RT), xs[i], qs[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i)
+      if (k + (kDepth + i) * RT < r1) rs[i] = row_of(k + (kDepth + i) * RT);
     while (k < r1) {
-      {
-        auto run = accumulate(xa, qa, k);
-        load_row(k + 2 * RT, ra, xa, qa);
-        if (k + 4 * RT < r1) ra = row_of(k + 4 * RT);
-        run();
+      bool done = false;
+#pragma unroll
+      for (int i = 0; i < kDepth; ++i) {
+        if (!done) {
+          const int kk = k + i * RT;
+          if (kk >= r1) {
+            done = true;
+          } else {
+            accumulate(xs[i], qs[i]);
+            load_row(kk + kDepth * RT, rs[i], xs[i], qs[i]);
+            if (kk + 2 * kDepth * RT < r1) rs[i] = row_of(kk + 2 * kDepth * RT);
+          }
+        }
       }
-      if (k + RT >= r1) break;
-      {
-        auto run = accumulate(xb, qb, k + RT);
-        load_row(k + 3 * RT, rb, xb, qb);
-        if (k + 5 * RT < r1) rb = row_of(k + 5 * RT);
-        run();
-      }
-      k += 2 * RT;
+      k += kDepth * RT;
     }
     __syncthreads();
     // flush: warp w owns bins [32w, 32w+32); lane l = feature l -> conflict-free reads; each lane
@@ -199,8 +213,8 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
       int4 *dst = reinterpret_cast<int4 *>(partial + (((size_t)item * kFG + lane) * kBins + bb * 32) * 2);
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
-        const int i0 = (bb * 32 + i) * kFG + lane, i1 = i0 + kFG;
-        int4 v = make_int4(Gp[i0], Hp[i0], Gp[i1], Hp[i1]);
+        const int i0 = (bb * 32 + i) * 64 + lane, i1 = i0 + 64;
+        int4 v = make_int4(S[i0], S[i0 + 32], S[i1], S[i1 + 32]);
         if (f < m) dst[i >> 1] = v;
       }
     }
@@ -282,7 +296,9 @@ __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const lo
     GL += g[i];
     HL += h[i];
     const int b = lane * 8 + i;
-    if (b <= B - 2) {
+    // an empty bin repeats the previous candidate exactly (same G_L, H_L -> same gain), which
+    // wins the tie (lower bin), so it can be skipped without changing the result
+    if (b <= B - 2 && (g[i] != 0 || h[i] != 0 || b == 0)) {
       const long long GR = G - GL, HR = H - HL;
       const double gl = __dmul_rn((double)GL, A.sg_inv), hl = __dmul_rn((double)HL, A.sh_inv);
       const double gr = __dmul_rn((double)GR, A.sg_inv), hr = __dmul_rn((double)HR, A.sh_inv);
@@ -339,12 +355,27 @@ __global__ void __launch_bounds__(256) k_eval(EvalArgs A) {
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) { g[i] = 0; h[i] = 0; }
-    for (int c = 0; c < P.n_chunks; ++c) {
-      const size_t item = (size_t)(P.chunk_base + c) * A.n_fg + j / kFG;
-      const int4 *src = reinterpret_cast<const int4 *>(A.partial + ((item * kFG + (j % kFG)) * kBins + lane * 8) * 2);
+    // sum the pair's chunk partials: 4 chunks (16 independent 16-B loads) in flight per step
+    const size_t cstride = (size_t)A.n_fg * kFG * kBins * 2;  // ints between consecutive chunks
+    const int *src0 = A.partial + (((size_t)P.chunk_base * A.n_fg + j / kFG) * kFG + (j % kFG)) * kBins * 2 + lane * 16;
+    int c = 0;
+    for (; c + 4 <= P.n_chunks; c += 4) {
+      int4 v[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[u][i] = __ldg(reinterpret_cast<const int4 *>(src0 + (c + u) * cstride) + i);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          g[2 * i] += v[u][i].x; h[2 * i] += v[u][i].y; g[2 * i + 1] += v[u][i].z; h[2 * i + 1] += v[u][i].w;
+        }
+    }
+    for (; c < P.n_chunks; ++c) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        int4 v = __ldg(src + i);
+        int4 v = __ldg(reinterpret_cast<const int4 *>(src0 + c * cstride) + i);
         g[2 * i] += v.x; h[2 * i] += v.y; g[2 * i + 1] += v.z; h[2 * i + 1] += v.w;
       }
     }
@@ -366,51 +397,70 @@ __global__ void __launch_bounds__(256) k_eval(EvalArgs A) {
 }
 
 // Split decision per node at depth d: argmax over features (ties: lowest feature, R13),
-// split iff gain > 0; children get their exact sums and Eq. 6 leaf values.
-__global__ void k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl,
-                           const Cand *__restrict__ cand, DNode *dn, const float *__restrict__ cut_values,
-                           const int *__restrict__ cut_ptrs, double sg_inv, double sh_inv,
-                           double lambda, double eta) {
-  const int lane = threadIdx.x & 31;
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int p = wid >> 1;
+// split iff gain > 0; children get their exact sums and Eq. 6 leaf values.  One 256-thread
+// block per node (blockIdx.x = 2 pair + side).
+struct BestSplit {
+  double gain;
+  int have, j, bin;
+  long long GL, HL;
+};
+__device__ __forceinline__ bool better(const BestSplit &a, const BestSplit &b) {  // a beats b
+  return a.have && (!b.have || a.gain > b.gain || (a.gain == b.gain && a.j < b.j));
+}
+__device__ __forceinline__ BestSplit shfl_best(const BestSplit &x, int o) {
+  BestSplit y;
+  y.gain = __shfl_down_sync(0xffffffffu, x.gain, o);
+  y.have = __shfl_down_sync(0xffffffffu, x.have, o);
+  y.j = __shfl_down_sync(0xffffffffu, x.j, o);
+  y.bin = __shfl_down_sync(0xffffffffu, x.bin, o);
+  y.GL = __shfl_down_sync(0xffffffffu, x.GL, o);
+  y.HL = __shfl_down_sync(0xffffffffu, x.HL, o);
+  return y;
+}
+
+__global__ void __launch_bounds__(256)
+k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Cand *__restrict__ cand,
+           DNode *dn, const float *__restrict__ cut_values, const int *__restrict__ cut_ptrs, double sg_inv,
+           double sh_inv, double lambda, double eta) {
+  const int p = blockIdx.x >> 1;
   if (p >= ctl->n_pairs) return;
   const Pair P = pairs[p];
-  const int node = (wid & 1) ? P.derived : P.built;
+  const int node = (blockIdx.x & 1) ? P.derived : P.built;
   if (node < 0) return;
   const int slot = node - level_first(d);
-  double best = 0.0;
-  int have = 0, bj = 0x7fffffff, bb = 0;
-  long long GL = 0, HL = 0;
-  for (int j = lane; j < m; j += 32) {
+  BestSplit best{0.0, 0, 0x7fffffff, 0, 0, 0};
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
     const Cand cd = cand[(size_t)slot * m + j];
-    if (cd.valid && (!have || cd.gain > best)) { have = 1; best = cd.gain; bj = j; bb = cd.bin; GL = cd.GL; HL = cd.HL; }
+    BestSplit x{cd.gain, cd.valid, j, cd.bin, cd.GL, cd.HL};
+    if (better(x, best)) best = x;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    double ob = __shfl_down_sync(0xffffffffu, best, o);
-    int oj = __shfl_down_sync(0xffffffffu, bj, o);
-    int obb = __shfl_down_sync(0xffffffffu, bb, o);
-    int oh = __shfl_down_sync(0xffffffffu, have, o);
-    long long oGL = __shfl_down_sync(0xffffffffu, GL, o);
-    long long oHL = __shfl_down_sync(0xffffffffu, HL, o);
-    bool take = oh && (!have || ob > best || (ob == best && oj < bj));
-    if (take) { best = ob; bj = oj; bb = obb; have = oh; GL = oGL; HL = oHL; }
+    BestSplit y = shfl_best(best, o);
+    if (better(y, best)) best = y;
   }
-  if (lane == 0 && have && best > 0.0) {
-    DNode &nd = dn[node];
-    nd.feature = bj;
-    nd.split_bin = bb;
-    nd.split_value = cut_values[cut_ptrs[bj] + bb];
-    nd.gain = best;
-    DNode L{}, R{};
-    L.feature = -1;
-    R.feature = -1;
-    node_fill(L, GL, HL, sg_inv, sh_inv, lambda, eta, &ctl->error);
-    node_fill(R, nd.Gq - GL, nd.Hq - HL, sg_inv, sh_inv, lambda, eta, &ctl->error);
-    dn[2 * node + 1] = L;
-    dn[2 * node + 2] = R;
-    atomicAdd(&ctl->n_splits, 1);
+  __shared__ BestSplit s_best[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) s_best[w] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int u = 1; u < (int)(blockDim.x >> 5); ++u)
+      if (better(s_best[u], best)) best = s_best[u];
+    if (best.have && best.gain > 0.0) {
+      DNode &nd = dn[node];
+      nd.feature = best.j;
+      nd.split_bin = best.bin;
+      nd.split_value = cut_values[cut_ptrs[best.j] + best.bin];
+      nd.gain = best.gain;
+      DNode L{}, R{};
+      L.feature = -1;
+      R.feature = -1;
+      node_fill(L, best.GL, best.HL, sg_inv, sh_inv, lambda, eta, &ctl->error);
+      node_fill(R, nd.Gq - best.GL, nd.Hq - best.HL, sg_inv, sh_inv, lambda, eta, &ctl->error);
+      dn[2 * node + 1] = L;
+      dn[2 * node + 2] = R;
+      atomicAdd(&ctl->n_splits, 1);
+    }
   }
 }
 
@@ -819,7 +869,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
       int64_t warps = (int64_t)max_pairs * m;
       k_eval<<<(unsigned)((warps + 7) / 8), 256, 0, c->stream>>>(A);
       OOCGB_CK(cudaGetLastError());
-      k_finalize<<<(unsigned)((max_pairs * 2 + 7) / 8), 256, 0, c->stream>>>(
+      k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, c->stream>>>(
           lv, m, w->pairs, w->ctl, w->cand, w->dnodes, d->d_cut_values, d->d_cut_ptrs, sg_inv, sh_inv,
           lambda, eta);
       OOCGB_CK(cudaGetLastError());
