@@ -132,6 +132,16 @@ def hist_algorithmic_bytes(nodes: np.ndarray, m: int) -> float:
     return rows * (m + 8 + 4) + built * m * 256 * 16.0
 
 
+def measured_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_hist launch from the committed ncu
+    --set full capture (profiles/k_hist_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k_hist_traffic.json")) as f:
+            return float(json.load(f)["traffic_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def launches_per_round(D: int) -> int:
     # update_margin 1 + logistic 1 + sample(NONE): absmax 1 + quantise 1
     # build_tree: init 1 + per level (hist, eval, finalize, part_flags, plan1, plan2, scatter) 7
@@ -318,6 +328,8 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
+    e2e_wall_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    e2e_diag = ctx.get_timings()
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -346,9 +358,12 @@ def main():
                           "launches": n_hist, "algorithmic_bytes_per_round": hist_bytes / args.steps},
             "phases_ms_per_round": {k: v / args.steps for k, v in tm.items() if k.endswith("_ms")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "k_hist",
+                         "frac": achieved / peak, "traffic": measured_traffic(), "kernel": "k_hist",
+                         "algorithmic_bytes_per_launch": hist_bytes / n_hist,
                          "peak_source": peak_src},
-            "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "wall_ms_per_step": e2e_wall_ms, "graph_captures": e2e_diag.get("graph_captures")},
+            "graph_captures_timed": tm.get("graph_captures"),
             "clocks": ck,
         }
         if cpu:

@@ -190,7 +190,7 @@ class Context:
         out = (ctypes.c_double * 16)()
         _check(load_library().oocgb_get_timings(self._h, out, 16))
         keys = ["hist_ms", "eval_ms", "partition_ms", "sample_ms", "predict_ms", "h2d_ms", "build_ms",
-                "hist_launches"]
+                "hist_launches", "hist_bytes", "graph_captures"]
         return {k: out[i] for i, k in enumerate(keys)}
 
 

@@ -21,6 +21,31 @@
 #include "internal.cuh"
 #include "stream.cuh"
 
+#include <climits>
+#include <cmath>
+
+// Per-call scalars read by the captured kernels (so one CUDA graph serves every round).
+struct RoundParams {
+  long long G, H, n_rows_global;
+  double sg_inv, sh_inv;
+  long long h_min;   // candidate valid iff H_L >= h_min and H_R >= h_min (exact form of R13)
+  float sg_inv_f, sh_inv_f;
+  int prefilter;     // 0: scales outside float's safe range -> every candidate evaluated exactly
+};
+
+struct GraphKey {
+  int n, D, m, ridx_mode, keep_debug, profiling, world;
+  double lambda, gamma, mcw, eta;
+  const void *bins;
+  size_t pitch;
+  int quant_bits;
+  bool operator==(const GraphKey &o) const {
+    return n == o.n && D == o.D && m == o.m && ridx_mode == o.ridx_mode && keep_debug == o.keep_debug &&
+           profiling == o.profiling && world == o.world && lambda == o.lambda && gamma == o.gamma &&
+           mcw == o.mcw && eta == o.eta && bins == o.bins && pitch == o.pitch && quant_bits == o.quant_bits;
+  }
+};
+
 struct Work {
   int64_t cap_rows = 0;
   int max_depth = -1, m = 0, n_fg = 0;
@@ -44,6 +69,11 @@ struct Work {
   size_t dbg_bytes = 0;
   int final_cur = 0;  // which ridx / segs buffer holds the final partition
   int hist_grid = 0;
+  RoundParams *d_rp = nullptr;     // device copy of the per-call scalars
+  RoundParams *h_rp = nullptr;     // pinned staging
+  cudaGraphExec_t graph = nullptr; // captured level loop of the last key
+  GraphKey key{};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> graph_events;  // profiling
 };
 
 namespace oocgb {
@@ -64,8 +94,8 @@ __device__ void node_fill(DNode &nd, long long Gq, long long Hq, double sg_inv, 
   nd.leaf_value = __double2float_rn(__dmul_rn(eta, w));
 }
 
-__global__ void k_init_build(DNode *dn, int n_nodes, long long G, long long H, long long n_rows_global,
-                             double sg_inv, double sh_inv, double lambda, double eta, Seg *segs,
+__global__ void k_init_build(DNode *dn, int n_nodes, const RoundParams *__restrict__ rp, double lambda,
+                             double eta, Seg *segs,
                              Pair *pairs, LevelCtl *ctl, int n_sel, int n_fg, int target_items,
                              int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
                              const int2 *q_in, int2 *q_out, int ridx_mode) {
@@ -83,8 +113,8 @@ __global__ void k_init_build(DNode *dn, int n_nodes, long long G, long long H, l
   if (tid == 0) {
     DNode r{};
     r.feature = -1;
-    r.n_rows = n_rows_global;
-    node_fill(r, G, H, sg_inv, sh_inv, lambda, eta, &ctl->error);
+    r.n_rows = rp->n_rows_global;
+    node_fill(r, rp->G, rp->H, rp->sg_inv, rp->sh_inv, lambda, eta, &ctl->error);
     dn[0] = r;
     segs[0] = Seg{0, n_sel, 0, 0};
     long long cr = ((long long)n_sel * n_fg + target_items - 1) / target_items;
@@ -261,7 +291,8 @@ struct EvalArgs {
   const int *cut_ptrs;
   DNode *dn;
   Cand *cand;
-  double lambda, gamma, mcw, sg_inv, sh_inv;
+  double lambda, gamma, mcw;
+  const RoundParams *rp;
 };
 
 __device__ __forceinline__ long long warp_excl_scan_ll(long long v, int lane, long long &total) {
@@ -275,61 +306,110 @@ __device__ __forceinline__ long long warp_excl_scan_ll(long long v, int lane, lo
   return incl - v;
 }
 
+// Exact Eq. 8 gain in double, the oracle's operation order (R14).
+__device__ __forceinline__ double gain_exact(long long GL, long long HL, long long G, long long H, double tP,
+                                             double sg_inv, double sh_inv, double lambda, double gamma) {
+  const double gl = __dmul_rn((double)GL, sg_inv), hl = __dmul_rn((double)HL, sh_inv);
+  const double gr = __dmul_rn((double)(G - GL), sg_inv), hr = __dmul_rn((double)(H - HL), sh_inv);
+  const double tL = __ddiv_rn(__dmul_rn(gl, gl), __dadd_rn(hl, lambda));
+  const double tR = __ddiv_rn(__dmul_rn(gr, gr), __dadd_rn(hr, lambda));
+  return __dsub_rn(__dmul_rn(0.5, __dsub_rn(__dadd_rn(tL, tR), tP)), gamma);
+}
+
+// EvaluateSplit of one node for feature j: lane owns bins [8 lane, 8 lane + 8).
+// 1) validity (R13) as an exact integer test: hl >= mcw and hl + lambda > 0 with hl = HL 2^-e_h
+//    exactly (power-of-two scaling) is HL >= h_min (host-derived integer threshold);
+// 2) float32 pre-filter: every candidate's gain in float with a rigorous bound tol
+//    (|gain_f - gain| <= tol, all terms non-negative); L = max(gain_f - tol) over the warp;
+// 3) exact double gains only for candidates with gain_f + tol >= L.  The exact argmax and all
+//    its exact ties always pass (gain_f + tol >= gain >= gain(c') >= gain_f(c') - tol(c')), so
+//    the result is identical to evaluating every candidate in double.
 __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const long long (&g)[8],
-                          const long long (&h)[8]) {
+                          const long long (&h)[8], const RoundParams &rp) {
   const int B = A.cut_ptrs[j + 1] - A.cut_ptrs[j];
   const long long G = A.dn[node].Gq, H = A.dn[node].Hq;
   long long lg = 0, lh = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) { lg += g[i]; lh += h[i]; }
   long long tg, th;
-  long long eg = warp_excl_scan_ll(lg, lane, tg);
-  long long eh = warp_excl_scan_ll(lh, lane, th);
-  const double gP = __dmul_rn((double)G, A.sg_inv), hP = __dmul_rn((double)H, A.sh_inv);
-  const double tP = __ddiv_rn(__dmul_rn(gP, gP), __dadd_rn(hP, A.lambda));
-  double best = 0.0;
-  int bbin = 0x7fffffff, have = 0;
-  long long bGL = 0, bHL = 0;
+  const long long eg = warp_excl_scan_ll(lg, lane, tg);
+  const long long eh = warp_excl_scan_ll(lh, lane, th);
+  const float lamf = (float)A.lambda;
+  const float gPf = (float)G * rp.sg_inv_f, hPf = (float)H * rp.sh_inv_f;
+  const float tPf = __fdiv_rn(gPf * gPf, hPf + lamf);
+  const float gamf = (float)A.gamma;
+  // pass 1: float gains + bounds
+  float gf[8], tf[8];
+  unsigned vmask = 0;
   long long GL = eg, HL = eh;
+  float Lmax = -INFINITY;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     GL += g[i];
     HL += h[i];
     const int b = lane * 8 + i;
-    // an empty bin repeats the previous candidate exactly (same G_L, H_L -> same gain), which
-    // wins the tie (lower bin), so it can be skipped without changing the result
-    if (b <= B - 2 && (g[i] != 0 || h[i] != 0 || b == 0)) {
-      const long long GR = G - GL, HR = H - HL;
-      const double gl = __dmul_rn((double)GL, A.sg_inv), hl = __dmul_rn((double)HL, A.sh_inv);
-      const double gr = __dmul_rn((double)GR, A.sg_inv), hr = __dmul_rn((double)HR, A.sh_inv);
-      const double dl = __dadd_rn(hl, A.lambda), dr = __dadd_rn(hr, A.lambda);
-      if (hl >= A.mcw && hr >= A.mcw && dl > 0.0 && dr > 0.0) {
-        const double tL = __ddiv_rn(__dmul_rn(gl, gl), dl);
-        const double tR = __ddiv_rn(__dmul_rn(gr, gr), dr);
-        const double gain = __dsub_rn(__dmul_rn(0.5, __dsub_rn(__dadd_rn(tL, tR), tP)), A.gamma);
-        if (!have || gain > best) { have = 1; best = gain; bbin = b; bGL = GL; bHL = HL; }
-      }
+    // an empty bin repeats the previous candidate exactly, which wins the tie (lower bin)
+    const bool v = b <= B - 2 && (g[i] != 0 || h[i] != 0 || b == 0) && HL >= rp.h_min && (H - HL) >= rp.h_min;
+    gf[i] = -INFINITY;
+    tf[i] = 0.f;
+    if (v) {
+      vmask |= 1u << i;
+      const float gl = (float)GL * rp.sg_inv_f, hl = (float)HL * rp.sh_inv_f;
+      const float gr = (float)(G - GL) * rp.sg_inv_f, hr = (float)(H - HL) * rp.sh_inv_f;
+      const float tL = __fdiv_rn(gl * gl, hl + lamf);
+      const float tR = __fdiv_rn(gr * gr, hr + lamf);
+      const float gain = 0.5f * ((tL + tR) - tPf) - gamf;
+      // each float op adds <= 2^-24 relative error; <= 12 ops touch any term: 2^-18 is >= 4x
+      // that bound on |tL| + |tR| + |tP| + |gamma|; non-finite -> always re-evaluate exactly
+      float tol = 0x1p-18f * (fabsf(tL) + fabsf(tR) + fabsf(tPf) + fabsf(gamf)) + 0x1p-100f;
+      if (!isfinite(gain) || !isfinite(tol) || !rp.prefilter) tol = INFINITY;
+      gf[i] = gain;
+      tf[i] = tol;
+      Lmax = fmaxf(Lmax, gain - tol);
     }
   }
-  // warp argmax: larger gain, then lower bin
+#pragma unroll
+  for (int o = 16; o; o >>= 1) Lmax = fmaxf(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, o));
+  // pass 2: exact double gains of the survivors
+  double tP = 0.0;
+  {
+    const double gP = __dmul_rn((double)G, rp.sg_inv), hP = __dmul_rn((double)H, rp.sh_inv);
+    tP = __ddiv_rn(__dmul_rn(gP, gP), __dadd_rn(hP, A.lambda));
+  }
+  double best = 0.0;
+  int bbin = 0x7fffffff, have = 0;
+  long long bGL = 0, bHL = 0;
+  GL = eg;
+  HL = eh;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    GL += g[i];
+    HL += h[i];
+    if (((vmask >> i) & 1u) && gf[i] + tf[i] >= Lmax) {
+      const double gain = gain_exact(GL, HL, G, H, tP, rp.sg_inv, rp.sh_inv, A.lambda, A.gamma);
+      if (!have || gain > best) { have = 1; best = gain; bbin = lane * 8 + i; bGL = GL; bHL = HL; }
+    }
+  }
+  // warp argmax over (gain, bin): larger gain, then lower bin; invalid = -inf.  Only the pair is
+  // shuffled; the lane that owns the winning bin writes its own G_L, H_L.
+  double bg = have ? best : -INFINITY;
+  int bb = have ? bbin : 0x7fffffff;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    double ob = __shfl_down_sync(0xffffffffu, best, o);
-    int obin = __shfl_down_sync(0xffffffffu, bbin, o);
-    int ohave = __shfl_down_sync(0xffffffffu, have, o);
-    long long oGL = __shfl_down_sync(0xffffffffu, bGL, o);
-    long long oHL = __shfl_down_sync(0xffffffffu, bHL, o);
-    bool take = ohave && (!have || ob > best || (ob == best && obin < bbin));
-    if (take) { best = ob; bbin = obin; have = ohave; bGL = oGL; bHL = oHL; }
+    const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+    const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+    if (og > bg || (og == bg && ob < bb)) { bg = og; bb = ob; }
   }
-  if (lane == 0) {
+  const bool any = bb != 0x7fffffff;
+  const int owner = any ? (bb >> 3) : 0;
+  if (lane == owner) {
     const int slot = node - level_first(A.d);
     Cand cd;
-    cd.gain = best;
-    cd.bin = bbin;
-    cd.valid = have;
-    cd.GL = bGL;
-    cd.HL = bHL;
+    cd.gain = any ? bg : 0.0;
+    cd.bin = bb;
+    cd.valid = any ? 1 : 0;
+    cd.GL = any ? bGL : 0;
+    cd.HL = any ? bHL : 0;
     A.cand[(size_t)slot * A.m + j] = cd;
   }
 }
@@ -340,7 +420,7 @@ __device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)
   for (int i = 0; i < 8; ++i) d2[i] = make_longlong2(g[i], h[i]);
 }
 
-__global__ void __launch_bounds__(256) k_eval(EvalArgs A) {
+__global__ void __launch_bounds__(256, 2) k_eval(EvalArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int p = (int)(wid / A.m), j = (int)(wid % A.m);
@@ -355,24 +435,24 @@ __global__ void __launch_bounds__(256) k_eval(EvalArgs A) {
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) { g[i] = 0; h[i] = 0; }
-    // sum the pair's chunk partials: 4 chunks (16 independent 16-B loads) in flight per step
+    // sum the pair's chunk partials: 2 chunks (8 independent 16-B loads) in flight per step
     const size_t cstride = (size_t)A.n_fg * kFG * kBins * 2;  // ints between consecutive chunks
     const int *src0 = A.partial + (((size_t)P.chunk_base * A.n_fg + j / kFG) * kFG + (j % kFG)) * kBins * 2 + lane * 16;
     int c = 0;
-    for (; c + 4 <= P.n_chunks; c += 4) {
-      int4 v[4][4];
+    for (; c + 2 <= P.n_chunks; c += 2) {
+      int4 v[2][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int i = 0; i < 4; ++i) v[u][i] = __ldg(reinterpret_cast<const int4 *>(src0 + (c + u) * cstride) + i);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           g[2 * i] += v[u][i].x; h[2 * i] += v[u][i].y; g[2 * i + 1] += v[u][i].z; h[2 * i + 1] += v[u][i].w;
         }
     }
-    for (; c < P.n_chunks; ++c) {
+    if (c < P.n_chunks) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         int4 v = __ldg(reinterpret_cast<const int4 *>(src0 + c * cstride) + i);
@@ -384,7 +464,8 @@ __global__ void __launch_bounds__(256) k_eval(EvalArgs A) {
   const int f_d = level_first(A.d);
   if (keep) store_hist8(A.phist_next + (size_t)(P.built - f_d) * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
   if (A.dbg) store_hist8(A.dbg + (size_t)P.built * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
-  eval_node(A, P.built, j, lane, g, h);
+  const RoundParams rp = *A.rp;
+  eval_node(A, P.built, j, lane, g, h, rp);
   if (P.derived >= 0) {
     const int ps = P.parent - level_first(A.d - 1);
     const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + ((size_t)j * kBins + lane * 8) * 2);
@@ -392,7 +473,7 @@ __global__ void __launch_bounds__(256) k_eval(EvalArgs A) {
     for (int i = 0; i < 8; ++i) { longlong2 v = src[i]; g[i] = v.x - g[i]; h[i] = v.y - h[i]; }
     if (keep) store_hist8(A.phist_next + (size_t)(P.derived - f_d) * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
     if (A.dbg) store_hist8(A.dbg + (size_t)P.derived * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
-    eval_node(A, P.derived, j, lane, g, h);
+    eval_node(A, P.derived, j, lane, g, h, rp);
   }
 }
 
@@ -420,8 +501,8 @@ __device__ __forceinline__ BestSplit shfl_best(const BestSplit &x, int o) {
 
 __global__ void __launch_bounds__(256)
 k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Cand *__restrict__ cand,
-           DNode *dn, const float *__restrict__ cut_values, const int *__restrict__ cut_ptrs, double sg_inv,
-           double sh_inv, double lambda, double eta) {
+           DNode *dn, const float *__restrict__ cut_values, const int *__restrict__ cut_ptrs,
+           const RoundParams *__restrict__ rp, double lambda, double eta) {
   const int p = blockIdx.x >> 1;
   if (p >= ctl->n_pairs) return;
   const Pair P = pairs[p];
@@ -455,8 +536,8 @@ k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Ca
       DNode L{}, R{};
       L.feature = -1;
       R.feature = -1;
-      node_fill(L, best.GL, best.HL, sg_inv, sh_inv, lambda, eta, &ctl->error);
-      node_fill(R, nd.Gq - best.GL, nd.Hq - best.HL, sg_inv, sh_inv, lambda, eta, &ctl->error);
+      node_fill(L, best.GL, best.HL, rp->sg_inv, rp->sh_inv, lambda, eta, &ctl->error);
+      node_fill(R, nd.Gq - best.GL, nd.Hq - best.HL, rp->sg_inv, rp->sh_inv, lambda, eta, &ctl->error);
       dn[2 * node + 1] = L;
       dn[2 * node + 2] = R;
       atomicAdd(&ctl->n_splits, 1);
@@ -756,7 +837,7 @@ static void ensure_work(oocgb_data d, int D) {
   const int64_t n = std::max<int64_t>(1, d->n_sel);
   const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
   const int hist_grid = c->num_sms * 3;
-  const int target = 2 * hist_grid;
+  const int target = hist_grid;
   const int64_t max_pairs = D > 0 ? (1LL << (D - 1)) : 1;
   int64_t items = std::max<int64_t>(target, (int64_t)n_fg * ((n + kmax - 1) / kmax)) + (int64_t)n_fg * (1 + max_pairs) + n_fg;
   if (w && w->cap_rows >= n && w->max_depth >= D && w->m == m && w->items_cap >= items) return;
@@ -791,8 +872,12 @@ static void ensure_work(oocgb_data d, int D) {
   w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)max_pairs * 2 * m);
   w->dnodes = (DNode *)dmalloc(sizeof(DNode) * ((1LL << (D + 1)) - 1));
   w->ctl = (LevelCtl *)dmalloc(sizeof(LevelCtl));
+  w->d_rp = (RoundParams *)dmalloc(sizeof(RoundParams));
+  OOCGB_CK(cudaMallocHost(&w->h_rp, sizeof(RoundParams)));
   OOCGB_CK(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem));
 }
+
+static void drop_graph(Work *w);
 
 void free_work(oocgb_data d) {
   Work *w = d->work;
@@ -800,9 +885,121 @@ void free_work(oocgb_data d) {
   for (int i = 0; i < 2; ++i) { dfree(w->ridx[i]); dfree(w->q[i]); dfree(w->segs[i]); dfree(w->phist[i]); }
   dfree(w->flagbits); dfree(w->tile_cnt); dfree(w->tile_off); dfree(w->bpart); dfree(w->seg_nr);
   dfree(w->seg_grb); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
-  dfree(w->cand); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg);
+  dfree(w->cand); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg); dfree(w->d_rp);
+  if (w->h_rp) cudaFreeHost(w->h_rp);
+  drop_graph(w);
   delete w;
   d->work = nullptr;
+}
+
+// Records the whole device side of one build_tree on the ctx stream (captured into a graph).
+// `tev` collects (slot, event pair) for profiling; events are recorded only if non-null.
+static void record_build(oocgb_data d, int D, double lambda, double gamma, double mcw, double eta,
+                         bool keep_debug, const uint8_t *bins, size_t pitch, int ridx_mode,
+                         std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> *tev) {
+  oocgb_ctx c = d->ctx;
+  Work *w = d->work;
+  const int m = d->m, n_fg = w->n_fg;
+  const int n = (int)d->n_sel;
+  const int n_nodes = (1 << (D + 1)) - 1;
+  const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
+  const int target = w->hist_grid;  // one wave of items per level
+  const size_t hsz = (size_t)m * kBins * 2;
+  auto mark = [&](int slot, bool begin) {
+    if (!tev) return;
+    if (begin) {
+      cudaEvent_t a, b;
+      OOCGB_CK(cudaEventCreate(&a));
+      OOCGB_CK(cudaEventCreate(&b));
+      tev->push_back({slot, {a, b}});
+      // external event nodes behave like ordinary stream records (timable) when replayed
+      OOCGB_CK(cudaEventRecordWithFlags(a, c->stream, cudaEventRecordExternal));
+    } else {
+      OOCGB_CK(cudaEventRecordWithFlags(tev->back().second.second, c->stream, cudaEventRecordExternal));
+    }
+  };
+  if (keep_debug) OOCGB_CK(cudaMemsetAsync(w->dbg, 0, sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1), c->stream));
+  OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
+  k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
+      w->dnodes, n_nodes, w->d_rp, lambda, eta, w->segs[0], w->pairs, w->ctl, n, n_fg, target, kmax, D,
+      d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode);
+  OOCGB_CK(cudaGetLastError());
+  int cur = 0;
+  const int tiles = (n + kPartTile - 1) / kPartTile;
+  for (int lv = 0; lv < D; ++lv) {
+    const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
+    mark(0, true);
+    k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur], w->q[cur],
+                                                                 w->pairs, w->ctl, w->partial,
+                                                                 (lv == 0 && ridx_mode == 0) ? 1 : 0, 0);
+    OOCGB_CK(cudaGetLastError());
+    mark(0, false);
+    if (c->world > 1) {
+      int64_t tot = (int64_t)max_pairs * m * kBins;
+      k_reduce_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
+          w->partial, w->pairs, w->ctl, m, n_fg, w->built64);
+      allreduce_sum_i64(c, w->built64, hsz * max_pairs);
+    }
+    mark(1, true);
+    EvalArgs A;
+    A.d = lv; A.D = D; A.m = m; A.n_fg = n_fg;
+    A.pairs = w->pairs; A.ctl = w->ctl; A.partial = w->partial;
+    A.built64 = c->world > 1 ? w->built64 : nullptr;
+    A.phist_prev = w->phist[(lv + 1) & 1];
+    A.phist_next = w->phist[lv & 1];
+    A.dbg = keep_debug ? w->dbg : nullptr;
+    A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
+    A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp;
+    const int64_t warps = (int64_t)max_pairs * m;
+    k_eval<<<(unsigned)((warps + 7) / 8), 256, 0, c->stream>>>(A);
+    OOCGB_CK(cudaGetLastError());
+    k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, c->stream>>>(lv, m, w->pairs, w->ctl, w->cand, w->dnodes,
+                                                                 d->d_cut_values, d->d_cut_ptrs, w->d_rp, lambda,
+                                                                 eta);
+    OOCGB_CK(cudaGetLastError());
+    mark(1, false);
+    mark(2, true);
+    if (n > 0) {
+      k_part_flags<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
+                                                          w->ridx[cur], w->flagbits, w->tile_cnt, w->bpart);
+      OOCGB_CK(cudaGetLastError());
+    }
+    k_part_plan1<<<1, 1024, 0, c->stream>>>(n, tiles, w->segs[cur], w->ctl, w->tile_cnt, w->tile_off, w->bpart,
+                                            w->seg_nr, w->seg_grb, w->seg_cnt);
+    OOCGB_CK(cudaGetLastError());
+    if (c->world > 1) allreduce_sum_i64(c, w->seg_cnt, 2 * (size_t)(1 << lv));
+    k_part_plan2<<<1, 1024, 0, c->stream>>>(w->segs[cur], w->segs[cur ^ 1], w->ctl, w->dnodes, w->seg_nr,
+                                            w->seg_cnt, w->pairs, n_fg, target, kmax);
+    OOCGB_CK(cudaGetLastError());
+    if (n > 0) {
+      k_part_scatter<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->flagbits, w->tile_off,
+                                                            w->seg_nr, w->seg_grb, w->ridx[cur], w->q[cur],
+                                                            w->ridx[cur ^ 1], w->q[cur ^ 1]);
+      OOCGB_CK(cudaGetLastError());
+    }
+    mark(2, false);
+    cur ^= 1;
+  }
+  w->final_cur = cur;
+}
+
+static void add_graph_timings(oocgb_ctx c, Work *w) {
+  for (auto &e : w->graph_events) {
+    float ms = 0.f;
+    OOCGB_CK(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+    c->timings[e.first] += ms;
+    if (e.first == 0) c->timings[7] += 1.0;
+  }
+}
+
+static void drop_graph(Work *w) {
+  if (w->graph) cudaGraphExecDestroy(w->graph);
+  w->graph = nullptr;
+  for (auto &e : w->graph_events) {
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  w->graph_events.clear();
 }
 
 oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double mcw, double eta,
@@ -811,12 +1008,9 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   PhaseTimer whole(c, 6);
   ensure_work(d, D);
   Work *w = d->work;
-  const int m = d->m, n_fg = w->n_fg;
+  const int m = d->m;
   const int n = (int)d->n_sel;
   const int n_nodes = (1 << (D + 1)) - 1;
-  const double sg_inv = ldexp(1.0, -d->e_g), sh_inv = ldexp(1.0, -d->e_h);
-  const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
-  const int target = 2 * w->hist_grid;
   const size_t hsz = (size_t)m * kBins * 2;
   const uint8_t *bins;
   int ridx_mode;
@@ -828,77 +1022,52 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   }
   if (keep_debug) {
     size_t need = sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1);
-    if (w->dbg_bytes < need) { dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
-    OOCGB_CK(cudaMemsetAsync(w->dbg, 0, need, c->stream));
+    if (w->dbg_bytes < need) { drop_graph(w); dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
   }
-  OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
-  k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
-      w->dnodes, n_nodes, d->G_root, d->H_root, d->n_sel_global, sg_inv, sh_inv, lambda, eta,
-      w->segs[0], w->pairs, w->ctl, n, n_fg, target, kmax, D, d->d_sel_rows, w->ridx[0], d->d_q,
-      w->q[0], ridx_mode);
-  OOCGB_CK(cudaGetLastError());
-  int cur = 0;
-  const int tiles = (n + kPartTile - 1) / kPartTile;
-  double hist_bytes = 0.0;
-  for (int lv = 0; lv < D; ++lv) {
-    const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
-    {
-      PhaseTimer t(c, 0);
-      k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur],
-                                                                   w->q[cur], w->pairs, w->ctl, w->partial,
-                                                                   (lv == 0 && ridx_mode == 0) ? 1 : 0, 0);
-      OOCGB_CK(cudaGetLastError());
-    }
-    if (c->world > 1) {
-      int64_t tot = (int64_t)max_pairs * m * kBins;
-      k_reduce_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
-          w->partial, w->pairs, w->ctl, m, n_fg, w->built64);
-      allreduce_sum_i64(c, w->built64, hsz * max_pairs);
-    }
-    {
-      PhaseTimer t(c, 1);
-      EvalArgs A;
-      A.d = lv; A.D = D; A.m = m; A.n_fg = n_fg;
-      A.pairs = w->pairs; A.ctl = w->ctl; A.partial = w->partial;
-      A.built64 = c->world > 1 ? w->built64 : nullptr;
-      A.phist_prev = w->phist[(lv + 1) & 1];
-      A.phist_next = w->phist[lv & 1];
-      A.dbg = keep_debug ? w->dbg : nullptr;
-      A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
-      A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.sg_inv = sg_inv; A.sh_inv = sh_inv;
-      int64_t warps = (int64_t)max_pairs * m;
-      k_eval<<<(unsigned)((warps + 7) / 8), 256, 0, c->stream>>>(A);
-      OOCGB_CK(cudaGetLastError());
-      k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, c->stream>>>(
-          lv, m, w->pairs, w->ctl, w->cand, w->dnodes, d->d_cut_values, d->d_cut_ptrs, sg_inv, sh_inv,
-          lambda, eta);
-      OOCGB_CK(cudaGetLastError());
-    }
-    {
-      PhaseTimer t(c, 2);
-      if (n > 0) {
-        k_part_flags<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
-                                                            w->ridx[cur], w->flagbits, w->tile_cnt, w->bpart);
-        OOCGB_CK(cudaGetLastError());
-      }
-      k_part_plan1<<<1, 1024, 0, c->stream>>>(n, tiles, w->segs[cur], w->ctl, w->tile_cnt, w->tile_off,
-                                              w->bpart, w->seg_nr, w->seg_grb, w->seg_cnt);
-      OOCGB_CK(cudaGetLastError());
-      if (c->world > 1) allreduce_sum_i64(c, w->seg_cnt, 2 * (size_t)(1 << lv));
-      k_part_plan2<<<1, 1024, 0, c->stream>>>(w->segs[cur], w->segs[cur ^ 1], w->ctl, w->dnodes, w->seg_nr,
-                                              w->seg_cnt, w->pairs, n_fg, target, kmax);
-      OOCGB_CK(cudaGetLastError());
-      if (n > 0) {
-        k_part_scatter<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->flagbits,
-                                                              w->tile_off, w->seg_nr, w->seg_grb,
-                                                              w->ridx[cur], w->q[cur], w->ridx[cur ^ 1],
-                                                              w->q[cur ^ 1]);
-        OOCGB_CK(cudaGetLastError());
-      }
-    }
-    cur ^= 1;
+  // per-call scalars -> device (ordered before the graph on the ctx stream)
+  w->h_rp->G = d->G_root;
+  w->h_rp->H = d->H_root;
+  w->h_rp->n_rows_global = d->n_sel_global;
+  w->h_rp->sg_inv = ldexp(1.0, -d->e_g);
+  w->h_rp->sh_inv = ldexp(1.0, -d->e_h);
+  w->h_rp->sg_inv_f = ldexpf(1.0f, -d->e_g);
+  w->h_rp->sh_inv_f = ldexpf(1.0f, -d->e_h);
+  // float pre-filter only while 2^-e and the dequantised sums stay well inside float's normal range
+  w->h_rp->prefilter = (std::abs(d->e_g) <= 60 && std::abs(d->e_h) <= 60) ? 1 : 0;
+  {
+    // R13 exactly, in integers: hl = HL 2^-e_h is exact, so hl >= mcw <=> HL >= ceil(mcw 2^e_h)
+    // and hl + lambda > 0 <=> HL >= floor(-lambda 2^e_h) + 1 (clamped to the int64 range)
+    auto clampll = [](double x) -> long long {
+      if (!(x > -9.0e18)) return LLONG_MIN / 2;
+      if (!(x < 9.0e18)) return LLONG_MAX / 2;
+      return (long long)x;
+    };
+    const long long t1 = clampll(ceil(ldexp(mcw, d->e_h)));
+    const long long t2 = clampll(floor(ldexp(-lambda, d->e_h))) + 1;
+    w->h_rp->h_min = std::max(t1, t2);
   }
-  w->final_cur = cur;
+  OOCGB_CK(cudaMemcpyAsync(w->d_rp, w->h_rp, sizeof(RoundParams), cudaMemcpyHostToDevice, c->stream));
+  GraphKey key{n, D, m, ridx_mode, keep_debug ? 1 : 0, c->profiling ? 1 : 0, c->world, lambda, gamma, mcw, eta,
+               bins, pitch, d->quant_bits};
+  if (!w->graph || !(w->key == key)) {
+    drop_graph(w);
+    cudaGraph_t g;
+    OOCGB_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      record_build(d, D, lambda, gamma, mcw, eta, keep_debug, bins, pitch, ridx_mode,
+                   c->profiling ? &w->graph_events : nullptr);
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &g);
+      throw;
+    }
+    OOCGB_CK(cudaStreamEndCapture(c->stream, &g));
+    OOCGB_CK(cudaGraphInstantiate(&w->graph, g, 0));
+    cudaGraphDestroy(g);
+    w->key = key;
+    c->timings[9] += 1.0;  // graph captures (diagnostic)
+  }
+  OOCGB_CK(cudaGraphLaunch(w->graph, c->stream));
+  const int cur = w->final_cur;
   // export
   std::vector<DNode> hn(n_nodes);
   LevelCtl hctl;
@@ -906,6 +1075,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   OOCGB_CK(cudaMemcpyAsync(&hctl, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
   OOCGB_CK(cudaStreamSynchronize(c->stream));
   OOCGB_REQUIRE(hctl.error == 0, OOCGB_ERR_ARG, "build_tree: H + lambda <= 0 at a node (S:L406)");
+  if (c->profiling) add_graph_timings(c, w);
   oocgb_tree t = new oocgb_tree_s();
   t->owner = d;
   t->serial = ++d->tree_serial;
