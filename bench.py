@@ -231,7 +231,10 @@ def main():
         import torch.distributed as tdist
         tdist.barrier()
     torch.cuda.set_device(local)
-    stream = torch.cuda.current_stream()
+    # one dedicated (non-default) stream shared by torch and the library: the library enqueues
+    # on it, the CUDA events below are recorded on it, and the build_tree graph is captured on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     nid = None
     if world > 1:
         import torch.distributed as tdist
@@ -253,7 +256,7 @@ def main():
             d.update_margin(prev_tree, margin)
             prev_tree.close()
         d.set_logistic_gradients(margin, yd)
-        d.sample(ob.SAMPLE_NONE, 1.0, round=r, quant_bits=QBITS)
+        d.sample(ob.SAMPLE_NONE, 1.0, round=r, quant_bits=QBITS, want_info=False)
         return d.build_tree(DEPTH, LAMBDA, GAMMA, MCW, ETA)
 
     tree = None
@@ -274,17 +277,16 @@ def main():
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    hist_bytes = 0.0
-    hist_rowfeat = 0.0
+    exported = []
     for _ in range(args.steps):
         tree = round_device(tree, r)
-        nodes = tree.export()
-        hist_bytes += hist_algorithmic_bytes(nodes, N_FEAT)
-        hist_rowfeat += hist_rows(nodes)[0] * N_FEAT
+        exported.append(tree.export())   # the tree a user gets back (C call + copy)
         r += 1
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    hist_bytes = sum(hist_algorithmic_bytes(nd, N_FEAT) for nd in exported)
+    hist_rowfeat = sum(hist_rows(nd)[0] * N_FEAT for nd in exported)
     tm = ctx.get_timings()
     ctx.set_profiling(False)
     ck = clocks.stop()
@@ -309,7 +311,7 @@ def main():
             d.update_margin(prev_tree, m_host)      # H2D + D2H of the margin
             prev_tree.close()
         d.set_logistic_gradients(m_host, y_host)    # H2D of margin + labels
-        d.sample(ob.SAMPLE_NONE, 1.0, round=r_, quant_bits=QBITS)
+        d.sample(ob.SAMPLE_NONE, 1.0, round=r_, quant_bits=QBITS, want_info=False)
         t = d.build_tree(DEPTH, LAMBDA, GAMMA, MCW, ETA)
         t.export()                                  # D2H of the tree
         return t

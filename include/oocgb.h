@@ -17,8 +17,11 @@
  *    (distinguished with cudaPointerGetAttributes); they are borrowed for the duration of the
  *    call only.  Anything the library keeps, it copies.  Host output buffers are caller-
  *    allocated with the sizes stated per call.
- *  - All device work is ordered on the context's stream; every call returns when its results
- *    are visible to the host (synchronous boundary, pipelining happens inside).
+ *  - All device work is ordered on the context's stream.  A call that reads or writes HOST
+ *    buffers returns when they may be reused / read; a call whose caller buffers are all DEVICE
+ *    pointers is stream-ordered (it may return before the device work finishes; the next call,
+ *    or any work the caller enqueues on the same stream, sees its results).  oocgb_build_tree
+ *    and oocgb_sample with a non-NULL info always synchronise (their outputs live on the host).
  *  - Handles are library-owned; free them with the matching *_destroy.
  *  - One owner thread per context (not thread-safe); exported trees are immutable.
  */
@@ -67,7 +70,7 @@ typedef struct {
   int64_t n_rows_global;  /* rows over all ranks                                             */
   int64_t row0_global;    /* global id of this rank's first row                              */
   int32_t n_features;     /* m                                                               */
-  int32_t row_stride;     /* bytes per ELLPACK row = ceil16(m) (R5)                          */
+  int32_t row_stride;     /* bytes per ELLPACK row = 32 ceil(m / 32) (R5; tiled pages)        */
   int32_t max_bin;
   int32_t placement;      /* OOCGB_PLACE_*                                                   */
   int64_t n_pages;        /* ELLPACK pages (1 for a single device page)                      */
@@ -144,7 +147,8 @@ int oocgb_set_logistic_gradients(oocgb_data data, const float *margin, const flo
  * q = rint(x 2^e), e = quant_bits - k with frexp(max|x|) = (., k); quant_bits in [8, 25].
  * For PINNED_HOST data this also compacts the selected rows of every page into one device
  * page (Alg. 7).  ERR_ARG: ratio not in (0, 1], bad mode/quant_bits; ERR_STATE:
- * no gradients; ERR_NOMEM: sampled page does not fit (lower ratio).  info may be NULL.     */
+ * no gradients; ERR_NOMEM: sampled page does not fit (lower ratio).  info may be NULL: then
+ * the f = 1 in-core path runs without any host synchronisation.                           */
 int oocgb_sample(oocgb_data data, int32_t mode, double ratio, double mvs_lambda, uint64_t seed,
                  uint64_t round, int32_t quant_bits, oocgb_sample_info *info);
 

@@ -239,7 +239,11 @@ class Data:
         _check(load_library().oocgb_set_logistic_gradients(self._h, pm, py, int(margin.shape[0])))
 
     def sample(self, mode: int = SAMPLE_NONE, ratio: float = 1.0, mvs_lambda: float = 1.0, seed: int = 1,
-               round: int = 0, quant_bits: int = 16) -> dict:
+               round: int = 0, quant_bits: int = 16, want_info: bool = True):
+        """Sample(g) + fixed point.  want_info=False skips the host synchronisation (returns None)."""
+        if not want_info:
+            _check(load_library().oocgb_sample(self._h, mode, ratio, mvs_lambda, seed, round, quant_bits, None))
+            return None
         si = SampleInfo()
         _check(load_library().oocgb_sample(self._h, mode, ratio, mvs_lambda, seed, round, quant_bits,
                                             ctypes.byref(si)))

@@ -31,6 +31,20 @@ void *dmalloc(size_t bytes) {
 void dfree(void *p) {
   if (p) cudaFree(p);
 }
+void *pool_get(oocgb_ctx c, size_t bytes) {
+  for (size_t i = 0; i < c->node_pool.size(); ++i)
+    if (c->node_pool[i].first == bytes) {
+      void *p = c->node_pool[i].second;
+      c->node_pool.erase(c->node_pool.begin() + (long)i);
+      return p;
+    }
+  return dmalloc(bytes);
+}
+void pool_put(oocgb_ctx c, size_t bytes, void *p) {
+  if (!p) return;
+  if (c->node_pool.size() >= 4096) { dfree(p); return; }
+  c->node_pool.push_back({bytes, p});
+}
 bool is_device_ptr(const void *p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -319,6 +333,7 @@ int oocgb_ctx_destroy(oocgb_ctx c) {
   for (auto e : c->pending_b) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->copy_stream);
+  for (auto &p : c->node_pool) cudaFree(p.second);
   cudaFree(c->d_small);
   cudaFreeHost(c->h_small);
   delete c;
@@ -472,8 +487,8 @@ int oocgb_set_gradients(oocgb_data d, const float *g, const float *h, int64_t n_
   if (n_local > 0) {
     OOCGB_CK(cudaMemcpyAsync(d->d_g, g, sizeof(float) * n_local, cudaMemcpyDefault, c->stream));
     OOCGB_CK(cudaMemcpyAsync(d->d_h, h, sizeof(float) * n_local, cudaMemcpyDefault, c->stream));
+    if (!is_device_ptr(g) || !is_device_ptr(h)) OOCGB_CK(cudaStreamSynchronize(c->stream));
   }
-  OOCGB_CK(cudaStreamSynchronize(c->stream));
   d->has_grad = true;
   d->has_sample = false;
   API_END
@@ -491,8 +506,8 @@ int oocgb_set_logistic_gradients(oocgb_data d, const float *margin, const float 
     view_on_device(c, margin, sizeof(float) * n_local, vm);
     view_on_device(c, labels, sizeof(float) * n_local, vy);
     logistic_gradients(d, (const float *)vm.ptr, (const float *)vy.ptr);
+    if (vm.owned || vy.owned) OOCGB_CK(cudaStreamSynchronize(c->stream));
   }
-  OOCGB_CK(cudaStreamSynchronize(c->stream));
   d->has_grad = true;
   d->has_sample = false;
   API_END
@@ -541,7 +556,8 @@ int oocgb_tree_export(oocgb_tree t, oocgb_node *nodes, int32_t capacity, int32_t
 int oocgb_tree_destroy(oocgb_tree t) {
   API_BEGIN
   OOCGB_REQUIRE(t, OOCGB_ERR_ARG, "tree is NULL");
-  dfree(t->d_pnodes);
+  // stream-ordered reuse: later users of the buffer run after every kernel already enqueued
+  pool_put(t->ctx, t->pnodes_bytes, t->d_pnodes);
   delete t;
   API_END
 }
@@ -581,7 +597,7 @@ int oocgb_predict(oocgb_data d, const oocgb_tree *trees, int32_t n_trees, float 
     if (!dev) dfree(dm);
     throw;
   }
-  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  if (d->placement == OOCGB_PLACE_PINNED_HOST) OOCGB_CK(cudaStreamSynchronize(c->stream));  // staging reuse
   API_END
 }
 

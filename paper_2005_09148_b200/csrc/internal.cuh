@@ -105,6 +105,15 @@ struct Cand {
   long long GL, HL;
 };
 
+// Device-resident result of oocgb_sample (R12): fixed-point exponents, root sums, counts.
+// Written by the sample kernels, read by build_tree's first kernel — no host round trip.
+struct SampleState {
+  unsigned long long maxbits[2];  // max |g'|, max |h'| as double bit patterns (all ranks)
+  long long G, H;                 // fixed-point root sums (all ranks)
+  long long n_sel_local, n_sel_global;
+  int e_g, e_h, quant_bits, pad;
+};
+
 struct LevelCtl {       // device-resident control block of one build
   int n_pairs;
   int n_items;
@@ -144,6 +153,7 @@ struct oocgb_ctx_s {
   std::vector<cudaEvent_t> ev_pool;          // recycled events
   std::vector<int> pending_slot;             // (slot, event a, event b) recorded, not yet read
   std::vector<cudaEvent_t> pending_a, pending_b;
+  std::vector<std::pair<size_t, void *>> node_pool;  // recycled tree node buffers (no cudaFree sync)
   // scratch for small host<->device exchanges
   void *d_small = nullptr;   // 1 MB device scratch
   void *h_small = nullptr;   // 1 MB pinned scratch
@@ -184,7 +194,9 @@ struct oocgb_data_s {
   int32_t *d_sel_rows = nullptr;   // local row ids, ascending
   int2 *d_q = nullptr;             // (q_g, q_h), |q| <= 2^quant_bits
   int32_t e_g = 0, e_h = 0, quant_bits = 16;
-  long long G_root = 0, H_root = 0;
+  long long G_root = 0, H_root = 0;   // host mirrors, valid after a synchronising sample
+  oocgb::SampleState *d_ss = nullptr; // device sample state (always valid after sample)
+  oocgb::SampleState *h_ss = nullptr; // pinned mirror
   uint8_t *d_sampled_page = nullptr;  // PINNED_HOST: compacted selected rows (Alg. 7)
   int64_t sampled_cap = 0;
   int64_t sel_cap = 0;
@@ -202,6 +214,8 @@ struct oocgb_data_s {
 
 struct oocgb_tree_s {
   oocgb_data owner = nullptr;
+  oocgb_ctx ctx = nullptr;
+  size_t pnodes_bytes = 0;
   uint64_t serial = 0;
   int32_t max_depth = 0;
   std::vector<oocgb_node> nodes;
@@ -217,6 +231,8 @@ namespace oocgb {
 // Host-side launchers, one per kernel family (quantise.cu, sample.cu, tree.cu).
 void set_last_error(const std::string &msg);
 void *dmalloc(size_t bytes);
+void *pool_get(oocgb_ctx c, size_t bytes);   // device buffer from the ctx pool (or cudaMalloc)
+void pool_put(oocgb_ctx c, size_t bytes, void *p);
 void dfree(void *p);
 bool is_device_ptr(const void *p);
 

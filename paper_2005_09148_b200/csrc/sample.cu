@@ -155,7 +155,7 @@ __global__ void k_select_flags(SelParams P, const long long *__restrict__ q64, i
   }
 }
 
-// single-block exclusive scan of n ints -> out (int64 totals at out_total)
+// single-block exclusive scan of n ints -> out (int64 total at *total)
 __global__ void k_scan_exclusive(const int *__restrict__ in, int64_t n, long long *__restrict__ out,
                                  long long *total) {
   __shared__ long long part[1024];
@@ -248,10 +248,40 @@ __global__ void k_absmax2(const float *__restrict__ g, const float *__restrict__
   if ((threadIdx.x & 31) == 0) { atomic_max_abs(&maxbits[0], mg); atomic_max_abs(&maxbits[1], mh); }
 }
 
-// q = rint(x 2^e) (half to even), plus exact int64 sums for the root node.
+// e = P - k with frexp(max |x|) = (., k); 0 when max = 0 (R12).  Device copy of the host rule.
+__device__ __forceinline__ int quant_exponent(unsigned long long maxbits, int P) {
+  const double M = __longlong_as_double((long long)maxbits);
+  if (!(M > 0.0)) return 0;
+  int k;
+  frexp(M, &k);
+  return P - k;
+}
+
+__global__ void k_sstate_init(SampleState *ss, long long n_sel_local, int quant_bits) {
+  ss->maxbits[0] = 0;
+  ss->maxbits[1] = 0;
+  ss->G = 0;
+  ss->H = 0;
+  ss->n_sel_local = n_sel_local;  // < 0: written later by the selection scan
+  ss->n_sel_global = 0;
+  ss->quant_bits = quant_bits;
+}
+
+__global__ void k_sstate_globalise(SampleState *ss) {
+  ss->n_sel_global = ss->n_sel_local;  // summed over ranks by an all-reduce when world > 1
+}
+
+// q = rint(x 2^e) (half to even), plus exact int64 sums for the root node; the exponents come
+// from the (all-reduced) maxima in the sample state, the row count from the selection scan.
 template <typename T>
-__global__ void k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, int64_t n,
-                           double sg, double sh, int2 *__restrict__ q, long long *sums) {
+__global__ void k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, SampleState *ss,
+                           int2 *__restrict__ q) {
+  const int eg = quant_exponent(ss->maxbits[0], ss->quant_bits);
+  const int eh = quant_exponent(ss->maxbits[1], ss->quant_bits);
+  if (blockIdx.x == 0 && threadIdx.x == 0) { ss->e_g = eg; ss->e_h = eh; }
+  const double sg = ldexp(1.0, eg), sh = ldexp(1.0, eh);
+  const int64_t n = ss->n_sel_local;
+  long long *sums = &ss->G;
   long long G = 0, H = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -270,6 +300,8 @@ __global__ void k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, i
     atomicAdd((unsigned long long *)&sums[1], (unsigned long long)H);
   }
 }
+
+// all-reduce helpers need contiguous arrays: sums (G, H) and counts live next to each other
 
 // Compact (Alg. 7): copy the selected rows of one staged page (rpp-row group planes)
 // into the sampled page (cap-row group planes): thread per (selected row, group, 16-B half).
@@ -443,20 +475,26 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
   }
   P.mode = eff_mode == OOCGB_SAMPLE_MVS ? 2 : 1;
 
-  unsigned long long *d_max = d_u + 8;
-  OOCGB_CK(cudaMemsetAsync(d_max, 0, 16, c->stream));
+  if (!d->d_ss) {
+    d->d_ss = (SampleState *)dmalloc(sizeof(SampleState));
+    OOCGB_CK(cudaMallocHost(&d->h_ss, sizeof(SampleState)));
+  }
+  SampleState *ss = d->d_ss;
+  d->quant_bits = quant_bits;
+  bool need_sync = (info != nullptr);
   if (eff_mode == OOCGB_SAMPLE_NONE) {
     d->all_selected = true;
     d->n_sel = n;
-    if (n > 0) k_absmax2<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, n, d_max);
+    k_sstate_init<<<1, 1, 0, c->stream>>>(ss, n, quant_bits);
+    if (n > 0) k_absmax2<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, n, ss->maxbits);
   } else {
     d->all_selected = false;
+    need_sync = true;  // the host needs n_sel (grids, graph key, compaction)
+    k_sstate_init<<<1, 1, 0, c->stream>>>(ss, 0, quant_bits);
     int64_t tiles = (n + kSelTile - 1) / kSelTile;
-    uint8_t *flags = (uint8_t *)d->d_gs;  // reuse: flags consumed before gs is written? no -> use q
-    flags = reinterpret_cast<uint8_t *>(d->d_q);
+    uint8_t *flags = reinterpret_cast<uint8_t *>(d->d_q);  // consumed before q is written
     int *tile_cnt = (int *)((char *)c->d_small + (256 << 10));
     long long *tile_off = (long long *)((char *)c->d_small + (512 << 10));
-    long long *d_total = (long long *)((char *)c->d_small + 1024);
     int *tcnt = tile_cnt;
     long long *toff = tile_off;
     std::vector<void *> tmp_alloc;
@@ -468,54 +506,35 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
     }
     if (n > 0) {
       k_select_flags<<<(unsigned)tiles, kSelThreads, 0, c->stream>>>(P, d->d_tmp64, n, flags, tcnt);
-      k_scan_exclusive<<<1, 1024, 0, c->stream>>>(tcnt, tiles, toff, d_total);
+      k_scan_exclusive<<<1, 1024, 0, c->stream>>>(tcnt, tiles, toff, &ss->n_sel_local);
       k_select_scatter<<<(unsigned)tiles, kSelThreads, 0, c->stream>>>(
-          P, d->d_tmp64, flags, toff, d->d_g, d->d_h, n, d->d_sel_rows, d->d_gs, d->d_hs, d_max);
+          P, d->d_tmp64, flags, toff, d->d_g, d->d_h, n, d->d_sel_rows, d->d_gs, d->d_hs, ss->maxbits);
       OOCGB_CK(cudaGetLastError());
-    } else {
-      OOCGB_CK(cudaMemsetAsync(d_total, 0, 8, c->stream));
     }
-    long long ns = 0;
-    OOCGB_CK(cudaMemcpyAsync(&ns, d_total, 8, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaMemcpyAsync(d->h_ss, ss, sizeof(SampleState), cudaMemcpyDeviceToHost, c->stream));
     OOCGB_CK(cudaStreamSynchronize(c->stream));
     for (void *p : tmp_alloc) dfree(p);
-    d->n_sel = ns;
+    d->n_sel = d->h_ss->n_sel_local;
   }
-  allreduce_max_u64(c, d_max, 2);
-  // n_sel global
-  long long *d_ns = (long long *)(d_u + 12);
-  long long ns_local = d->n_sel;
-  OOCGB_CK(cudaMemcpyAsync(d_ns, &ns_local, 8, cudaMemcpyHostToDevice, c->stream));
-  allreduce_sum_i64(c, d_ns, 1);
-  OOCGB_CK(cudaMemcpyAsync(h_u, d_max, 16, cudaMemcpyDeviceToHost, c->stream));
-  OOCGB_CK(cudaMemcpyAsync(h_u + 2, d_ns, 8, cudaMemcpyDeviceToHost, c->stream));
-  OOCGB_CK(cudaStreamSynchronize(c->stream));
-  double Mg, Mh;
-  memcpy(&Mg, &h_u[0], 8);
-  memcpy(&Mh, &h_u[1], 8);
-  d->n_sel_global = (long long)h_u[2];
-  int kg = 0, kh = 0;
-  d->e_g = 0;
-  d->e_h = 0;
-  if (Mg > 0.0) { frexp(Mg, &kg); d->e_g = quant_bits - kg; }
-  if (Mh > 0.0) { frexp(Mh, &kh); d->e_h = quant_bits - kh; }
-  d->quant_bits = quant_bits;
-  long long *d_sums = (long long *)(d_u + 14);
-  OOCGB_CK(cudaMemsetAsync(d_sums, 0, 16, c->stream));
-  const double sg = ldexp(1.0, d->e_g), sh = ldexp(1.0, d->e_h);
-  if (d->n_sel > 0) {
-    if (d->all_selected)
-      k_quantise<float><<<grid_for(c, d->n_sel), 256, 0, c->stream>>>(d->d_g, d->d_h, d->n_sel, sg, sh, d->d_q, d_sums);
-    else
-      k_quantise<double><<<grid_for(c, d->n_sel), 256, 0, c->stream>>>(d->d_gs, d->d_hs, d->n_sel, sg, sh, d->d_q, d_sums);
-  }
+  allreduce_max_u64(c, ss->maxbits, 2);
+  k_sstate_globalise<<<1, 1, 0, c->stream>>>(ss);
+  allreduce_sum_i64(c, &ss->n_sel_global, 1);
+  const int qgrid = grid_for(c, std::max<int64_t>(1, d->n_sel));
+  if (d->all_selected)
+    k_quantise<float><<<qgrid, 256, 0, c->stream>>>(d->d_g, d->d_h, ss, d->d_q);
+  else
+    k_quantise<double><<<qgrid, 256, 0, c->stream>>>(d->d_gs, d->d_hs, ss, d->d_q);
   OOCGB_CK(cudaGetLastError());
-  allreduce_sum_i64(c, d_sums, 2);
-  long long hs2[2];
-  OOCGB_CK(cudaMemcpyAsync(hs2, d_sums, 16, cudaMemcpyDeviceToHost, c->stream));
-  OOCGB_CK(cudaStreamSynchronize(c->stream));
-  d->G_root = hs2[0];
-  d->H_root = hs2[1];
+  allreduce_sum_i64(c, &ss->G, 2);
+  if (need_sync || d->placement == OOCGB_PLACE_PINNED_HOST) {
+    OOCGB_CK(cudaMemcpyAsync(d->h_ss, ss, sizeof(SampleState), cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    d->n_sel_global = d->h_ss->n_sel_global;
+    d->e_g = d->h_ss->e_g;
+    d->e_h = d->h_ss->e_h;
+    d->G_root = d->h_ss->G;
+    d->H_root = d->h_ss->H;
+  }
 
   // Compact (Alg. 7): pinned pages -> one device page of the selected rows
   if (d->placement == OOCGB_PLACE_PINNED_HOST) {
@@ -554,6 +573,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
     }
   }
   d->has_sample = true;
+  if (!info) return;
   si.n_selected_local = d->n_sel;
   si.n_selected_global = d->n_sel_global;
   si.e_g = d->e_g;

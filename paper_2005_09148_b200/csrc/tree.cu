@@ -94,8 +94,16 @@ __device__ void node_fill(DNode &nd, long long Gq, long long Hq, double sg_inv, 
   nd.leaf_value = __double2float_rn(__dmul_rn(eta, w));
 }
 
-__global__ void k_init_build(DNode *dn, int n_nodes, const RoundParams *__restrict__ rp, double lambda,
-                             double eta, Seg *segs,
+// Derives the per-call scalars from the device sample state (exactly the host formulas they
+// replace: dequantisation scales 2^-e, the integer form of R13, the pre-filter guard).
+__device__ __forceinline__ long long clamp_ll(double x) {
+  if (!(x > -9.0e18)) return LLONG_MIN / 2;
+  if (!(x < 9.0e18)) return LLONG_MAX / 2;
+  return (long long)x;
+}
+
+__global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restrict__ ss, RoundParams *rp,
+                             double lambda, double mcw, double eta, Seg *segs,
                              Pair *pairs, LevelCtl *ctl, int n_sel, int n_fg, int target_items,
                              int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
                              const int2 *q_in, int2 *q_out, int ridx_mode) {
@@ -111,10 +119,25 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const RoundParams *__restri
     q_out[i] = q_in[i];
   }
   if (tid == 0) {
+    RoundParams P;
+    P.G = ss->G;
+    P.H = ss->H;
+    P.n_rows_global = ss->n_sel_global;
+    P.sg_inv = ldexp(1.0, -ss->e_g);
+    P.sh_inv = ldexp(1.0, -ss->e_h);
+    P.sg_inv_f = ldexpf(1.0f, -ss->e_g);
+    P.sh_inv_f = ldexpf(1.0f, -ss->e_h);
+    // R13 exactly, in integers: hl = HL 2^-e_h is exact, so hl >= mcw <=> HL >= ceil(mcw 2^e_h)
+    // and hl + lambda > 0 <=> HL >= floor(-lambda 2^e_h) + 1 (clamped to the int64 range)
+    const long long t1 = clamp_ll(ceil(ldexp(mcw, ss->e_h)));
+    const long long t2 = clamp_ll(floor(ldexp(-lambda, ss->e_h))) + 1;
+    P.h_min = t1 > t2 ? t1 : t2;
+    P.prefilter = (abs(ss->e_g) <= 60 && abs(ss->e_h) <= 60) ? 1 : 0;
+    *rp = P;
     DNode r{};
     r.feature = -1;
-    r.n_rows = rp->n_rows_global;
-    node_fill(r, rp->G, rp->H, rp->sg_inv, rp->sh_inv, lambda, eta, &ctl->error);
+    r.n_rows = P.n_rows_global;
+    node_fill(r, P.G, P.H, P.sg_inv, P.sh_inv, lambda, eta, &ctl->error);
     dn[0] = r;
     segs[0] = Seg{0, n_sel, 0, 0};
     long long cr = ((long long)n_sel * n_fg + target_items - 1) / target_items;
@@ -420,61 +443,95 @@ __device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)
   for (int i = 0; i < 8; ++i) d2[i] = make_longlong2(g[i], h[i]);
 }
 
-__global__ void __launch_bounds__(256, 2) k_eval(EvalArgs A) {
-  const int lane = threadIdx.x & 31;
+// One warp per (pair, feature j, side): side 0 evaluates the built child (sum of its s32 chunk
+// partials, or the all-reduced int64 buffer), side 1 the derived sibling = parent - built (R17).
+// Loads, the subtraction and the parent store use the coalesced bin order bin = 32 i + lane;
+// a padded per-warp shared tile (conflict-free for both orders) then hands each lane its 8
+// consecutive bins 8 lane .. 8 lane + 7 for the scan and the evaluation.
+constexpr int kEvalWarps = 8;
+__global__ void __launch_bounds__(kEvalWarps * 32, 2) k_eval(EvalArgs A) {
+  __shared__ longlong2 tile[kEvalWarps][256 + 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int p = (int)(wid / A.m), j = (int)(wid % A.m);
+  const int side = (int)(wid & 1);
+  const int64_t pj = wid >> 1;
+  const int p = (int)(pj / A.m), j = (int)(pj % A.m);
   if (p >= A.ctl->n_pairs) return;
   const Pair P = A.pairs[p];
-  long long g[8], h[8];
+  const int node = side ? P.derived : P.built;
+  if (node < 0) return;
+  long long g[8], h[8];  // strided: element i is bin 32 i + lane
   const size_t hsz = (size_t)A.m * kBins * 2;
-  if (A.built64) {
-    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.built64 + (size_t)p * hsz + ((size_t)j * kBins + lane * 8) * 2);
+  longlong2 par[8];
+  if (side) {  // parent loads first so they overlap the chunk loads
+    const int ps = P.parent - level_first(A.d - 1);
+    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + (size_t)j * kBins * 2);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { longlong2 v = src[i]; g[i] = v.x; h[i] = v.y; }
+    for (int i = 0; i < 8; ++i) par[i] = __ldg(src + 32 * i + lane);
+  }
+  if (A.built64) {
+    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.built64 + (size_t)p * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { longlong2 v = src[32 * i + lane]; g[i] = v.x; h[i] = v.y; }
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) { g[i] = 0; h[i] = 0; }
-    // sum the pair's chunk partials: 2 chunks (8 independent 16-B loads) in flight per step
-    const size_t cstride = (size_t)A.n_fg * kFG * kBins * 2;  // ints between consecutive chunks
-    const int *src0 = A.partial + (((size_t)P.chunk_base * A.n_fg + j / kFG) * kFG + (j % kFG)) * kBins * 2 + lane * 16;
+    const size_t cstride = (size_t)A.n_fg * kFG * kBins;  // int2 elements between chunks
+    const int2 *src0 = reinterpret_cast<const int2 *>(A.partial) +
+                       (((size_t)P.chunk_base * A.n_fg + j / kFG) * kFG + (j % kFG)) * kBins + lane;
     int c = 0;
     for (; c + 2 <= P.n_chunks; c += 2) {
-      int4 v[2][4];
+      int2 v[2][8];
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[u][i] = __ldg(reinterpret_cast<const int4 *>(src0 + (c + u) * cstride) + i);
+        for (int i = 0; i < 8; ++i) v[u][i] = __ldg(src0 + (c + u) * cstride + 32 * i);
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          g[2 * i] += v[u][i].x; h[2 * i] += v[u][i].y; g[2 * i + 1] += v[u][i].z; h[2 * i + 1] += v[u][i].w;
-        }
+        for (int i = 0; i < 8; ++i) { g[i] += v[u][i].x; h[i] += v[u][i].y; }
     }
     if (c < P.n_chunks) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        int4 v = __ldg(reinterpret_cast<const int4 *>(src0 + c * cstride) + i);
-        g[2 * i] += v.x; h[2 * i] += v.y; g[2 * i + 1] += v.z; h[2 * i + 1] += v.w;
+      for (int i = 0; i < 8; ++i) {
+        int2 v = __ldg(src0 + c * cstride + 32 * i);
+        g[i] += v.x; h[i] += v.y;
       }
     }
   }
-  const bool keep = A.d <= A.D - 2;
-  const int f_d = level_first(A.d);
-  if (keep) store_hist8(A.phist_next + (size_t)(P.built - f_d) * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
-  if (A.dbg) store_hist8(A.dbg + (size_t)P.built * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
-  const RoundParams rp = *A.rp;
-  eval_node(A, P.built, j, lane, g, h, rp);
-  if (P.derived >= 0) {
-    const int ps = P.parent - level_first(A.d - 1);
-    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + ((size_t)j * kBins + lane * 8) * 2);
+  if (side) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { longlong2 v = src[i]; g[i] = v.x - g[i]; h[i] = v.y - h[i]; }
-    if (keep) store_hist8(A.phist_next + (size_t)(P.derived - f_d) * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
-    if (A.dbg) store_hist8(A.dbg + (size_t)P.derived * hsz + ((size_t)j * kBins + lane * 8) * 2, g, h);
-    eval_node(A, P.derived, j, lane, g, h, rp);
+    for (int i = 0; i < 8; ++i) { g[i] = par[i].x - g[i]; h[i] = par[i].y - h[i]; }
   }
+  const int f_d = level_first(A.d);
+  if (A.d <= A.D - 2) {
+    longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
+  }
+  if (A.dbg) {
+    longlong2 *dst = reinterpret_cast<longlong2 *>(A.dbg + (size_t)node * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
+  }
+  // transpose through the padded tile: element e lives in slot e + e / 8 (16-B slots), which
+  // is conflict-free per quarter-warp both for e = 32 i + lane and for e = 8 lane + i
+  longlong2 *tl = tile[wib];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = 32 * i + lane;
+    tl[e + (e >> 3)] = make_longlong2(g[i], h[i]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = 8 * lane + i;
+    const longlong2 v = tl[e + (e >> 3)];
+    g[i] = v.x;
+    h[i] = v.y;
+  }
+  const RoundParams rp = *A.rp;
+  eval_node(A, node, j, lane, g, h, rp);
 }
 
 // Split decision per node at depth d: argmax over features (ties: lowest feature, R13),
@@ -811,11 +868,12 @@ __global__ void k_predict(const uint8_t *__restrict__ bins, size_t pitch, int64_
 }
 
 // margin[row] += leaf of the row's final segment (in-core, all rows selected).
-__global__ void k_update_margin(int n, const Seg *__restrict__ segs, int n_segs, const DNode *__restrict__ dn,
-                                const int32_t *__restrict__ ridx, float *__restrict__ margin) {
+__global__ void k_update_margin(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
+                                const DNode *__restrict__ dn, const int32_t *__restrict__ ridx,
+                                float *__restrict__ margin) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int s = seg_of(segs, n_segs, i);
+  int s = seg_of(segs, ctl->n_segs, i);
   margin[ridx[i]] = margin[ridx[i]] + dn[segs[s].node].leaf_value;
 }
 
@@ -921,8 +979,8 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   if (keep_debug) OOCGB_CK(cudaMemsetAsync(w->dbg, 0, sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1), c->stream));
   OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
-      w->dnodes, n_nodes, w->d_rp, lambda, eta, w->segs[0], w->pairs, w->ctl, n, n_fg, target, kmax, D,
-      d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode);
+      w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta, w->segs[0], w->pairs, w->ctl, n, n_fg, target, kmax,
+      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode);
   OOCGB_CK(cudaGetLastError());
   int cur = 0;
   const int tiles = (n + kPartTile - 1) / kPartTile;
@@ -950,8 +1008,8 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.dbg = keep_debug ? w->dbg : nullptr;
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp;
-    const int64_t warps = (int64_t)max_pairs * m;
-    k_eval<<<(unsigned)((warps + 7) / 8), 256, 0, c->stream>>>(A);
+    const int64_t warps = (int64_t)max_pairs * m * 2;
+    k_eval<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, c->stream>>>(A);
     OOCGB_CK(cudaGetLastError());
     k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, c->stream>>>(lv, m, w->pairs, w->ctl, w->cand, w->dnodes,
                                                                  d->d_cut_values, d->d_cut_ptrs, w->d_rp, lambda,
@@ -1024,29 +1082,6 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     size_t need = sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1);
     if (w->dbg_bytes < need) { drop_graph(w); dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
   }
-  // per-call scalars -> device (ordered before the graph on the ctx stream)
-  w->h_rp->G = d->G_root;
-  w->h_rp->H = d->H_root;
-  w->h_rp->n_rows_global = d->n_sel_global;
-  w->h_rp->sg_inv = ldexp(1.0, -d->e_g);
-  w->h_rp->sh_inv = ldexp(1.0, -d->e_h);
-  w->h_rp->sg_inv_f = ldexpf(1.0f, -d->e_g);
-  w->h_rp->sh_inv_f = ldexpf(1.0f, -d->e_h);
-  // float pre-filter only while 2^-e and the dequantised sums stay well inside float's normal range
-  w->h_rp->prefilter = (std::abs(d->e_g) <= 60 && std::abs(d->e_h) <= 60) ? 1 : 0;
-  {
-    // R13 exactly, in integers: hl = HL 2^-e_h is exact, so hl >= mcw <=> HL >= ceil(mcw 2^e_h)
-    // and hl + lambda > 0 <=> HL >= floor(-lambda 2^e_h) + 1 (clamped to the int64 range)
-    auto clampll = [](double x) -> long long {
-      if (!(x > -9.0e18)) return LLONG_MIN / 2;
-      if (!(x < 9.0e18)) return LLONG_MAX / 2;
-      return (long long)x;
-    };
-    const long long t1 = clampll(ceil(ldexp(mcw, d->e_h)));
-    const long long t2 = clampll(floor(ldexp(-lambda, d->e_h))) + 1;
-    w->h_rp->h_min = std::max(t1, t2);
-  }
-  OOCGB_CK(cudaMemcpyAsync(w->d_rp, w->h_rp, sizeof(RoundParams), cudaMemcpyHostToDevice, c->stream));
   GraphKey key{n, D, m, ridx_mode, keep_debug ? 1 : 0, c->profiling ? 1 : 0, c->world, lambda, gamma, mcw, eta,
                bins, pitch, d->quant_bits};
   if (!w->graph || !(w->key == key)) {
@@ -1096,7 +1131,9 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     if (o.feature == -1) { o.split_bin = 0; o.split_value = 0; o.gain = 0; }
     pn[v] = PNode{o.feature, o.split_bin, o.leaf_value, 0};
   }
-  t->d_pnodes = (PNode *)dmalloc(sizeof(PNode) * n_nodes);
+  t->ctx = c;
+  t->pnodes_bytes = sizeof(PNode) * n_nodes;
+  t->d_pnodes = (PNode *)pool_get(c, t->pnodes_bytes);
   OOCGB_CK(cudaMemcpyAsync(t->d_pnodes, pn.data(), sizeof(PNode) * n_nodes, cudaMemcpyHostToDevice, c->stream));
   if (keep_debug) {
     t->debug = true;
@@ -1157,15 +1194,10 @@ void update_margin(oocgb_data d, oocgb_tree t, float *d_margin) {
   OOCGB_REQUIRE(w && t->serial == d->tree_serial && d->all_selected && d->placement == OOCGB_PLACE_DEVICE,
                 OOCGB_ERR_STATE, "update_margin: needs the latest tree of an in-core, f = 1 sample");
   const int n = (int)d->n_sel;
-  LevelCtl h;
-  OOCGB_CK(cudaMemcpyAsync(&h, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
-  OOCGB_CK(cudaStreamSynchronize(c->stream));
-  const int n_segs = t->max_depth > 0 ? h.n_segs : 1;
   if (n > 0)
-    k_update_margin<<<(n + 255) / 256, 256, 0, c->stream>>>(n, w->segs[w->final_cur], n_segs, w->dnodes,
+    k_update_margin<<<(n + 255) / 256, 256, 0, c->stream>>>(n, w->segs[w->final_cur], w->ctl, w->dnodes,
                                                             w->ridx[w->final_cur], d_margin);
   OOCGB_CK(cudaGetLastError());
-  OOCGB_CK(cudaStreamSynchronize(c->stream));
 }
 
 }  // namespace oocgb
