@@ -159,17 +159,26 @@ using namespace oocgb;
 
 static void bind(oocgb_ctx c) { OOCGB_CK(cudaSetDevice(c->device)); }
 
-// Copy a caller array (host or device) to a fresh device buffer; returns {ptr, owned}.
+// Device view of a caller array: the pointer itself if it is device memory, else a copy in
+// the data handle's persistent staging slot (no per-call allocation).
 struct DevView {
   const void *ptr = nullptr;
-  void *owned = nullptr;
-  ~DevView() { dfree(owned); }
+  bool staged = false;
 };
-static void view_on_device(oocgb_ctx c, const void *src, size_t bytes, DevView &v) {
+static void *arg_slot(oocgb_data d, int slot, size_t bytes) {
+  if (d->arg_bytes[slot] < bytes) {
+    dfree(d->d_arg[slot]);
+    d->d_arg[slot] = dmalloc(bytes);
+    d->arg_bytes[slot] = bytes;
+  }
+  return d->d_arg[slot];
+}
+static void view_on_device(oocgb_data d, int slot, const void *src, size_t bytes, DevView &v) {
   if (is_device_ptr(src)) { v.ptr = src; return; }
-  v.owned = dmalloc(bytes);
-  OOCGB_CK(cudaMemcpyAsync(v.owned, src, bytes, cudaMemcpyHostToDevice, c->stream));
-  v.ptr = v.owned;
+  void *dst = arg_slot(d, slot, bytes);
+  OOCGB_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, d->ctx->stream));
+  v.ptr = dst;
+  v.staged = true;
 }
 
 static oocgb_data new_data(oocgb_ctx c, int64_t n_local, int64_t row0, int64_t n_global, int m,
@@ -209,6 +218,9 @@ static void free_data(oocgb_data d) {
   dfree(d->d_sketch_count); dfree(d->d_g); dfree(d->d_h); dfree(d->d_sel_rows); dfree(d->d_q);
   dfree(d->d_sampled_page); dfree(d->d_gs); dfree(d->d_hs); dfree(d->d_tmp64);
   for (int i = 0; i < 3; ++i) dfree(d->d_stage[i]);
+  for (int i = 0; i < 2; ++i) dfree(d->d_arg[i]);
+  if (d->d_ss) cudaFree(d->d_ss);
+  if (d->h_ss) cudaFreeHost(d->h_ss);
   if (d->h_pages) cudaFreeHost(d->h_pages);
   d->ctx->live_data--;
   delete d;
@@ -503,10 +515,10 @@ int oocgb_set_logistic_gradients(oocgb_data d, const float *margin, const float 
   ensure_grad(d);
   DevView vm, vy;
   if (n_local > 0) {
-    view_on_device(c, margin, sizeof(float) * n_local, vm);
-    view_on_device(c, labels, sizeof(float) * n_local, vy);
+    view_on_device(d, 0, margin, sizeof(float) * n_local, vm);
+    view_on_device(d, 1, labels, sizeof(float) * n_local, vy);
     logistic_gradients(d, (const float *)vm.ptr, (const float *)vy.ptr);
-    if (vm.owned || vy.owned) OOCGB_CK(cudaStreamSynchronize(c->stream));
+    if (vm.staged || vy.staged) OOCGB_CK(cudaStreamSynchronize(c->stream));
   }
   d->has_grad = true;
   d->has_sample = false;
@@ -574,10 +586,10 @@ int oocgb_predict(oocgb_data d, const oocgb_tree *trees, int32_t n_trees, float 
   const bool dev = is_device_ptr(margin);
   float *dm = margin;
   if (!dev) {
-    dm = (float *)dmalloc(sizeof(float) * d->n_local);
+    dm = (float *)arg_slot(d, 0, sizeof(float) * d->n_local);
     OOCGB_CK(cudaMemcpyAsync(dm, margin, sizeof(float) * d->n_local, cudaMemcpyHostToDevice, c->stream));
   }
-  try {
+  {
     for (int t0 = 0; t0 < n_trees; t0 += 4096) {
       int nt = std::min(4096, n_trees - t0);
       if (d->placement == OOCGB_PLACE_DEVICE) {
@@ -591,11 +603,7 @@ int oocgb_predict(oocgb_data d, const oocgb_tree *trees, int32_t n_trees, float 
     if (!dev) {
       OOCGB_CK(cudaMemcpyAsync(margin, dm, sizeof(float) * d->n_local, cudaMemcpyDeviceToHost, c->stream));
       OOCGB_CK(cudaStreamSynchronize(c->stream));
-      dfree(dm);
     }
-  } catch (...) {
-    if (!dev) dfree(dm);
-    throw;
   }
   if (d->placement == OOCGB_PLACE_PINNED_HOST) OOCGB_CK(cudaStreamSynchronize(c->stream));  // staging reuse
   API_END
@@ -609,12 +617,10 @@ int oocgb_update_margin(oocgb_data d, oocgb_tree t, float *margin) {
   bind(c);
   PhaseTimer timer(c, 4);
   if (d->n_local == 0) return OOCGB_OK;
-  DevView v;
   const bool dev = is_device_ptr(margin);
   float *dm = margin;
   if (!dev) {
-    dm = (float *)dmalloc(sizeof(float) * d->n_local);
-    v.owned = dm;
+    dm = (float *)arg_slot(d, 0, sizeof(float) * d->n_local);
     OOCGB_CK(cudaMemcpyAsync(dm, margin, sizeof(float) * d->n_local, cudaMemcpyHostToDevice, c->stream));
   }
   update_margin(d, t, dm);

@@ -95,6 +95,8 @@ struct Pair {
   int32_t chunk_base;  // first global chunk of this pair
   int32_t n_chunks;
   int32_t chunk_rows;
+  int32_t compact;     // bit 0: parent, bit 1: built, bit 2: derived histogram kept as s32 pairs
+  int32_t pad[3];
 };
 
 // Best split candidate of one (node, feature).
@@ -206,6 +208,9 @@ struct oocgb_data_s {
   // tree workspace (lazy, sized for (n_sel cap, depth))
   struct Work *work = nullptr;
   uint64_t tree_serial = 0;
+  // persistent device staging for host-pointer arguments (margin, labels): no per-call malloc
+  void *d_arg[2] = {nullptr, nullptr};
+  size_t arg_bytes[2] = {0, 0};
   // staging for streamed pages
   uint8_t *d_stage[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t stage_ev[3] = {};

@@ -144,7 +144,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
     if (cr < 1024) cr = 1024;
     if (cr > kmax) cr = kmax;
     int nch = (int)((n_sel + cr - 1) / cr);
-    pairs[0] = Pair{-1, 0, -1, 0, n_sel, 0, nch, (int)cr};
+    pairs[0] = Pair{-1, 0, -1, 0, n_sel, 0, nch, (int)cr, (P.n_rows_global <= kmax) ? 2 : 0, {0, 0, 0}};
     ctl->n_pairs = max_depth > 0 ? 1 : 0;
     ctl->n_items = max_depth > 0 ? nch * n_fg : 0;
     ctl->n_segs = 1;
@@ -316,6 +316,7 @@ struct EvalArgs {
   Cand *cand;
   double lambda, gamma, mcw;
   const RoundParams *rp;
+  long long kmax;  // nodes with <= kmax rows keep their parent histogram as exact s32 pairs
 };
 
 __device__ __forceinline__ long long warp_excl_scan_ll(long long v, int lane, long long &total) {
@@ -348,9 +349,8 @@ __device__ __forceinline__ double gain_exact(long long GL, long long HL, long lo
 //    its exact ties always pass (gain_f + tol >= gain >= gain(c') >= gain_f(c') - tol(c')), so
 //    the result is identical to evaluating every candidate in double.
 __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const long long (&g)[8],
-                          const long long (&h)[8], const RoundParams &rp) {
+                          const long long (&h)[8], const RoundParams &rp, const long long G, const long long H) {
   const int B = A.cut_ptrs[j + 1] - A.cut_ptrs[j];
-  const long long G = A.dn[node].Gq, H = A.dn[node].Hq;
   long long lg = 0, lh = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) { lg += g[i]; lh += h[i]; }
@@ -359,7 +359,7 @@ __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const lo
   const long long eh = warp_excl_scan_ll(lh, lane, th);
   const float lamf = (float)A.lambda;
   const float gPf = (float)G * rp.sg_inv_f, hPf = (float)H * rp.sh_inv_f;
-  const float tPf = __fdiv_rn(gPf * gPf, hPf + lamf);
+  const float tPf = __fdividef(gPf * gPf, hPf + lamf);
   const float gamf = (float)A.gamma;
   // pass 1: float gains + bounds
   float gf[8], tf[8];
@@ -379,11 +379,12 @@ __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const lo
       vmask |= 1u << i;
       const float gl = (float)GL * rp.sg_inv_f, hl = (float)HL * rp.sh_inv_f;
       const float gr = (float)(G - GL) * rp.sg_inv_f, hr = (float)(H - HL) * rp.sh_inv_f;
-      const float tL = __fdiv_rn(gl * gl, hl + lamf);
-      const float tR = __fdiv_rn(gr * gr, hr + lamf);
+      const float tL = __fdividef(gl * gl, hl + lamf);  // <= 2 ulp (denominator in range, see guard)
+      const float tR = __fdividef(gr * gr, hr + lamf);
       const float gain = 0.5f * ((tL + tR) - tPf) - gamf;
-      // each float op adds <= 2^-24 relative error; <= 12 ops touch any term: 2^-18 is >= 4x
-      // that bound on |tL| + |tR| + |tP| + |gamma|; non-finite -> always re-evaluate exactly
+      // each float op adds <= 2^-24 relative error (the two divisions <= 2 ulp), so every term
+      // carries <= ~10 2^-24: 2^-18 is >= 6x that bound on |tL| + |tR| + |tP| + |gamma|;
+      // non-finite (overflow, division by 0) -> always re-evaluate exactly
       float tol = 0x1p-18f * (fabsf(tL) + fabsf(tR) + fabsf(tPf) + fabsf(gamf)) + 0x1p-100f;
       if (!isfinite(gain) || !isfinite(tol) || !rp.prefilter) tol = INFINITY;
       gf[i] = gain;
@@ -456,18 +457,31 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 2) k_eval(EvalArgs A) {
   const int side = (int)(wid & 1);
   const int64_t pj = wid >> 1;
   const int p = (int)(pj / A.m), j = (int)(pj % A.m);
-  if (p >= A.ctl->n_pairs) return;
+  const int max_pairs = A.d == 0 ? 1 : (1 << (A.d - 1));
+  if (p >= max_pairs) return;
+  const int n_pairs = A.ctl->n_pairs;  // independent of the pair load below
   const Pair P = A.pairs[p];
+  if (p >= n_pairs) return;
   const int node = side ? P.derived : P.built;
   if (node < 0) return;
+  const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;  // prefetched for eval_node
   long long g[8], h[8];  // strided: element i is bin 32 i + lane
   const size_t hsz = (size_t)A.m * kBins * 2;
   longlong2 par[8];
   if (side) {  // parent loads first so they overlap the chunk loads
     const int ps = P.parent - level_first(A.d - 1);
-    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + (size_t)j * kBins * 2);
+    if (P.compact & 1) {  // compact s32 parent (exact: |sum| < 2^31)
+      const int2 *src = reinterpret_cast<const int2 *>(A.phist_prev + (size_t)ps * hsz) + (size_t)j * kBins;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) par[i] = __ldg(src + 32 * i + lane);
+      for (int i = 0; i < 8; ++i) {
+        const int2 v = __ldg(src + 32 * i + lane);
+        par[i] = make_longlong2(v.x, v.y);
+      }
+    } else {
+      const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) par[i] = __ldg(src + 32 * i + lane);
+    }
   }
   if (A.built64) {
     const longlong2 *src = reinterpret_cast<const longlong2 *>(A.built64 + (size_t)p * hsz + (size_t)j * kBins * 2);
@@ -505,9 +519,15 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 2) k_eval(EvalArgs A) {
   }
   const int f_d = level_first(A.d);
   if (A.d <= A.D - 2) {
-    longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)j * kBins * 2);
+    if (P.compact & (side ? 4 : 2)) {
+      int2 *dst = reinterpret_cast<int2 *>(A.phist_next + (size_t)(node - f_d) * hsz) + (size_t)j * kBins;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
+      for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_int2((int)g[i], (int)h[i]);
+    } else {
+      longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
+    }
   }
   if (A.dbg) {
     longlong2 *dst = reinterpret_cast<longlong2 *>(A.dbg + (size_t)node * hsz + (size_t)j * kBins * 2);
@@ -531,7 +551,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 2) k_eval(EvalArgs A) {
     h[i] = v.y;
   }
   const RoundParams rp = *A.rp;
-  eval_node(A, node, j, lane, g, h, rp);
+  eval_node(A, node, j, lane, g, h, rp, nodeG, nodeH);
 }
 
 // Split decision per node at depth d: argmax over features (ties: lowest feature, R13),
@@ -617,29 +637,85 @@ __device__ __forceinline__ int seg_of(const Seg *segs, int n_segs, int i) {
   return lo;
 }
 
+// Segments overlapping one partition tile, staged in shared memory (at most kTileSegs; a tile
+// that overlaps more falls back to global lookups).
+constexpr int kTileSegs = 256;
+struct TileSegs {
+  int first, count;  // segment range overlapping the tile
+  int begin[kTileSegs], end[kTileSegs];
+  int feat[kTileSegs], sbin[kTileSegs];
+};
+
+__device__ __forceinline__ void load_tile_segs(TileSegs &T, const Seg *__restrict__ segs, int n_segs,
+                                               const DNode *__restrict__ dn, int t0, int t1) {
+  if (threadIdx.x == 0) {
+    const int f = seg_of(segs, n_segs, t0);
+    const int l = seg_of(segs, n_segs, t1 - 1);
+    T.first = f;
+    T.count = l - f + 1;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < T.count && k < kTileSegs; k += blockDim.x) {
+    const Seg S = segs[T.first + k];
+    T.begin[k] = S.begin;
+    T.end[k] = S.begin + S.count;
+    const DNode &nd = dn[S.node];
+    T.feat[k] = nd.feature;
+    T.sbin[k] = nd.split_bin;
+  }
+  __syncthreads();
+}
+
+// index (relative to T.first) of the segment containing position i, searching upward from k
+__device__ __forceinline__ int tile_seg(const TileSegs &T, int k, int i) {
+  while (T.end[k] <= i) ++k;
+  return k;
+}
+
 __global__ void __launch_bounds__(kPartThreads)
 k_part_flags(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
              const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, size_t pitch,
              const int32_t *__restrict__ ridx, uint32_t *__restrict__ flagbits, int *__restrict__ tile_cnt,
              int *__restrict__ bpart) {
   __shared__ uint32_t s_words[kPartTile / 32];
+  __shared__ TileSegs T;
   const int n_segs = ctl->n_segs;
   const int t0 = blockIdx.x * kPartTile;
+  const int t1 = min(n, t0 + kPartTile);
   const int p0 = t0 + threadIdx.x * 8;
+  load_tile_segs(T, segs, n_segs, dn, t0, t1);
   uint32_t bits = 0;
   if (p0 < n) {
-    int s = seg_of(segs, n_segs, p0);
+    // 8 row ids (32 contiguous bytes per thread), their segments, then 8 independent gathers
+    int rows[8], feat[8], sbin[8];
+    const bool staged = T.count <= kTileSegs;
+    int k = 0, sg = 0;
+    if (staged) k = tile_seg(T, 0, p0); else sg = seg_of(segs, n_segs, p0);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int i = p0 + k;
-      if (i >= n) break;
-      while (segs[s].begin + segs[s].count <= i) ++s;
-      const DNode &nd = dn[segs[s].node];
-      if (nd.feature >= 0) {
-        const uint8_t b = bins[(size_t)(nd.feature >> 5) * pitch + (size_t)ridx[i] * 32 + (nd.feature & 31)];
-        bits |= (uint32_t)(b > nd.split_bin) << k;
+    for (int u = 0; u < 8; ++u) {
+      const int i = p0 + u;
+      rows[u] = (i < n) ? ridx[i] : 0;
+      feat[u] = -1;
+      sbin[u] = 0;
+      if (i < n) {
+        if (staged) {
+          k = tile_seg(T, k, i);
+          feat[u] = T.feat[k];
+          sbin[u] = T.sbin[k];
+        } else {
+          while (segs[sg].begin + segs[sg].count <= i) ++sg;
+          const DNode &nd = dn[segs[sg].node];
+          feat[u] = nd.feature;
+          sbin[u] = nd.split_bin;
+        }
       }
     }
+    uint8_t b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      b[u] = feat[u] >= 0 ? bins[(size_t)(feat[u] >> 5) * pitch + (size_t)rows[u] * 32 + (feat[u] & 31)] : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bits |= (uint32_t)(feat[u] >= 0 && b[u] > sbin[u]) << u;
   }
   reinterpret_cast<uint8_t *>(s_words)[threadIdx.x] = (uint8_t)bits;
   __syncthreads();
@@ -656,15 +732,14 @@ k_part_flags(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
     tile_cnt[blockIdx.x] = t;
   }
   // boundary partials for segments beginning inside this tile
-  const int t1 = min(n, t0 + kPartTile);
   int lo = 0, hi = n_segs;  // first segment with begin >= t0
   while (lo < hi) { int mid = (lo + hi) >> 1; if (segs[mid].begin < t0) lo = mid + 1; else hi = mid; }
-  for (int s = lo + threadIdx.x; s < n_segs && segs[s].begin < t1; s += blockDim.x) {
-    const int off = segs[s].begin - t0;
+  for (int sidx = lo + threadIdx.x; sidx < n_segs && segs[sidx].begin < t1; sidx += blockDim.x) {
+    const int off = segs[sidx].begin - t0;
     int r = 0;
     for (int w = 0; w < (off >> 5); ++w) r += __popc(s_words[w]);
     if (off & 31) r += __popc(s_words[off >> 5] & ((1u << (off & 31)) - 1u));
-    bpart[s] = r;
+    bpart[sidx] = r;
   }
 }
 
@@ -763,9 +838,12 @@ k_part_plan2(const Seg *__restrict__ segs, Seg *__restrict__ segs_next, LevelCtl
         segs_next[ns + 1] = Seg{S.begin + nl, nr, 2 * S.node + 2, 0};
         Pair pr;
         pr.parent = S.node;
-        if (gl <= gr) { pr.built = 2 * S.node + 1; pr.derived = 2 * S.node + 2; pr.begin = S.begin; pr.count = nl; }
-        else { pr.built = 2 * S.node + 2; pr.derived = 2 * S.node + 1; pr.begin = S.begin + nl; pr.count = nr; }
+        long long gb, gd;
+        if (gl <= gr) { pr.built = 2 * S.node + 1; pr.derived = 2 * S.node + 2; pr.begin = S.begin; pr.count = nl; gb = gl; gd = gr; }
+        else { pr.built = 2 * S.node + 2; pr.derived = 2 * S.node + 1; pr.begin = S.begin + nl; pr.count = nr; gb = gr; gd = gl; }
         pr.chunk_base = 0; pr.n_chunks = 0; pr.chunk_rows = 0;
+        // s32 histograms are exact for nodes with <= kmax rows (|q| <= 2^quant_bits)
+        pr.compact = ((gl + gr) <= kmax ? 1 : 0) | (gb <= kmax ? 2 : 0) | (gd <= kmax ? 4 : 0);
         pairs[np] = pr;
         rows_local += pr.count;
       } else {
@@ -814,11 +892,29 @@ k_part_scatter(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__
                const int32_t *__restrict__ ridx, const int2 *__restrict__ q, int32_t *__restrict__ ridx_out,
                int2 *__restrict__ q_out) {
   __shared__ uint32_t s_words[kPartTile / 32];
+  __shared__ int s_first, s_count;
+  __shared__ int s_begin[kTileSegs], s_end[kTileSegs], s_nl[kTileSegs], s_grb[kTileSegs];
   const int nw = kPartTile / 32;
   const int t0 = blockIdx.x * kPartTile;
-  if (threadIdx.x < nw) s_words[threadIdx.x] = flagbits[(size_t)blockIdx.x * nw + threadIdx.x];
-  __syncthreads();
+  const int t1 = min(n, t0 + kPartTile);
   const int n_segs = ctl->pad[0];
+  if (threadIdx.x < nw) s_words[threadIdx.x] = flagbits[(size_t)blockIdx.x * nw + threadIdx.x];
+  if (threadIdx.x == 0) {
+    const int f = seg_of(segs, n_segs, t0);
+    s_first = f;
+    s_count = seg_of(segs, n_segs, t1 - 1) - f + 1;
+  }
+  __syncthreads();
+  const bool staged = s_count <= kTileSegs;
+  if (staged)
+    for (int k = threadIdx.x; k < s_count; k += blockDim.x) {
+      const Seg S = segs[s_first + k];
+      s_begin[k] = S.begin;
+      s_end[k] = S.begin + S.count;
+      s_nl[k] = S.count - seg_nr[s_first + k];
+      s_grb[k] = seg_grb[s_first + k];
+    }
+  __syncthreads();
   const int p0 = t0 + threadIdx.x * 8;
   if (p0 >= n) return;
   // rights in this tile before p0
@@ -828,20 +924,31 @@ k_part_scatter(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__
   if (off & 31) r += __popc(s_words[off >> 5] & ((1u << (off & 31)) - 1u));
   const uint32_t bits = (s_words[off >> 5] >> (off & 31)) & 0xffu;
   int gr = tile_off[blockIdx.x] + r;  // global right rank at p0
-  int s = seg_of(segs, n_segs, p0);
+  int rows[8];
+  int2 qs[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = p0 + k;
+  for (int u = 0; u < 8; ++u) {
+    if (p0 + u < n) { rows[u] = ridx[p0 + u]; qs[u] = q[p0 + u]; }
+  }
+  int k = 0, sg = 0;
+  if (staged) { while (s_end[k] <= p0) ++k; } else { sg = seg_of(segs, n_segs, p0); }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int i = p0 + u;
     if (i >= n) break;
-    while (segs[s].begin + segs[s].count <= i) ++s;
-    const Seg S = segs[s];
-    const int rr = gr - seg_grb[s];
-    const int right = (bits >> k) & 1;
-    int pos;
-    if (right) pos = S.begin + (S.count - seg_nr[s]) + rr;
-    else pos = i - rr;
-    ridx_out[pos] = ridx[i];
-    q_out[pos] = q[i];
+    int begin, nl, grb;
+    if (staged) {
+      while (s_end[k] <= i) ++k;
+      begin = s_begin[k]; nl = s_nl[k]; grb = s_grb[k];
+    } else {
+      while (segs[sg].begin + segs[sg].count <= i) ++sg;
+      begin = segs[sg].begin; nl = segs[sg].count - seg_nr[sg]; grb = seg_grb[sg];
+    }
+    const int rr = gr - grb;
+    const int right = (bits >> u) & 1;
+    const int pos = right ? begin + nl + rr : i - rr;
+    ridx_out[pos] = rows[u];
+    q_out[pos] = qs[u];
     gr += right;
   }
 }
@@ -1007,7 +1114,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.phist_next = w->phist[lv & 1];
     A.dbg = keep_debug ? w->dbg : nullptr;
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
-    A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp;
+    A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax;
     const int64_t warps = (int64_t)max_pairs * m * 2;
     k_eval<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, c->stream>>>(A);
     OOCGB_CK(cudaGetLastError());
