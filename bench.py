@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--rows", type=int, default=N_ROWS, help="rows per GPU (config 2: 1M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON line)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
+                    help="2: 1M x 500 in-core f=1 (the driver's bench); 3: 20M x 500 out-of-core, "
+                         "32 MiB pinned pages, MVS f=0.1")
+    ap.add_argument("--rows3", type=int, default=20_000_000, help="config 3 rows")
     return ap.parse_args()
 
 
@@ -213,9 +217,99 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_config3(args, rank, world, local):
+    """Config 3 (BASELINE.json configs[2]): 20M x 500 streamed as 32 MiB ELLPACK pages from pinned
+    host memory, gradient-based (MVS) sampling f = 0.1, depth 8.  Per round: predict(tree t-1)
+    streams every page (Eq. 1), logistic gradients, sample(MVS) + Compact streams every page
+    again (Alg. 7), build_tree on the compacted device page.  Link busy = H2D copy time / round
+    time; link GB/s = bytes copied / copy time (CUDA events on the copy stream)."""
+    import torch
+    import paper_2005_09148_b200 as ob
+    import synth
+    n, m = args.rows3, N_FEAT
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = ob.Context(local, rank, world, None, stream=stream.cuda_stream)
+    chunk = 1 << 20
+    d = ctx.sketch_begin(m, MAX_BIN, n, page_bytes=32 << 20, placement=ob.PLACE_PINNED_HOST, seed=2)
+    t0 = time.perf_counter()
+    for r0 in range(0, n, chunk):
+        X, _ = synth.torch_classification_chunk(r0, min(chunk, n - r0), m, seed=3)
+        d.sketch_push(X, r0)
+    d.cuts_finalize()
+    ys = []
+    for r0 in range(0, n, chunk):
+        X, y = synth.torch_classification_chunk(r0, min(chunk, n - r0), m, seed=3)
+        d.pages_push(X, r0)
+        ys.append(y)
+    del X
+    labels = torch.cat(ys)
+    torch.cuda.synchronize()
+    prep_s = time.perf_counter() - t0
+    info = d.info()
+    margin = torch.zeros(n, dtype=torch.float32, device="cuda")
+    tree = None
+    sel = []
+
+    def one_round(prev, r):
+        if prev is not None:
+            d.predict([prev], margin)     # streams all pages
+            prev.close()
+        d.set_logistic_gradients(margin, labels)
+        si = d.sample(ob.SAMPLE_MVS, 0.1, 1.0, seed=1, round=r, quant_bits=QBITS)  # + Compact
+        sel.append(si["n_selected_global"])
+        return d.build_tree(DEPTH, LAMBDA, GAMMA, MCW, ETA)
+
+    r = 0
+    for _ in range(args.warmup):
+        tree = one_round(tree, r)
+        r += 1
+    ctx.set_profiling(True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    e0.record(stream)
+    for _ in range(args.steps):
+        tree = one_round(tree, r)
+        r += 1
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    tm = ctx.get_timings()
+    page_bytes_per_pass = n * info["row_stride"]
+    copied = 2 * page_bytes_per_pass  # predict pass + compaction pass per round
+    h2d_ms = tm["h2d_ms"] / args.steps
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8 symbols, int32/int64 fixed-point sums, f64 gains",
+        "data": "synthetic (make_classification-style, generated on the GPU per chunk, seeded)",
+        "config": {"workload": "config 3: 20M x 500 out-of-core, 32 MiB pinned-host ELLPACK pages, MVS f=0.1, depth 8",
+                   "rows": n, "n_features": m, "n_pages": info["n_pages"], "rows_per_page": info["rows_per_page"],
+                   "max_depth": DEPTH, "sample": "MVS", "ratio": 0.1},
+        "link": {"bytes_per_round": copied, "h2d_ms_per_round": h2d_ms,
+                 "gbps_while_copying": copied / (h2d_ms * 1e-3) / 1e9 if h2d_ms > 0 else None,
+                 "busy_frac": h2d_ms / ms, "effective_gbps": copied / (ms * 1e-3) / 1e9},
+        "phases_ms_per_round": {k: v / args.steps for k, v in tm.items() if k.endswith("_ms")},
+        "selected_rows_per_round": sel[-args.steps:],
+        "prep_s": prep_s, "clocks": ck,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if tree is not None:
+        tree.close()
+    d.close()
+    ctx.close()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.config == 3 and args.impl == "ours":
+        run_config3(args, rank, world, local)
+        return
     if world > 1:
         import torch.distributed as tdist
         tdist.init_process_group("gloo")

@@ -87,3 +87,32 @@ def gradient_pairs(n: int, seed: int = 0, kind: str = "logistic"):
 def labels_like(n: int, seed: int = 0):
     rng = np.random.default_rng(seed)
     return (rng.random(n) < 0.5).astype(np.float32)
+
+
+def torch_classification_chunk(row0: int, n_rows: int, n_features: int, seed: int = 0, device="cuda"):
+    """make_classification-shaped rows [row0, row0 + n_rows) generated on the GPU with torch, for
+    the 10^7..10^8-row configurations (3, 4) where X is never materialised on the host.  The
+    chunk's values depend only on (seed, row0, n_rows): regenerating a chunk gives identical
+    data, so the two quantise passes (sketch, pages) see the same rows.  Structure as
+    fast_classification: 4 clusters on {+-1}^2, 2 redundant combinations, N(0,1) noise,
+    1% label flips, a fixed column permutation.  Returns (X float32 [n, m], y float32 [n])."""
+    import torch
+
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    A = torch.rand((4, 2, 2), generator=g) * 2 - 1
+    Bm = torch.rand((2, 2), generator=g) * 2 - 1
+    perm = torch.randperm(n_features, generator=g)
+    gc = torch.Generator(device=device).manual_seed((seed * 1_000_003 + row0) % (2**63 - 1))
+    cluster = torch.randint(0, 4, (n_rows,), generator=gc, device=device)
+    centroids = torch.tensor([[-1, -1], [1, -1], [-1, 1], [1, 1]], dtype=torch.float32, device=device)
+    z = torch.randn((n_rows, 2), generator=gc, device=device)
+    x_inf = torch.einsum("ni,nij->nj", z, A.to(device)[cluster]) + centroids[cluster]
+    X = torch.randn((n_rows, n_features), generator=gc, device=device)
+    X[:, 0:2] = x_inf
+    if n_features > 2:
+        X[:, 2:4] = (x_inf @ Bm.to(device))[:, : max(0, min(2, n_features - 2))]
+    y = (cluster % 2).to(torch.float32)
+    flip = torch.rand((n_rows,), generator=gc, device=device) < 0.01
+    y[flip] = torch.randint(0, 2, (int(flip.sum().item()),), generator=gc, device=device).to(torch.float32)
+    X = X[:, perm.to(device)].contiguous()
+    return X, y
