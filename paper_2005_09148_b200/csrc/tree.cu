@@ -226,7 +226,7 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
     // is unrolled by kDepth); a set is consumed (rotation + reductions) and only then refilled
     // with the row kDepth steps ahead, so no in-flight register is ever copied; the row id for
     // a refill is loaded one round earlier still.
-    constexpr int kDepth = 3;
+    constexpr int kDepth = 5;
     int k = r0 + (threadIdx.x >> 1);
     uint4 xs[kDepth];
     int2 qs[kDepth];
