@@ -101,6 +101,16 @@ int oocgb_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t 
                      uint64_t cuda_stream, oocgb_ctx *out);
 int oocgb_ctx_destroy(oocgb_ctx ctx);
 
+/* Test-only transport for the exchange steps (several ranks sharing one GPU, or no NCCL):
+ * every collective is run as: synchronise the ctx stream, copy the device buffer to host,
+ * call fn, copy back.  op: 0 all-reduce sum, 1 all-reduce max, 2 all-gather (buf holds
+ * world * count elements, this rank's block at rank * count); dtype: 0 int64, 1 uint64,
+ * 2 uint32.  fn returns 0 on success.  The compute path is unchanged (all kernels on the GPU);
+ * build_tree is not graph-captured in this mode.  ERR_ARG if fn is NULL or world < 1.       */
+typedef int (*oocgb_collective_fn)(int32_t op, int32_t dtype, void *buf, int64_t count, void *user);
+int oocgb_ctx_create_hostcomm(int32_t device, int32_t rank, int32_t world, oocgb_collective_fn fn,
+                              void *user, uint64_t cuda_stream, oocgb_ctx *out);
+
 /* ---- quantise: Alg. 2 (in-core sketch) + Alg. 4 (ELLPACK page), PAPER.md L256-318 ---------
  * X: float32 row-major [n_rows][n_features], this rank's rows, global ids
  * row0_global .. row0_global+n_rows-1 of n_rows_global in total.  max_bin in [2, 256]

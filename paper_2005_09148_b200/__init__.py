@@ -32,7 +32,11 @@ ABI_SYMBOLS = (
     "oocgb_tree_destroy", "oocgb_predict", "oocgb_update_margin", "oocgb_get_cuts",
     "oocgb_get_bins", "oocgb_get_sample", "oocgb_get_histogram", "oocgb_get_partition",
     "oocgb_get_timings", "oocgb_set_profiling", "oocgb_last_error", "oocgb_abi_version",
+    "oocgb_ctx_create_hostcomm",
 )
+
+COLLECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
+                                 ctypes.c_void_p)
 
 
 class OocgbError(RuntimeError):
@@ -108,6 +112,7 @@ def load_library():
         "oocgb_get_partition": [p, p],
         "oocgb_get_timings": [p, p, i32],
         "oocgb_set_profiling": [p, i32],
+        "oocgb_ctx_create_hostcomm": [i32, i32, i32, COLLECTIVE_FN, p, u64, p],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -149,11 +154,31 @@ class Context:
     """One per process == one GPU (oocgb_ctx_create)."""
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 stream: int = 0):
+                 stream: int = 0, host_collective=None):
+        """host_collective: optional Python callable(op, np_array) performing the exchange in place
+        (test transport, see oocgb_ctx_create_hostcomm); otherwise NCCL when world > 1."""
         L = load_library()
         h = ctypes.c_void_p()
-        idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
-        _check(L.oocgb_ctx_create(device, rank, world, idbuf, stream, ctypes.byref(h)))
+        self._cb = None
+        if host_collective is not None:
+            dtypes = {0: np.int64, 1: np.uint64, 2: np.uint32}
+
+            def _cb(op, dtype, buf, count, user):
+                try:
+                    n = count * (world if op == 2 else 1)
+                    arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_uint8)),
+                                                shape=(n * np.dtype(dtypes[dtype]).itemsize,)).view(dtypes[dtype])
+                    host_collective(op, arr)
+                    return 0
+                except Exception as e:  # pragma: no cover - reported through the status code
+                    print("host collective failed:", e)
+                    return 1
+
+            self._cb = COLLECTIVE_FN(_cb)
+            _check(L.oocgb_ctx_create_hostcomm(device, rank, world, self._cb, None, stream, ctypes.byref(h)))
+        else:
+            idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+            _check(L.oocgb_ctx_create(device, rank, world, idbuf, stream, ctypes.byref(h)))
         self._h = h
         self.device, self.rank, self.world = device, rank, world
 

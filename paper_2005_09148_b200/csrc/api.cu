@@ -78,11 +78,44 @@ const NcclApi &nccl_api() {
 
 void allreduce_sum_i64(oocgb_ctx c, long long *d_buf, size_t count) {
   if (c->world <= 1 || count == 0) return;
+  if (c->host_coll) {
+    std::vector<long long> h(count);
+    OOCGB_CK(cudaMemcpyAsync(h.data(), d_buf, 8 * count, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    OOCGB_REQUIRE(c->host_coll(0, 0, h.data(), (int64_t)count, c->host_coll_user) == 0, OOCGB_ERR_DEVICE,
+                  "host collective (all-reduce sum) failed");
+    OOCGB_CK(cudaMemcpyAsync(d_buf, h.data(), 8 * count, cudaMemcpyHostToDevice, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
   OOCGB_NCCL(nccl_api().AllReduce(d_buf, d_buf, count, ncclInt64, ncclSum, c->comm, c->stream));
 }
 void allreduce_max_u64(oocgb_ctx c, unsigned long long *d_buf, size_t count) {
   if (c->world <= 1 || count == 0) return;
+  if (c->host_coll) {
+    std::vector<unsigned long long> h(count);
+    OOCGB_CK(cudaMemcpyAsync(h.data(), d_buf, 8 * count, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    OOCGB_REQUIRE(c->host_coll(1, 1, h.data(), (int64_t)count, c->host_coll_user) == 0, OOCGB_ERR_DEVICE,
+                  "host collective (all-reduce max) failed");
+    OOCGB_CK(cudaMemcpyAsync(d_buf, h.data(), 8 * count, cudaMemcpyHostToDevice, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
   OOCGB_NCCL(nccl_api().AllReduce(d_buf, d_buf, count, ncclUint64, ncclMax, c->comm, c->stream));
+}
+void allgather_u32(oocgb_ctx c, const uint32_t *d_send, uint32_t *d_recv, size_t count) {
+  if (c->host_coll) {
+    std::vector<uint32_t> h(count * c->world);
+    OOCGB_CK(cudaMemcpyAsync(h.data() + (size_t)c->rank * count, d_send, 4 * count, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    OOCGB_REQUIRE(c->host_coll(2, 2, h.data(), (int64_t)count, c->host_coll_user) == 0, OOCGB_ERR_DEVICE,
+                  "host collective (all-gather) failed");
+    OOCGB_CK(cudaMemcpyAsync(d_recv, h.data(), 4 * count * c->world, cudaMemcpyHostToDevice, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
+  OOCGB_NCCL(nccl_api().AllGather(d_send, d_recv, count, ncclUint32, c->comm, c->stream));
 }
 
 cudaEvent_t pool_event(oocgb_ctx c) {
@@ -329,6 +362,22 @@ int oocgb_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t 
     delete c;
     throw;
   }
+  *out = c;
+  API_END
+}
+
+int oocgb_ctx_create_hostcomm(int32_t device, int32_t rank, int32_t world, oocgb_collective_fn fn, void *user,
+                              uint64_t cuda_stream, oocgb_ctx *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(fn && out, OOCGB_ERR_ARG, "collective callback / out is NULL");
+  OOCGB_REQUIRE(world >= 1 && rank >= 0 && rank < world, OOCGB_ERR_ARG, "need 0 <= rank < world");
+  oocgb_ctx c = nullptr;
+  const int rc = oocgb_ctx_create(device, 0, 1, nullptr, cuda_stream, &c);
+  if (rc != OOCGB_OK) return rc;
+  c->rank = rank;
+  c->world = world;
+  c->host_coll = fn;
+  c->host_coll_user = user;
   *out = c;
   API_END
 }

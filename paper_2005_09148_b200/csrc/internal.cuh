@@ -148,6 +148,8 @@ struct oocgb_ctx_s {
   bool own_stream = false;
   cudaStream_t copy_stream = nullptr;
   ncclComm_t comm = nullptr;
+  oocgb_collective_fn host_coll = nullptr;  // test transport (oocgb_ctx_create_hostcomm)
+  void *host_coll_user = nullptr;
   int live_data = 0;
   int num_sms = 148;
   bool profiling = false;
@@ -263,6 +265,7 @@ void free_work(oocgb_data d);
 // NCCL helpers (no-ops when world == 1)
 void allreduce_sum_i64(oocgb_ctx c, long long *d_buf, size_t count);
 void allreduce_max_u64(oocgb_ctx c, unsigned long long *d_buf, size_t count);
+void allgather_u32(oocgb_ctx c, const uint32_t *d_send, uint32_t *d_recv, size_t count);
 
 // profiling: when ctx->profiling, records an event pair around a phase on the ctx stream
 // (no synchronisation); oocgb_get_timings() later sums the elapsed times into timings[slot].

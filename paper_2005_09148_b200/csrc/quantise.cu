@@ -226,7 +226,7 @@ void cuts_finalize(oocgb_data d) {
     OOCGB_CK(cudaMemcpyAsync(padded, rowmajor, sizeof(uint32_t) * (size_t)n_local_sample * m,
                              cudaMemcpyDeviceToDevice, c->stream));
     gathered = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<unsigned long long>(1, maxc) * m * c->world);
-    OOCGB_NCCL(nccl_api().AllGather(padded, gathered, (size_t)maxc * m, ncclUint32, c->comm, c->stream));
+    allgather_u32(c, padded, gathered, (size_t)maxc * m);
     OOCGB_CK(cudaStreamSynchronize(c->stream));
     dfree(padded);
     rowmajor = gathered;

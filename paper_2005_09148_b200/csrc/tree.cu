@@ -1191,7 +1191,12 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   }
   GraphKey key{n, D, m, ridx_mode, keep_debug ? 1 : 0, c->profiling ? 1 : 0, c->world, lambda, gamma, mcw, eta,
                bins, pitch, d->quant_bits};
-  if (!w->graph || !(w->key == key)) {
+  if (c->host_coll) {
+    // host-callback collectives synchronise the stream: run the level loop directly
+    drop_graph(w);
+    record_build(d, D, lambda, gamma, mcw, eta, keep_debug, bins, pitch, ridx_mode,
+                 c->profiling ? &w->graph_events : nullptr);
+  } else if (!w->graph || !(w->key == key)) {
     drop_graph(w);
     cudaGraph_t g;
     OOCGB_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -1208,7 +1213,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     w->key = key;
     c->timings[9] += 1.0;  // graph captures (diagnostic)
   }
-  OOCGB_CK(cudaGraphLaunch(w->graph, c->stream));
+  if (!c->host_coll) OOCGB_CK(cudaGraphLaunch(w->graph, c->stream));
   const int cur = w->final_cur;
   // export
   std::vector<DNode> hn(n_nodes);

@@ -36,3 +36,20 @@ def context_for_rank(make_context, rank: int, world: int, local_rank: int, strea
     import paper_2005_09148_b200 as ob
     nid = bootstrap_nccl_id(rank, ob.nccl_unique_id) if world > 1 else None
     return make_context(local_rank, rank, world, nid, stream)
+
+
+def gloo_collective(group=None):
+    """Host transport for Context(host_collective=...): op 0 sum, 1 max, 2 all-gather (the
+    caller's buffer is zero outside its own block, so a sum gathers), through torch.distributed
+    on CPU tensors (gloo).  Values are widened to int64 for the reduction (uint64 maxima here are
+    bit patterns of non-negative doubles, < 2^63)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    def fn(op, arr):
+        t = torch.from_numpy(arr.astype(np.int64))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM, group=group)
+        arr[...] = t.numpy().astype(arr.dtype)
+
+    return fn
