@@ -1,0 +1,129 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times, on outputs
+the oracle can compute: config 2 (1M x 500) cuts of sampled features, bins of sampled rows, the
+complete root histogram, the root split and the level-1 partition; config 3 scale (20M rows)
+complete MVS sample set.  Plus degenerate inputs (0 rows, 1 row, max_bin = 2, depth 16)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+ob = pytest.importorskip("paper_2005_09148_b200")
+
+
+@pytest.fixture(scope="module")
+def config2():
+    X, y = synth.fast_classification(1_000_000, 500, seed=1000)  # bench.py's rank-0 data
+    return X, y
+
+
+def test_config2_cuts_bins_root_histogram_split(ctx, config2):
+    X, y = config2
+    n, m = X.shape
+    d = ctx.quantise(X, 256)
+    gv, gp = d.get_cuts()
+    rng = np.random.default_rng(0)
+    feats = np.sort(rng.choice(m, size=8, replace=False))
+    # cuts of sampled features (oracle sorts the full 1M-value column, R1)
+    cv, cp = oracle.cuts(np.ascontiguousarray(X[:, feats]), 256)
+    for k, j in enumerate(feats):
+        np.testing.assert_array_equal(gv[gp[j]:gp[j + 1]], cv[cp[k]:cp[k + 1]], err_msg=f"feature {j}")
+    # full cuts from the oracle are needed for bins / trees: 500 x sort(1M) ~ 1 min single thread
+    cv_all, cp_all = oracle.cuts(X, 256)
+    assert gv.tobytes() == cv_all.tobytes() and np.array_equal(gp, cp_all)
+    rows = np.sort(rng.choice(n, size=10_000, replace=False))
+    B_s = oracle.bins(X[rows], cv_all, cp_all)
+    np.testing.assert_array_equal(d.get_bins()[rows], B_s)
+    # one round at f = 1 with bench.py's parameters; root histogram + depth-1 tree
+    margin = np.zeros(n, np.float32)
+    g, h = oracle.logistic_grad(margin, y)
+    d.set_gradients(g, h)
+    d.sample(ob.SAMPLE_NONE, 1.0, quant_bits=16)
+    t = d.build_tree(1, 1.0, 0.0, 1.0, 0.1, keep_debug=True)
+    B = oracle.bins(X, cv_all, cp_all)
+    qg, e_g = oracle.quantise(g.astype(np.float64), 16)
+    qh, e_h = oracle.quantise(h.astype(np.float64), 16)
+    on, lor, hist = oracle.build_tree(B, m, cv_all, cp_all, qg, qh, e_g, e_h, 1, want_hist=True)
+    np.testing.assert_array_equal(t.get_histogram(0), hist[0])
+    gn = t.export()
+    for f in on.dtype.names:
+        np.testing.assert_array_equal(gn[f], on[f], err_msg=f)
+    np.testing.assert_array_equal(t.get_partition(n), lor)
+    t.close()
+    # the bench's depth-8 tree: conservation and sibling consistency of the GPU tree itself
+    t8 = d.build_tree(8)
+    n8 = t8.export()
+    for v in range(255):
+        if n8["feature"][v] >= 0:
+            assert n8["n_rows"][2 * v + 1] + n8["n_rows"][2 * v + 2] == n8["n_rows"][v]
+            assert n8["gain"][v] > 0
+    assert n8["n_rows"][0] == n
+    t8.close()
+    d.close()
+
+
+def test_config3_scale_mvs_sample_set(ctx):
+    """20M rows (config 3's row count), MVS f = 0.1: the complete selected set, k*, mu and the
+    fixed-point pairs are bit-exact against the oracle's sort-based threshold (R9)."""
+    n = 20_000_000
+    g, h = synth.gradient_pairs(n, seed=21, kind="logistic")
+    X = np.zeros((n, 1), np.float32)
+    d = ctx.quantise(X, 2)
+    d.set_gradients(g, h)
+    info = d.sample(ob.SAMPLE_MVS, 0.1, 1.0, seed=4, round=11, quant_bits=16)
+    s = oracle.sample(g, h, oracle.SAMPLE_MVS, 0.1, 1.0, 4, 11)
+    sel = s["selected"].astype(bool)
+    assert info["n_selected_local"] == s["n_selected"]
+    assert (info["k_star"], info["mu"]) == (s["k_star"], s["mu"])
+    gid, qg, qh = d.get_sample(info["n_selected_local"])
+    np.testing.assert_array_equal(gid, np.nonzero(sel)[0])
+    og, e_g = oracle.quantise(s["gs"][sel], 16)
+    oh, e_h = oracle.quantise(s["hs"][sel], 16)
+    assert (info["e_g"], info["e_h"]) == (e_g, e_h)
+    np.testing.assert_array_equal(qg, og)
+    np.testing.assert_array_equal(qh, oh)
+    d.close()
+
+
+def test_zero_rows(ctx):
+    X = np.zeros((0, 7), np.float32)
+    d = ctx.quantise(X, 256)
+    cv, cp = d.get_cuts()
+    assert list(cp) == list(range(8)) and np.all(cv == 0)  # R1: empty column -> one cut 0.0
+    d.set_gradients(np.zeros(0, np.float32), np.zeros(0, np.float32))
+    info = d.sample(ob.SAMPLE_MVS, 0.5)
+    assert info["n_selected_global"] == 0
+    t = d.build_tree(4)
+    nd = t.export()
+    assert nd["feature"][0] == -1 and nd["n_rows"][0] == 0 and nd["leaf_value"][0] == 0.0
+    assert np.all(nd["feature"][1:] == -2)
+    assert d.predict([t], np.zeros(0, np.float32)).shape == (0,)
+    t.close()
+    d.close()
+
+
+# depth 16 (the ABI maximum) with tiny m: keep_debug stores (2^D - 1) node histograms
+@pytest.mark.parametrize("n,m,max_bin,depth", [(1, 5, 256, 3), (300, 3, 2, 16), (64, 40, 4, 10)])
+def test_degenerate_shapes_match_oracle(ctx, n, m, max_bin, depth):
+    rng = np.random.default_rng(n + m)
+    X = rng.normal(size=(n, m)).astype(np.float32)
+    y = (rng.random(n) < 0.5).astype(np.float32)
+    cv, cp = oracle.cuts(X, max_bin)
+    B = oracle.bins(X, cv, cp)
+    g, h = oracle.logistic_grad(rng.normal(size=n).astype(np.float32), y)
+    qg, e_g = oracle.quantise(g.astype(np.float64), 16)
+    qh, e_h = oracle.quantise(h.astype(np.float64), 16)
+    on, lor, _ = oracle.build_tree(B, m, cv, cp, qg, qh, e_g, e_h, depth, 1.0, 0.0, 0.0, 0.1)
+    d = ctx.quantise(X, max_bin)
+    np.testing.assert_array_equal(d.get_bins(), B)
+    d.set_gradients(g, h)
+    d.sample(ob.SAMPLE_NONE, 1.0)
+    t = d.build_tree(depth, 1.0, 0.0, 0.0, 0.1, keep_debug=True)
+    gn = t.export()
+    for f in on.dtype.names:
+        np.testing.assert_array_equal(gn[f], on[f], err_msg=f)
+    np.testing.assert_array_equal(t.get_partition(n), lor)
+    t.close()
+    d.close()
