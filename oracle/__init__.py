@@ -81,6 +81,8 @@ def _declare(L):
     L.orc_bins.restype = ctypes.c_int
     L.orc_sample.argtypes = [_p, _p, _i64, _i32, _d, _d, _u64, _u64, _p, _p, _p, _p, _p]
     L.orc_sample.restype = ctypes.c_int
+    L.orc_sample_goss.argtypes = [_p, _p, _i64, _d, _d, _u64, _u64, _p, _p, _p, _p, _p]
+    L.orc_sample_goss.restype = ctypes.c_int
     L.orc_quantise.argtypes = [_p, _i64, _i32, _p]
     L.orc_quantise.restype = ctypes.c_int
     L.orc_histogram.argtypes = [_p, _i32, _i32, _p, _i64, _p, _p, _p]
@@ -176,6 +178,24 @@ def sample(g, h, mode: int, ratio: float, mvs_lambda: float = 1.0, seed: int = 1
         raise OracleError(f"orc_sample rc={rc}")
     return dict(selected=sel, p=p, gs=gs, hs=hs, n_selected=int(info[0]), k_star=int(info[1]),
                 mu=float(info[2]), e_prime=int(info[3]))
+
+
+def sample_goss(g, h, a: float, b: float, seed: int = 1, round_: int = 0):
+    """O4b GOSS: returns dict(selected, p, gs, hs, n_selected, k_a, t, e_prime)."""
+    g = _c(g, np.float32)
+    h = _c(h, np.float32)
+    n = g.shape[0]
+    sel = np.zeros(n, np.uint8)
+    p = np.zeros(n, np.float64)
+    gs = np.zeros(n, np.float64)
+    hs = np.zeros(n, np.float64)
+    info = np.zeros(4, np.float64)
+    rc = lib().orc_sample_goss(_ptr(g), _ptr(h), n, a, b, seed, round_, _ptr(sel), _ptr(p), _ptr(gs), _ptr(hs),
+                               _ptr(info))
+    if rc != 0:
+        raise OracleError(f"orc_sample_goss rc={rc}")
+    return dict(selected=sel, p=p, gs=gs, hs=hs, n_selected=int(info[0]), k_a=int(info[1]), t=float(info[2]),
+                e_prime=int(info[3]))
 
 
 # ---------------------------------------------------------------------------------------- O5

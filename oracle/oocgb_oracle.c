@@ -20,6 +20,8 @@
  *   orc_bins           pinned: SPEC examples, np.searchsorted, brute-force linear scan
  *   orc_sample         pinned: closed forms, Fraction brute force, Monte-Carlo
  *                      unbiasedness, sum p = f n, monotone inclusion
+ *   orc_sample_goss    pinned: SPEC S:L313 example, top-set = np.argsort definition, Monte-Carlo
+ *                      unbiasedness, scale (1-a)/b
  *   orc_quantise       pinned: closed-form round trip, |q| <= 2^P, exact dequantisation
  *   orc_histogram      pinned: brute-force masks, conservation, additivity
  *   orc_build_tree     pinned: exhaustive greedy enumeration from raw rows (n <= 256),
@@ -275,6 +277,62 @@ int orc_sample(const float *g, const float *h, int64_t n, int32_t mode, double r
     }
   }
   info[0] = (double)ns;
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * O4b. GOSS: "the top a x 100% of training instances with
+ * the largest gradients are selected, then from the rest of the data a random sample of
+ * b x 100% instances is drawn.  The samples are scaled by (1-a)/b".  Reading R25:
+ * |g| is quantised like MVS's g_hat (e' from frexp(max |g|)); k_a = round(a_q n / 2^32) (half
+ * up) with a_q = rint(a 2^32); t = the k_a-th largest |g|_q (no top set when k_a = 0, or when t = 0);
+ * top rows (|g|_q >= t) have p = 1; every other row is drawn Bernoulli(p_rest) with
+ * p_rest = b_q / (2^32 - a_q) (expected b n rows) and scaled g' = g / p_rest, h' = h / p_rest
+ * (= (1-a)/b).  info: [0] n_selected, [1] k_a, [2] t (as double), [3] e'.
+ * ---------------------------------------------------------------------------------------- */
+int orc_sample_goss(const float *g, const float *h, int64_t n, double a, double b, uint64_t seed,
+                    uint64_t round, uint8_t *selected, double *p, double *gs, double *hs,
+                    double *info) {
+  if (!(a >= 0.0 && b > 0.0 && a + b <= 1.0)) return 2;
+  uint64_t a_q = (uint64_t)nearbyint(a * 4294967296.0);
+  uint64_t b_q = (uint64_t)nearbyint(b * 4294967296.0);
+  if (a_q >= 4294967296ULL) return 2;
+  double p_rest = (double)b_q / (double)(4294967296ULL - a_q);
+  if (p_rest > 1.0) p_rest = 1.0;
+  double gmax = 0.0;
+  for (int64_t i = 0; i < n; ++i) if (fabs((double)g[i]) > gmax) gmax = fabs((double)g[i]);
+  int64_t *q = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  int64_t *sorted = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  int e = 0;
+  if (gmax > 0.0) {
+    int kM;
+    frexp(gmax, &kM);
+    e = (62 - ceil_log2_i64(n)) - kM;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    q[i] = gmax > 0.0 ? (int64_t)nearbyint(ldexp(fabs((double)g[i]), e)) : 0;
+    sorted[i] = q[i];
+  }
+  qsort(sorted, (size_t)n, sizeof(int64_t), cmp_i64_desc);
+  int64_t k_a = (int64_t)(((unsigned __int128)a_q * (unsigned __int128)n + (1ULL << 31)) >> 32);
+  int64_t t = INT64_MAX;  /* no top set */
+  if (k_a > 0 && sorted[k_a - 1] > 0) t = sorted[k_a - 1];
+  int64_t ns = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int top = q[i] >= t;
+    p[i] = top ? 1.0 : p_rest;
+    int sel = top || orc_uniform(seed, round, (uint64_t)i, 0) < p_rest;
+    selected[i] = (uint8_t)sel;
+    gs[i] = sel ? (double)g[i] / p[i] : 0.0;
+    hs[i] = sel ? (double)h[i] / p[i] : 0.0;
+    ns += sel;
+  }
+  info[0] = (double)ns;
+  info[1] = (double)k_a;
+  info[2] = (double)t;
+  info[3] = (double)e;
+  free(q);
+  free(sorted);
   return 0;
 }
 

@@ -272,6 +272,50 @@ def test_all_zero_ghat_falls_back_to_uniform():
     assert abs(s["n_selected"] / n - 0.25) < 0.03
 
 
+def test_goss_worked_example():
+    """Golden S:L313: |g| = [5,4,3,2,1], a = 0.2, b = 0.25 -> the |g| = 5 row always (scale 1),
+    the others with p = b / (1 - a) and scale (1 - a) / b = 3.2."""
+    ex = GOLD["goss"]
+    g = np.array(ex["abs_g"], np.float32) * np.array([1, -1, 1, -1, 1], np.float32)
+    h = np.ones(5, np.float32)
+    hits = np.zeros(5)
+    for seed in range(400):
+        s = oracle.sample_goss(g, h, ex["a"], ex["b"], seed=seed)
+        assert s["selected"][0] == 1 and s["p"][0] == 1.0 and s["gs"][0] == g[0]
+        assert s["k_a"] == 1
+        rest = s["selected"][1:].astype(bool)
+        np.testing.assert_allclose(s["gs"][1:][rest] / g[1:][rest], ex["rest_scale"], rtol=1e-9)
+        hits += s["selected"]
+    assert abs(hits[1:].mean() / 400 - ex["b"] / (1 - ex["a"])) < 0.05
+
+
+def test_goss_top_set_is_argsort_definition():
+    """The top set = the k_a largest |g| (np.argsort, library routine), ties to the same side."""
+    g, h = synth.gradient_pairs(5000, seed=3, kind="wide")
+    s = oracle.sample_goss(g, h, 0.1, 0.2, seed=1)
+    k = s["k_a"]
+    assert k == int((round(0.1 * 2**32) * 5000 + 2**31) >> 32) == 500
+    order = np.argsort(-np.abs(g.astype(np.float64)), kind="stable")
+    thr = np.abs(g[order[k - 1]])
+    top = np.abs(g) >= thr
+    np.testing.assert_array_equal(s["p"] == 1.0, top)
+    assert top.sum() >= k
+
+
+def test_goss_unbiased_monte_carlo():
+    """P:L228 'scaled by (1-a)/b to make the gradient statistics unbiased': mean over 1000 seeds of
+    sum selected g' within 2% (and h')."""
+    g, h = synth.gradient_pairs(1000, seed=12, kind="logistic")
+    G, H = float(np.sum(g, dtype=np.float64)), float(np.sum(h, dtype=np.float64))
+    sg, sh = [], []
+    for seed in range(1000):
+        s = oracle.sample_goss(g, h, 0.1, 0.2, seed=seed, round_=5)
+        sg.append(s["gs"].sum())
+        sh.append(s["hs"].sum())
+    assert abs(np.mean(sg) - G) <= 0.02 * np.sum(np.abs(g))
+    assert abs(np.mean(sh) - H) <= 0.02 * abs(H)
+
+
 # ------------------------------------------------------------------------------ O5 fixed point
 def test_quantise_properties():
     rng = np.random.default_rng(0)
