@@ -47,7 +47,7 @@ typedef struct oocgb_data_s *oocgb_data; /* cuts + ELLPACK pages + per-round row
 typedef struct oocgb_tree_s *oocgb_tree; /* one regression tree f_k (Eq. 1) + debug dumps      */
 
 enum { OOCGB_PLACE_DEVICE = 0, OOCGB_PLACE_PINNED_HOST = 1 };
-enum { OOCGB_SAMPLE_NONE = 0, OOCGB_SAMPLE_UNIFORM = 1, OOCGB_SAMPLE_MVS = 2 };
+enum { OOCGB_SAMPLE_NONE = 0, OOCGB_SAMPLE_UNIFORM = 1, OOCGB_SAMPLE_MVS = 2, OOCGB_SAMPLE_GOSS = 3 };
 
 /* Exported tree node, heap order: children of i are 2i+1 (left: bin <= split_bin, i.e.
  * x <= split_value) and 2i+2.  feature = -1 leaf, -2 absent slot below a leaf.
@@ -161,6 +161,15 @@ int oocgb_set_logistic_gradients(oocgb_data data, const float *margin, const flo
  * the f = 1 in-core path runs without any host synchronisation.                           */
 int oocgb_sample(oocgb_data data, int32_t mode, double ratio, double mvs_lambda, uint64_t seed,
                  uint64_t round, int32_t quant_bits, oocgb_sample_info *info);
+
+/* GOSS (R25): the round(a n) rows with the largest |g| (quantised like MVS's g_hat;
+ * ties at the threshold all included) are kept with p = 1; every other row is drawn
+ * Bernoulli(p_rest), p_rest = rint(b 2^32) / (2^32 - rint(a 2^32)), and scaled by 1 / p_rest
+ * (= (1-a)/b, "to make the gradient statistics unbiased").  Same Philox draws, fixed point and
+ * compaction as oocgb_sample.  ERR_ARG unless 0 <= a, 0 < b, a + b <= 1.  info->k_star = the top
+ * count round(a n), info->mu = p_rest.                                                        */
+int oocgb_sample_goss(oocgb_data data, double a, double b, uint64_t seed, uint64_t round,
+                      int32_t quant_bits, oocgb_sample_info *info);
 
 /* build_tree (Alg. 1, depth-wise R16): histograms (fixed-point int, bit-exact), sibling
  * subtraction (R17), split evaluation (Eq. 8, R13-R14), stable partition, leaf values

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "liboocgb.so")
 
 OK, ERR_ARG, ERR_NOMEM, ERR_DEVICE, ERR_STATE = 0, 2, 3, 4, 5
 PLACE_DEVICE, PLACE_PINNED_HOST = 0, 1
-SAMPLE_NONE, SAMPLE_UNIFORM, SAMPLE_MVS = 0, 1, 2
+SAMPLE_NONE, SAMPLE_UNIFORM, SAMPLE_MVS, SAMPLE_GOSS = 0, 1, 2, 3
 
 # Every symbol include/oocgb.h declares (tests check the library exports all of them).
 ABI_SYMBOLS = (
@@ -32,7 +32,7 @@ ABI_SYMBOLS = (
     "oocgb_tree_destroy", "oocgb_predict", "oocgb_update_margin", "oocgb_get_cuts",
     "oocgb_get_bins", "oocgb_get_sample", "oocgb_get_histogram", "oocgb_get_partition",
     "oocgb_get_timings", "oocgb_set_profiling", "oocgb_last_error", "oocgb_abi_version",
-    "oocgb_ctx_create_hostcomm",
+    "oocgb_ctx_create_hostcomm", "oocgb_sample_goss",
 )
 
 COLLECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
@@ -113,6 +113,7 @@ def load_library():
         "oocgb_get_timings": [p, p, i32],
         "oocgb_set_profiling": [p, i32],
         "oocgb_ctx_create_hostcomm": [i32, i32, i32, COLLECTIVE_FN, p, u64, p],
+        "oocgb_sample_goss": [p, d, d, u64, u64, i32, p],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -272,6 +273,12 @@ class Data:
         si = SampleInfo()
         _check(load_library().oocgb_sample(self._h, mode, ratio, mvs_lambda, seed, round, quant_bits,
                                             ctypes.byref(si)))
+        return {k: getattr(si, k) for k, _ in SampleInfo._fields_}
+
+    def sample_goss(self, a: float, b: float, seed: int = 1, round: int = 0, quant_bits: int = 16) -> dict:
+        """GOSS: top round(a n) by |g| with p = 1, the rest Bernoulli(b / (1 - a)), scale 1/p."""
+        si = SampleInfo()
+        _check(load_library().oocgb_sample_goss(self._h, a, b, seed, round, quant_bits, ctypes.byref(si)))
         return {k: getattr(si, k) for k, _ in SampleInfo._fields_}
 
     def build_tree(self, max_depth: int = 8, lam: float = 1.0, gamma: float = 0.0,

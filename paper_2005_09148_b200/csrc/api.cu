@@ -589,6 +589,21 @@ int oocgb_sample(oocgb_data d, int32_t mode, double ratio, double mvs_lambda, ui
   API_END
 }
 
+int oocgb_sample_goss(oocgb_data d, double a, double b, uint64_t seed, uint64_t round, int32_t quant_bits,
+                      oocgb_sample_info *info) {
+  API_BEGIN
+  OOCGB_REQUIRE(d, OOCGB_ERR_ARG, "data is NULL");
+  OOCGB_REQUIRE(a >= 0.0 && b > 0.0 && a + b <= 1.0 && std::isfinite(a) && std::isfinite(b), OOCGB_ERR_ARG,
+                "GOSS needs 0 <= a, 0 < b, a + b <= 1 (S:L309)");
+  OOCGB_REQUIRE(nearbyint(a * 4294967296.0) < 4294967296.0, OOCGB_ERR_ARG, "GOSS needs a < 1");
+  OOCGB_REQUIRE(quant_bits >= 8 && quant_bits <= 20, OOCGB_ERR_ARG, "quant_bits must be in [8, 20] (R12)");
+  OOCGB_REQUIRE(d->cuts_ready && d->rows_written == d->n_local, OOCGB_ERR_STATE, "sample: pages not complete");
+  OOCGB_REQUIRE(d->has_grad, OOCGB_ERR_STATE, "sample before set_gradients");
+  bind(d->ctx);
+  sample_rows(d, OOCGB_SAMPLE_GOSS, a, 0.0, seed, round, quant_bits, info, b);
+  API_END
+}
+
 int oocgb_build_tree(oocgb_data d, int32_t max_depth, double lambda, double gamma, double min_child_weight,
                      double eta, int32_t keep_debug, oocgb_tree *out) {
   API_BEGIN

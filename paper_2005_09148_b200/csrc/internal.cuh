@@ -251,7 +251,7 @@ void bin_rows(oocgb_data d, const float *dX, int64_t n, int64_t row_local0, uint
 // sample.cu
 void logistic_gradients(oocgb_data d, const float *d_margin, const float *d_labels);
 void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64_t seed,
-                 uint64_t round, int quant_bits, oocgb_sample_info *info);
+                 uint64_t round, int quant_bits, oocgb_sample_info *info, double goss_b = 0.0);
 
 // tree.cu
 oocgb_tree build_tree(oocgb_data d, int max_depth, double lambda, double gamma, double mcw,

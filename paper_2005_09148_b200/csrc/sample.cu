@@ -110,7 +110,7 @@ __global__ void k_threshold_totals(const long long *__restrict__ q, int64_t n, l
 }
 
 struct SelParams {
-  int mode;          // 1 uniform, 2 mvs
+  int mode;          // 1 uniform, 2 mvs, 3 goss (p_uniform = p_rest, t = top threshold)
   double p_uniform;  // f_q 2^-32
   int has_t;         // MVS: threshold exists
   long long t;       // MVS t* = a_{k*+1}
@@ -121,6 +121,7 @@ struct SelParams {
 
 __device__ __forceinline__ double sel_prob(const SelParams &P, const long long *q64, int64_t i) {
   if (P.mode == 1) return P.p_uniform;
+  if (P.mode == 3) return (P.has_t && q64[i] >= P.t) ? 1.0 : P.p_uniform;
   long long v = q64[i];
   if (v == 0) return 0.0;
   if (!P.has_t) return 1.0;
@@ -212,7 +213,7 @@ __global__ void k_select_scatter(SelParams P, const long long *__restrict__ q64,
     if (local[k]) {
       sel_rows[pos] = (int32_t)i;
       double gi = (double)g[i], hi = (double)h[i];
-      if (P.mode == 2) {
+      if (P.mode >= 2) {
         double p = sel_prob(P, q64, i);
         gi = __ddiv_rn(gi, p);
         hi = __ddiv_rn(hi, p);
@@ -352,7 +353,7 @@ static void ensure_sample_buffers(oocgb_data d) {
 }
 
 void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64_t seed,
-                 uint64_t round, int quant_bits, oocgb_sample_info *info) {
+                 uint64_t round, int quant_bits, oocgb_sample_info *info, double goss_b) {
   oocgb_ctx c = d->ctx;
   PhaseTimer timer(c, 3);
   const int64_t n = d->n_local;
@@ -473,7 +474,63 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       }
     }
   }
-  P.mode = eff_mode == OOCGB_SAMPLE_MVS ? 2 : 1;
+  if (mode == OOCGB_SAMPLE_GOSS) {
+    // R25: |g| quantised like g_hat (lambda = 0: sqrt(g^2) = |g| exactly), the k_a-th largest
+    // by a radix select over the counts, then Bernoulli(p_rest) for the rest, scale 1/p
+    const uint64_t a_q = (uint64_t)nearbyint(ratio * 4294967296.0);
+    const uint64_t b_q = (uint64_t)nearbyint(goss_b * 4294967296.0);
+    double p_rest = (double)b_q / (double)(4294967296ULL - a_q);
+    if (p_rest > 1.0) p_rest = 1.0;
+    const long long k_a = (long long)(((unsigned __int128)a_q * (unsigned __int128)d->n_global + (1ULL << 31)) >> 32);
+    P.p_uniform = p_rest;
+    P.has_t = 0;
+    OOCGB_CK(cudaMemsetAsync(d_u, 0, 8, c->stream));
+    if (n > 0)
+      k_ghat<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, n, 0.0, (double *)d->d_tmp64, d_u);
+    allreduce_max_u64(c, d_u, 1);
+    OOCGB_CK(cudaMemcpyAsync(h_u, d_u, 8, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    double gmax;
+    memcpy(&gmax, h_u, 8);
+    int e = 0;
+    if (gmax > 0.0) {
+      int kM;
+      frexp(gmax, &kM);
+      e = (62 - ceil_log2(d->n_global)) - kM;
+    }
+    si.e_prime = e;
+    if (n > 0) k_ghat_q<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, ldexp(1.0, e));
+    if (k_a > 0 && gmax > 0.0) {
+      // radix select of the k_a-th largest value over [0, 2^63)
+      const int shifts[6] = {52, 41, 30, 19, 8, 0};
+      const int widths[6] = {11, 11, 11, 11, 11, 8};
+      unsigned long long lo = 0, above = 0;
+      unsigned long long *d_stats = d_u + 16;
+      unsigned long long *h_stats = h_u + 16;
+      for (int pass = 0; pass < 6; ++pass) {
+        const int nb = 1 << widths[pass], sh = shifts[pass];
+        OOCGB_CK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 3 * nb, c->stream));
+        if (n > 0)
+          k_radix_stats<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, lo, sh, nb, d_stats,
+                                                               d_stats + nb, d_stats + 2 * nb);
+        OOCGB_CK(cudaGetLastError());
+        allreduce_sum_i64(c, (long long *)d_stats, (size_t)nb);
+        OOCGB_CK(cudaMemcpyAsync(h_stats, d_stats, sizeof(unsigned long long) * nb, cudaMemcpyDeviceToHost, c->stream));
+        OOCGB_CK(cudaStreamSynchronize(c->stream));
+        int j = nb - 1;
+        for (; j > 0; --j) {
+          if (above + h_stats[j] >= (unsigned long long)k_a) break;
+          above += h_stats[j];
+        }
+        lo += (unsigned long long)j << sh;
+      }
+      if (lo > 0) { P.has_t = 1; P.t = (long long)lo; }
+    }
+    si.k_star = k_a;
+    si.mu = p_rest;
+    eff_mode = OOCGB_SAMPLE_GOSS;
+  }
+  P.mode = eff_mode == OOCGB_SAMPLE_MVS ? 2 : (eff_mode == OOCGB_SAMPLE_GOSS ? 3 : 1);
 
   if (!d->d_ss) {
     d->d_ss = (SampleState *)dmalloc(sizeof(SampleState));

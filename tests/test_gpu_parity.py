@@ -112,6 +112,29 @@ def test_sample_bit_exact(ctx, mode, ratio, kind, n):
     d.close()
 
 
+@pytest.mark.parametrize("a,b", [(0.1, 0.1), (0.2, 0.25), (0.0, 0.5), (0.3, 0.7)])
+@pytest.mark.parametrize("kind", ["logistic", "wide", "ties"])
+@pytest.mark.parametrize("n", [5, 3001, 40000])
+def test_goss_bit_exact(ctx, a, b, kind, n):
+    X = np.zeros((n, 2), np.float32)
+    g, h = synth.gradient_pairs(n, seed=n + 7, kind=kind)
+    d = ctx.quantise(X, 16)
+    d.set_gradients(g, h)
+    info = d.sample_goss(a, b, seed=13, round=4, quant_bits=16)
+    s = oracle.sample_goss(g, h, a, b, 13, 4)
+    sel = s["selected"].astype(bool)
+    assert info["n_selected_local"] == s["n_selected"]
+    assert info["k_star"] == s["k_a"]
+    gid, gq, hq = d.get_sample(info["n_selected_local"])
+    np.testing.assert_array_equal(gid, np.nonzero(sel)[0])
+    qg, e_g = oracle.quantise(s["gs"][sel], 16)
+    qh, e_h = oracle.quantise(s["hs"][sel], 16)
+    assert (info["e_g"], info["e_h"]) == (e_g, e_h)
+    np.testing.assert_array_equal(gq, qg)
+    np.testing.assert_array_equal(hq, qh)
+    d.close()
+
+
 # ------------------------------------------------------------------------------------------ trees
 def _oracle_tree(B, m, cv, cp, g, h, mode, ratio, depth, quant_bits=16, lam=1.0, gamma=0.0, mcw=1.0,
                  eta=0.1, seed=1, round_=0):
