@@ -46,10 +46,12 @@ def parse():
     ap.add_argument("--rows", type=int, default=N_ROWS, help="rows per GPU (config 2: 1M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON line)")
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4],
                     help="2: 1M x 500 in-core f=1 (the driver's bench); 3: 20M x 500 out-of-core, "
                          "32 MiB pinned pages, MVS f=0.1")
     ap.add_argument("--rows3", type=int, default=20_000_000, help="config 3 rows")
+    ap.add_argument("--rows4", type=int, default=100_000_000, help="config 4 training rows")
+    ap.add_argument("--rounds4", type=int, default=50, help="config 4 boosting rounds per setting")
     return ap.parse_args()
 
 
@@ -305,9 +307,94 @@ def run_config3(args, rank, world, local):
     ctx.close()
 
 
+def run_config4(args, rank, world, local):
+    """Config 4 (BASELINE.json configs[3]): 100M x 500 in-core (51.2 GB of ELLPACK in HBM), 5M
+    held-out rows (P:L460-461's 0.95/0.05 split analogue).  For f = 1 and for uniform (SGB), MVS
+    and GOSS sampling at f in {0.1, 0.3, 0.5}: `rounds4` boosting rounds (depth 8, eta 0.1) from
+    margin 0, then the held-out AUC (sklearn.metrics.roc_auc_score on the binned predict) and the
+    median sec/round.  The paper's claim: MVS keeps accuracy at rates as low as 10% (P:L242-243,
+    Fig. 1, Table 2)."""
+    import torch
+    from sklearn.metrics import roc_auc_score
+    import paper_2005_09148_b200 as ob
+    import synth
+    n, m, n_eval = args.rows4, N_FEAT, 5_000_000
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = ob.Context(local, rank, world, None, stream=stream.cuda_stream)
+    chunk = 1 << 21
+    t0 = time.perf_counter()
+    d = ctx.sketch_begin(m, MAX_BIN, n, seed=2)
+    for r0 in range(0, n, chunk):
+        X, _ = synth.torch_classification_chunk(r0, min(chunk, n - r0), m, seed=4)
+        d.sketch_push(X, r0)
+    d.cuts_finalize()
+    ys = []
+    for r0 in range(0, n, chunk):
+        X, y = synth.torch_classification_chunk(r0, min(chunk, n - r0), m, seed=4)
+        d.pages_push(X, r0)
+        ys.append(y)
+    labels = torch.cat(ys)
+    del ys
+    Xe, ye = synth.torch_classification_chunk(n, n_eval, m, seed=4)  # held-out rows n .. n + 5M
+    de = d.quantise_like(Xe)
+    del Xe, X
+    torch.cuda.synchronize()
+    prep_s = time.perf_counter() - t0
+    settings = [("none", 1.0)] + [(mode, f) for mode in ("uniform", "mvs", "goss") for f in (0.1, 0.3, 0.5)]
+    results = []
+    for mode, f in settings:
+        margin = torch.zeros(n, dtype=torch.float32, device="cuda")
+        em = torch.zeros(n_eval, dtype=torch.float32, device="cuda")
+        trees, times = [], []
+        for r in range(args.rounds4):
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            if trees:
+                d.predict([trees[-1]], margin)   # every row gets the new tree (R18)
+            d.set_logistic_gradients(margin, labels)
+            if mode == "none":
+                d.sample(ob.SAMPLE_NONE, 1.0, round=r, quant_bits=QBITS, want_info=False)
+            elif mode == "uniform":
+                d.sample(ob.SAMPLE_UNIFORM, f, seed=1, round=r, quant_bits=QBITS)
+            elif mode == "mvs":
+                d.sample(ob.SAMPLE_MVS, f, 1.0, seed=1, round=r, quant_bits=QBITS)
+            else:  # GOSS with a = b = f / 2
+                d.sample_goss(f / 2, f / 2, seed=1, round=r, quant_bits=QBITS)
+            t = d.build_tree(DEPTH, LAMBDA, GAMMA, MCW, ETA)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+            trees.append(t)
+        de.predict(trees, em)
+        auc = roc_auc_score(ye.cpu().numpy(), em.cpu().numpy())
+        for t in trees:
+            t.close()
+        results.append({"mode": mode, "f": f, "auc": auc, "ms_per_round_median": statistics.median(times[1:]),
+                        "rounds": args.rounds4})
+        print(json.dumps(results[-1]), file=sys.stderr, flush=True)
+    base = results[0]["auc"]
+    for r_ in results:
+        r_["auc_rel_diff_vs_f1"] = (r_["auc"] - base) / base
+    line = {"config": {"workload": "config 4: 100M x 500 in-core (51.2 GB ELLPACK), 5M held-out rows, depth 8, "
+                                   f"eta 0.1, {args.rounds4} rounds; GOSS a = b = f/2",
+                       "rows": n, "held_out": n_eval, "n_features": m},
+            "data": "synthetic (make_classification-style, generated on the GPU per chunk, seeded)",
+            "prep_s": prep_s, "results": results}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    de.close()
+    d.close()
+    ctx.close()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.config == 4 and args.impl == "ours":
+        run_config4(args, rank, world, local)
+        return
     if args.config == 3 and args.impl == "ours":
         run_config3(args, rank, world, local)
         return

@@ -394,17 +394,22 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       int e = (62 - ceil_log2(d->n_global)) - kM;
       si.e_prime = e;
       if (n > 0) k_ghat_q<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, ldexp(1.0, e));
-      // radix descent over [0, 2^63): passes of 11,11,11,11,11,8 bits
-      const int shifts[6] = {52, 41, 30, 19, 8, 0};
-      const int widths[6] = {11, 11, 11, 11, 11, 8};
+      // radix descent over [0, 2^qbits), qbits = bit width of the largest g_hat_q (known from
+      // the global max), in passes of <= 11 bits: starting at the top set bit keeps the first
+      // pass's buckets spread (no all-in-bucket-0 contention at large n)
+      const unsigned long long qmax = (unsigned long long)nearbyint(ldexp(gmax, e));
+      const int qbits = qmax ? 64 - __builtin_clzll(qmax) : 1;
       unsigned long long lo = 0, above = 0, below_sum = 0;
       long long below_max = -1, fallback = -1;
       bool have_fb = false, found = false;
       long long tstar = -1;
       unsigned long long *d_stats = d_u + 16;
       unsigned long long *h_stats = h_u + 16;
-      for (int pass = 0; pass < 6 && !found; ++pass) {
-        int nb = 1 << widths[pass], sh = shifts[pass];
+      for (int bits_left = qbits; bits_left > 0 && !found;) {
+        const int wdt = std::min(11, bits_left);
+        const int sh = bits_left - wdt;
+        bits_left -= wdt;
+        int nb = 1 << wdt;
         OOCGB_CK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 3 * nb, c->stream));
         if (n > 0)
           k_radix_stats<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, lo, sh, nb, d_stats,
@@ -501,14 +506,17 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
     si.e_prime = e;
     if (n > 0) k_ghat_q<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, ldexp(1.0, e));
     if (k_a > 0 && gmax > 0.0) {
-      // radix select of the k_a-th largest value over [0, 2^63)
-      const int shifts[6] = {52, 41, 30, 19, 8, 0};
-      const int widths[6] = {11, 11, 11, 11, 11, 8};
+      // radix select of the k_a-th largest value over [0, 2^qbits), passes of <= 11 bits
+      const unsigned long long qmax = (unsigned long long)nearbyint(ldexp(gmax, e));
+      const int qbits = qmax ? 64 - __builtin_clzll(qmax) : 1;
       unsigned long long lo = 0, above = 0;
       unsigned long long *d_stats = d_u + 16;
       unsigned long long *h_stats = h_u + 16;
-      for (int pass = 0; pass < 6; ++pass) {
-        const int nb = 1 << widths[pass], sh = shifts[pass];
+      for (int bits_left = qbits; bits_left > 0;) {
+        const int wdt = std::min(11, bits_left);
+        const int sh = bits_left - wdt;
+        bits_left -= wdt;
+        const int nb = 1 << wdt;
         OOCGB_CK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 3 * nb, c->stream));
         if (n > 0)
           k_radix_stats<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, lo, sh, nb, d_stats,
