@@ -657,10 +657,10 @@ int oocgb_predict(oocgb_data d, const oocgb_tree *trees, int32_t n_trees, float 
     for (int t0 = 0; t0 < n_trees; t0 += 4096) {
       int nt = std::min(4096, n_trees - t0);
       if (d->placement == OOCGB_PLACE_DEVICE) {
-        predict_device(d, d->d_bins, d->rows_per_page, d->n_local, 0, trees + t0, nt, dm);
+        predict_device(d, d->d_bins, 32, (size_t)d->rows_per_page * 32, d->n_local, 0, trees + t0, nt, dm);
       } else {
         for_each_page(d, [&](const uint8_t *page, int64_t r0, int64_t nr) {
-          predict_device(d, page, d->rows_per_page, nr, r0, trees + t0, nt, dm);
+          predict_device(d, page, (size_t)d->stride, 32, nr, r0, trees + t0, nt, dm);  // row-major page
         });
       }
     }
@@ -711,6 +711,10 @@ int oocgb_get_bins(oocgb_data d, int64_t row0_local, int64_t n, uint8_t *out) {
                 "get_bins: row range outside the written pages");
   bind(d->ctx);
   if (n == 0) return OOCGB_OK;
+  if (d->placement == OOCGB_PLACE_PINNED_HOST) {  // pinned pages are already row-major
+    memcpy(out, d->h_pages + (size_t)row0_local * d->stride, (size_t)n * d->stride);
+    return OOCGB_OK;
+  }
   // tiled pages -> row-major [n][stride] (ABI order: row i, feature j at out[i * stride + j])
   const int64_t rpp = d->rows_per_page;
   std::vector<uint8_t> page_buf;

@@ -180,8 +180,11 @@ struct oocgb_data_s {
   // Tiled ELLPACK (R5): pages of rows_per_page rows; inside a page the symbols of
   // feature group g (features 32g..32g+31) of all the page's rows are contiguous:
   //   offset(row, f) = page * (rpp * stride) + (f / 32) * (rpp * 32) + (row % rpp) * 32 + f % 32
-  uint8_t *d_bins = nullptr;    // DEVICE placement: one page, rpp = n_local
-  uint8_t *h_pages = nullptr;   // PINNED_HOST placement: n_pages pages (last one padded)
+  uint8_t *d_bins = nullptr;    // DEVICE placement: one tiled page, rpp = n_local
+  // PINNED_HOST placement: ROW-MAJOR [n_local][stride] (a row is one contiguous block, so pages
+  // stream as plain row ranges and selected rows can be gathered zero-copy over PCIe); the
+  // device-side sampled page built from it is tiled.
+  uint8_t *h_pages = nullptr;
   int64_t rows_written = 0;     // streamed pages_push progress
   // streamed sketch state
   uint32_t *d_sketch = nullptr; // column-major ordered keys [m][cap]
@@ -256,7 +259,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
 // tree.cu
 oocgb_tree build_tree(oocgb_data d, int max_depth, double lambda, double gamma, double mcw,
                       double eta, bool keep_debug);
-void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t rpp, int64_t n_rows, int64_t row_offset,
+void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t pitch, int64_t n_rows, int64_t row_offset,
                     const oocgb_tree *trees, int n_trees, float *d_margin);
 void update_margin(oocgb_data d, oocgb_tree t, float *d_margin);
 void free_work(oocgb_data d);

@@ -304,20 +304,23 @@ __global__ void k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, S
 
 // all-reduce helpers need contiguous arrays: sums (G, H) and counts live next to each other
 
-// Compact (Alg. 7): copy the selected rows of one staged page (rpp-row group planes)
-// into the sampled page (cap-row group planes): thread per (selected row, group, 16-B half).
-__global__ void k_compact_page(const uint8_t *__restrict__ page, int64_t page_row0, int64_t rpp, int n_fg,
-                               const int32_t *__restrict__ sel_rows, int64_t k0, int64_t k1, int64_t cap,
-                               uint8_t *__restrict__ out) {
-  const int64_t total = (k1 - k0) * n_fg * 2;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int h = (int)(t & 1);
-    const int g = (int)((t >> 1) % n_fg);
-    const int64_t k = k0 + (t >> 1) / n_fg;
-    const int64_t r = sel_rows[k] - page_row0;
-    *reinterpret_cast<uint4 *>(out + ((size_t)g * cap + k) * 32 + h * 16) =
-        *reinterpret_cast<const uint4 *>(page + ((size_t)g * rpp + r) * 32 + h * 16);
+// Compact (Alg. 7): row-major rows -> the tiled device sampled page.  One warp per row:
+// lane l moves 16-B chunk l (features 16l .. 16l + 15 -> group l / 2, half l % 2).  The source is
+// either a staged page in HBM (f = 1: src_rows = nullptr, row k of the output is row r0 + k of
+// the page) or the pinned host pages read zero-copy over PCIe (f < 1: only the selected rows
+// cross the link, 512 contiguous bytes per row).
+__global__ void k_rows_to_tiled(const uint8_t *__restrict__ src, int stride, const int32_t *__restrict__ src_rows,
+                                int64_t src_row0, int64_t k0, int64_t k1, int64_t cap, uint8_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int chunks = stride / 16;
+  for (int64_t k = k0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); k < k1;
+       k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = (src_rows ? (int64_t)src_rows[k] : k) - src_row0;
+    const uint8_t *srow = src + (size_t)r * stride;
+    for (int ch = lane; ch < chunks; ch += 32) {
+      const uint4 v = *reinterpret_cast<const uint4 *>(srow + ch * 16);
+      *reinterpret_cast<uint4 *>(out + ((size_t)(ch >> 1) * cap + k) * 32 + (ch & 1) * 16) = v;
+    }
   }
 }
 
@@ -610,31 +613,22 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       d->d_sampled_page = (uint8_t *)dmalloc((size_t)std::max<int64_t>(1, d->n_sel) * d->stride);  // tiled, cap rows
       d->sampled_cap = std::max<int64_t>(1, d->n_sel);
     }
-    std::vector<int32_t> hsel;
-    const int32_t *sel = d->d_sel_rows;
     if (d->all_selected) {
-      // identity selection: every page is copied whole
+      // f = 1: every page streams (H2D) and is re-laid out tiled on the device
       for_each_page(d, [&](const uint8_t *page, int64_t r0, int64_t nr) {
-        OOCGB_CK(cudaMemcpy2DAsync(d->d_sampled_page + r0 * 32, (size_t)d->sampled_cap * 32, page,
-                                   (size_t)d->rows_per_page * 32, (size_t)nr * 32, (size_t)d->n_fg,
-                                   cudaMemcpyDeviceToDevice, c->stream));
+        const int blocks = (int)std::min<int64_t>((nr + 7) / 8, (int64_t)c->num_sms * 16);
+        k_rows_to_tiled<<<blocks, 256, 0, c->stream>>>(page, d->stride, nullptr, r0, r0, r0 + nr,
+                                                       d->sampled_cap, d->d_sampled_page);
+        OOCGB_CK(cudaGetLastError());
       });
-    } else {
-      // per-page ranges of sel_rows (ascending) via host binary search over a D2H copy
-      hsel.resize((size_t)d->n_sel);
-      if (d->n_sel)
-        OOCGB_CK(cudaMemcpyAsync(hsel.data(), sel, sizeof(int32_t) * d->n_sel, cudaMemcpyDeviceToHost, c->stream));
-      OOCGB_CK(cudaStreamSynchronize(c->stream));
-      for_each_page(d, [&](const uint8_t *page, int64_t r0, int64_t nr) {
-        int64_t k0 = std::lower_bound(hsel.begin(), hsel.end(), (int32_t)r0) - hsel.begin();
-        int64_t k1 = std::lower_bound(hsel.begin(), hsel.end(), (int32_t)(r0 + nr)) - hsel.begin();
-        if (k1 > k0) {
-          int64_t tot = (k1 - k0) * d->n_fg * 2;
-          k_compact_page<<<grid_for(c, tot), 256, 0, c->stream>>>(page, r0, d->rows_per_page, d->n_fg, sel, k0, k1,
-                                                                    d->sampled_cap, d->d_sampled_page);
-          OOCGB_CK(cudaGetLastError());
-        }
-      });
+    } else if (d->n_sel > 0) {
+      // f < 1: gather only the selected rows, zero-copy from the pinned pages (NEXT #2: the link
+      // carries n_sel rows instead of a second full pass)
+      PhaseTimer link(c, 5);
+      const int blocks = (int)std::min<int64_t>((d->n_sel + 7) / 8, (int64_t)c->num_sms * 32);
+      k_rows_to_tiled<<<blocks, 256, 0, c->stream>>>(d->h_pages, d->stride, d->d_sel_rows, 0, 0, d->n_sel,
+                                                     d->sampled_cap, d->d_sampled_page);
+      OOCGB_CK(cudaGetLastError());
     }
   }
   d->has_sample = true;

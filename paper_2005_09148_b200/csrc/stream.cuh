@@ -1,7 +1,8 @@
 // Out-of-core page streamer ("streamed ... via a multi-threaded
 // pre-fetcher", here pinned host -> HBM over PCIe): pages of the ELLPACK matrix live in pinned
 // host memory; fn(page_device_ptr, first_row, n_rows) consumes them on the ctx stream while the
-// next pages are copied on the copy stream (one 2D copy per page: n_fg planes of nr rows) into a ring of kStages device staging buffers.
+// next pages are copied on the copy stream (one row-range copy per page) into a ring of
+// kStages device staging buffers.
 // Copy and compute are chained by events only — no host synchronisation inside the loop.
 #pragma once
 #include "internal.cuh"
@@ -39,10 +40,9 @@ void for_each_page(oocgb_data d, F fn) {
     OOCGB_CK(cudaStreamWaitEvent(c->copy_stream, consumed[slot], 0));
     cudaEvent_t ta = nullptr, tb = nullptr;
     if (c->profiling) { ta = pool_event(c); tb = pool_event(c); OOCGB_CK(cudaEventRecord(ta, c->copy_stream)); }
-    // page p = n_fg group planes of rpp * 32 bytes; copy the nr valid rows of every plane
-    OOCGB_CK(cudaMemcpy2DAsync(d->d_stage[slot], (size_t)rpp * 32, d->h_pages + (size_t)p * rpp * d->stride,
-                               (size_t)rpp * 32, (size_t)nr * 32, (size_t)d->n_fg, cudaMemcpyHostToDevice,
-                               c->copy_stream));
+    // pinned pages are row-major: page p is the contiguous row range [r0, r0 + nr)
+    OOCGB_CK(cudaMemcpyAsync(d->d_stage[slot], d->h_pages + (size_t)r0 * d->stride, (size_t)nr * d->stride,
+                             cudaMemcpyHostToDevice, c->copy_stream));
     if (c->profiling) { OOCGB_CK(cudaEventRecord(tb, c->copy_stream)); record_copy_timing(c, ta, tb); }
     OOCGB_CK(cudaEventRecord(copy_done[slot], c->copy_stream));
     OOCGB_CK(cudaStreamWaitEvent(c->stream, copy_done[slot], 0));

@@ -955,12 +955,15 @@ k_part_scatter(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__
 
 // ---------------------------------------------------------------------------------------------
 // Prediction (Eq. 1): margin[row] += leaf(tree, bins_row), binned traversal, per tree in order.
-__global__ void k_predict(const uint8_t *__restrict__ bins, size_t pitch, int64_t n,
+// Layout-generic addressing: symbol (row i, f) at bins + i * row_step + (f / 32) * pitch + f % 32
+// (tiled device page: row_step 32, pitch rpp * 32; row-major pinned page: row_step = stride,
+// pitch 32).
+__global__ void k_predict(const uint8_t *__restrict__ bins, size_t row_step, size_t pitch, int64_t n,
                           const PNode *const *__restrict__ trees, int n_trees, float *__restrict__ margin) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float mg = margin[i];
-    const uint8_t *row = bins + i * 32;  // row i of group plane 0 (plane g at + g * pitch)
+    const uint8_t *row = bins + i * row_step;
     for (int t = 0; t < n_trees; ++t) {
       const PNode *nd = trees[t];
       int v = 0;
@@ -1286,7 +1289,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   return t;
 }
 
-void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t rpp, int64_t n_rows, int64_t row_offset,
+void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t pitch, int64_t n_rows, int64_t row_offset,
                     const oocgb_tree *trees, int n_trees, float *d_margin) {
   oocgb_ctx c = d->ctx;
   if (n_rows <= 0 || n_trees <= 0) return;
@@ -1296,7 +1299,7 @@ void predict_device(oocgb_data d, const uint8_t *d_bins, int64_t rpp, int64_t n_
   OOCGB_REQUIRE(n_trees <= 4096, OOCGB_ERR_ARG, "predict: at most 4096 trees per call");
   OOCGB_CK(cudaMemcpyAsync(d_ptrs, ptrs.data(), sizeof(void *) * n_trees, cudaMemcpyHostToDevice, c->stream));
   int blocks = (int)std::min<int64_t>((n_rows + 255) / 256, (int64_t)c->num_sms * 16);
-  k_predict<<<blocks, 256, 0, c->stream>>>(d_bins, (size_t)rpp * 32, n_rows, d_ptrs, n_trees, d_margin + row_offset);
+  k_predict<<<blocks, 256, 0, c->stream>>>(d_bins, row_step, pitch, n_rows, d_ptrs, n_trees, d_margin + row_offset);
   OOCGB_CK(cudaGetLastError());
 }
 
