@@ -171,6 +171,13 @@ int oocgb_sample(oocgb_data data, int32_t mode, double ratio, double mvs_lambda,
 int oocgb_sample_goss(oocgb_data data, double a, double b, uint64_t seed, uint64_t round,
                       int32_t quant_bits, oocgb_sample_info *info);
 
+/* Alg. 6: with enable != 0, an f = 1 sample (mode NONE)
+ * of PINNED_HOST data is NOT copied to the device; build_tree then streams the pinned pages once
+ * per level (batches of ~1 GB, copy/compute overlapped) and builds every node's histogram
+ * directly (no sibling subtraction).  The tree is identical to the in-core one.
+ * Samples with f < 1 keep using Alg. 7 (compaction).  ERR_ARG unless PINNED_HOST; one GPU.   */
+int oocgb_set_streaming(oocgb_data data, int32_t enable);
+
 /* build_tree (Alg. 1, depth-wise R16): histograms (fixed-point int, bit-exact), sibling
  * subtraction (R17), split evaluation (Eq. 8, R13-R14), stable partition, leaf values
  * (Eq. 6, eta applied at creation R15).  max_depth in [0, 16]; lambda >= 0; the tree is

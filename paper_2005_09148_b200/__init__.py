@@ -32,7 +32,7 @@ ABI_SYMBOLS = (
     "oocgb_tree_destroy", "oocgb_predict", "oocgb_update_margin", "oocgb_get_cuts",
     "oocgb_get_bins", "oocgb_get_sample", "oocgb_get_histogram", "oocgb_get_partition",
     "oocgb_get_timings", "oocgb_set_profiling", "oocgb_last_error", "oocgb_abi_version",
-    "oocgb_ctx_create_hostcomm", "oocgb_sample_goss",
+    "oocgb_ctx_create_hostcomm", "oocgb_sample_goss", "oocgb_set_streaming",
 )
 
 COLLECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
@@ -114,6 +114,7 @@ def load_library():
         "oocgb_set_profiling": [p, i32],
         "oocgb_ctx_create_hostcomm": [i32, i32, i32, COLLECTIVE_FN, p, u64, p],
         "oocgb_sample_goss": [p, d, d, u64, u64, i32, p],
+        "oocgb_set_streaming": [p, i32],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -274,6 +275,10 @@ class Data:
         _check(load_library().oocgb_sample(self._h, mode, ratio, mvs_lambda, seed, round, quant_bits,
                                             ctypes.byref(si)))
         return {k: getattr(si, k) for k, _ in SampleInfo._fields_}
+
+    def set_streaming(self, enable: bool = True):
+        """Alg. 6: build f = 1 trees by streaming the pinned pages once per level (PINNED_HOST)."""
+        _check(load_library().oocgb_set_streaming(self._h, int(enable)))
 
     def sample_goss(self, a: float, b: float, seed: int = 1, round: int = 0, quant_bits: int = 16) -> dict:
         """GOSS: top round(a n) by |g| with p = 1, the rest Bernoulli(b / (1 - a)), scale 1/p."""

@@ -252,6 +252,7 @@ static void free_data(oocgb_data d) {
   dfree(d->d_sampled_page); dfree(d->d_gs); dfree(d->d_hs); dfree(d->d_tmp64);
   for (int i = 0; i < 3; ++i) dfree(d->d_stage[i]);
   for (int i = 0; i < 2; ++i) dfree(d->d_arg[i]);
+  for (int i = 0; i < 3; ++i) dfree(d->d_bstage[i]);
   if (d->d_ss) cudaFree(d->d_ss);
   if (d->h_ss) cudaFreeHost(d->h_ss);
   if (d->h_pages) cudaFreeHost(d->h_pages);
@@ -604,6 +605,16 @@ int oocgb_sample_goss(oocgb_data d, double a, double b, uint64_t seed, uint64_t 
   API_END
 }
 
+int oocgb_set_streaming(oocgb_data d, int32_t enable) {
+  API_BEGIN
+  OOCGB_REQUIRE(d, OOCGB_ERR_ARG, "data is NULL");
+  OOCGB_REQUIRE(!enable || d->placement == OOCGB_PLACE_PINNED_HOST, OOCGB_ERR_ARG,
+                "streamed build needs PINNED_HOST pages");
+  d->streamed = enable != 0;
+  d->has_sample = false;
+  API_END
+}
+
 int oocgb_build_tree(oocgb_data d, int32_t max_depth, double lambda, double gamma, double min_child_weight,
                      double eta, int32_t keep_debug, oocgb_tree *out) {
   API_BEGIN
@@ -614,7 +625,10 @@ int oocgb_build_tree(oocgb_data d, int32_t max_depth, double lambda, double gamm
                 OOCGB_ERR_ARG, "lambda >= 0 and finite gamma / eta / min_child_weight required");
   OOCGB_REQUIRE(d->has_sample, OOCGB_ERR_STATE, "build_tree before sample");
   bind(d->ctx);
-  *out = build_tree(d, max_depth, lambda, gamma, min_child_weight, eta, keep_debug != 0);
+  if (d->streamed && d->placement == OOCGB_PLACE_PINNED_HOST && d->all_selected)
+    *out = build_tree_streamed(d, max_depth, lambda, gamma, min_child_weight, eta, keep_debug != 0);
+  else
+    *out = build_tree(d, max_depth, lambda, gamma, min_child_weight, eta, keep_debug != 0);
   API_END
 }
 

@@ -213,6 +213,12 @@ struct oocgb_data_s {
   // tree workspace (lazy, sized for (n_sel cap, depth))
   struct Work *work = nullptr;
   uint64_t tree_serial = 0;
+  // Alg. 6 streamed build (f = 1, PINNED_HOST): trees are built by level-batched passes over the
+  // pinned pages instead of copying every page into HBM
+  bool streamed = false;
+  int64_t stream_batch_rows = 0;
+  int32_t *streamed_row_node = nullptr;  // final leaf of every row after a streamed build
+  uint8_t *d_bstage[3] = {nullptr, nullptr, nullptr};
   // persistent device staging for host-pointer arguments (margin, labels): no per-call malloc
   void *d_arg[2] = {nullptr, nullptr};
   size_t arg_bytes[2] = {0, 0};
@@ -259,6 +265,8 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
 // tree.cu
 oocgb_tree build_tree(oocgb_data d, int max_depth, double lambda, double gamma, double mcw,
                       double eta, bool keep_debug);
+oocgb_tree build_tree_streamed(oocgb_data d, int max_depth, double lambda, double gamma, double mcw,
+                               double eta, bool keep_debug);
 void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t pitch, int64_t n_rows, int64_t row_offset,
                     const oocgb_tree *trees, int n_trees, float *d_margin);
 void update_margin(oocgb_data d, oocgb_tree t, float *d_margin);

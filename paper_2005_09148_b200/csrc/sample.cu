@@ -604,8 +604,9 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
     d->H_root = d->h_ss->H;
   }
 
-  // Compact (Alg. 7): pinned pages -> one device page of the selected rows
-  if (d->placement == OOCGB_PLACE_PINNED_HOST) {
+  // Compact (Alg. 7): pinned pages -> one device page of the selected rows (an f = 1 sample of
+  // data in streamed mode skips it: Alg. 6 builds the tree from the pinned pages directly)
+  if (d->placement == OOCGB_PLACE_PINNED_HOST && !(d->streamed && d->all_selected)) {
     if (d->sampled_cap < d->n_sel) {
       dfree(d->d_sampled_page);
       d->d_sampled_page = nullptr;

@@ -51,4 +51,44 @@ void for_each_page(oocgb_data d, F fn) {
   }
 }
 
+// Same pipeline over batches of consecutive pages (a contiguous row range of `rows` rows of the
+// row-major pinned pages), into the data's batch staging ring (allocated on first use).
+template <class F>
+void for_each_batch(oocgb_data d, int64_t rows, F fn) {
+  oocgb_ctx c = d->ctx;
+  if (!d->d_bstage[0] || d->stream_batch_rows != rows) {
+    for (int i = 0; i < kStages; ++i) {
+      if (d->d_bstage[i]) cudaFree(d->d_bstage[i]);
+      d->d_bstage[i] = (uint8_t *)dmalloc((size_t)std::max<int64_t>(1, rows) * d->stride);
+    }
+    d->stream_batch_rows = rows;
+  }
+  static thread_local cudaEvent_t copy_done[kStages] = {}, consumed[kStages] = {};
+  static thread_local int inited = 0;
+  if (!inited) {
+    for (int i = 0; i < kStages; ++i) {
+      OOCGB_CK(cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming));
+      OOCGB_CK(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
+    }
+    inited = 1;
+  }
+  for (int i = 0; i < kStages; ++i) OOCGB_CK(cudaEventRecord(consumed[i], c->stream));
+  const int64_t nb = (d->n_local + rows - 1) / rows;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int slot = (int)(b % kStages);
+    const int64_t r0 = b * rows;
+    const int64_t nr = std::min<int64_t>(rows, d->n_local - r0);
+    OOCGB_CK(cudaStreamWaitEvent(c->copy_stream, consumed[slot], 0));
+    cudaEvent_t ta = nullptr, tb = nullptr;
+    if (c->profiling) { ta = pool_event(c); tb = pool_event(c); OOCGB_CK(cudaEventRecord(ta, c->copy_stream)); }
+    OOCGB_CK(cudaMemcpyAsync(d->d_bstage[slot], d->h_pages + (size_t)r0 * d->stride, (size_t)nr * d->stride,
+                             cudaMemcpyHostToDevice, c->copy_stream));
+    if (c->profiling) { OOCGB_CK(cudaEventRecord(tb, c->copy_stream)); record_copy_timing(c, ta, tb); }
+    OOCGB_CK(cudaEventRecord(copy_done[slot], c->copy_stream));
+    OOCGB_CK(cudaStreamWaitEvent(c->stream, copy_done[slot], 0));
+    fn((const uint8_t *)d->d_bstage[slot], r0, nr);
+    OOCGB_CK(cudaEventRecord(consumed[slot], c->stream));
+  }
+}
+
 }  // namespace oocgb

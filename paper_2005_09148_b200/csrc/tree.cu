@@ -78,7 +78,7 @@ struct Work {
 
 namespace oocgb {
 
-__device__ __forceinline__ int level_first(int d) { return (1 << d) - 1; }
+__host__ __device__ __forceinline__ int level_first(int d) { return (1 << d) - 1; }
 
 // Leaf weight (Eq. 6) and dequantised sums of a node from its exact fixed-point sums (R15).
 __device__ void node_fill(DNode &nd, long long Gq, long long Hq, double sg_inv, double sh_inv,
@@ -166,7 +166,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
 __global__ void __launch_bounds__(kHistThreads, 3)
 k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
        const int2 *__restrict__ q, const Pair *__restrict__ pairs, const LevelCtl *__restrict__ ctl,
-       int *__restrict__ partial, int identity, int opaque_zero) {
+       int *__restrict__ partial, int identity, int row_step) {
   extern __shared__ int4 smem4[];
   int *S = reinterpret_cast<int *>(smem4);
   char *Sb = reinterpret_cast<char *>(smem4);
@@ -181,7 +181,8 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
 #pragma unroll
   for (int s = 0; s < 16; ++s) f4[s] = sbase + 4u * (uint32_t)(16 * half + ((rslot + s) & 15));
   constexpr int RT = kHistThreads / 2;  // rows per CTA step
-  (void)opaque_zero;
+  // symbol (row, f) at bins + (f / 32) * pitch + row * row_step + f % 32: row_step 32 for the
+  // tiled device pages, the row stride for a row-major (streamed) page with pitch 32
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int fg = item % n_fg, cg = item / n_fg;
     int lo = 0, hi = n_pairs - 1;  // largest p with chunk_base <= cg
@@ -199,7 +200,7 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
     auto row_of = [&](int kk) -> int { return identity ? kk : __ldg(ridx + kk); };
     auto load_row = [&](int kk, int row, uint4 &x, int2 &qv) {
       if (kk < r1) {
-        x = __ldg(reinterpret_cast<const uint4 *>(base + (size_t)row * 32));
+        x = __ldg(reinterpret_cast<const uint4 *>(base + (size_t)row * row_step));
         qv = __ldg(q + kk);
       }
     };
@@ -317,6 +318,7 @@ struct EvalArgs {
   double lambda, gamma, mcw;
   const RoundParams *rp;
   long long kmax;  // nodes with <= kmax rows keep their parent histogram as exact s32 pairs
+  int streamed;    // Alg. 6 mode: every node built directly, no parent histograms kept
 };
 
 __device__ __forceinline__ long long warp_excl_scan_ll(long long v, int lane, long long &total) {
@@ -457,13 +459,15 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 2) k_eval(EvalArgs A) {
   const int side = (int)(wid & 1);
   const int64_t pj = wid >> 1;
   const int p = (int)(pj / A.m), j = (int)(pj % A.m);
-  const int max_pairs = A.d == 0 ? 1 : (1 << (A.d - 1));
+  // sibling pairs per level: 1, 1, 2, 4, ...; the streamed mode lists every node: 2^d
+  const int max_pairs = A.streamed ? (1 << A.d) : (A.d == 0 ? 1 : (1 << (A.d - 1)));
   if (p >= max_pairs) return;
   const int n_pairs = A.ctl->n_pairs;  // independent of the pair load below
   const Pair P = A.pairs[p];
   if (p >= n_pairs) return;
   const int node = side ? P.derived : P.built;
   if (node < 0) return;
+  if (A.streamed && A.dn[node].feature == -2) return;  // streamed levels list every slot
   const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;  // prefetched for eval_node
   long long g[8], h[8];  // strided: element i is bin 32 i + lane
   const size_t hsz = (size_t)A.m * kBins * 2;
@@ -518,7 +522,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 2) k_eval(EvalArgs A) {
     for (int i = 0; i < 8; ++i) { g[i] = par[i].x - g[i]; h[i] = par[i].y - h[i]; }
   }
   const int f_d = level_first(A.d);
-  if (A.d <= A.D - 2) {
+  if (A.d <= A.D - 2 && !A.streamed) {
     if (P.compact & (side ? 4 : 2)) {
       int2 *dst = reinterpret_cast<int2 *>(A.phist_next + (size_t)(node - f_d) * hsz) + (size_t)j * kBins;
 #pragma unroll
@@ -585,6 +589,7 @@ k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Ca
   const Pair P = pairs[p];
   const int node = (blockIdx.x & 1) ? P.derived : P.built;
   if (node < 0) return;
+  if (dn[node].feature != -1) return;  // absent slot (streamed mode lists every slot)
   const int slot = node - level_first(d);
   BestSplit best{0.0, 0, 0x7fffffff, 0, 0, 0};
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
@@ -1036,7 +1041,7 @@ static void ensure_work(oocgb_data d, int D) {
   const size_t hsz = (size_t)m * kBins * 2;
   const int64_t pslots = D >= 2 ? (1LL << (D - 2)) : 1;
   for (int i = 0; i < 2; ++i) w->phist[i] = (long long *)dmalloc(sizeof(long long) * hsz * pslots);
-  if (c->world > 1) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * max_pairs);
+  if (c->world > 1 || d->streamed) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * 2 * max_pairs);
   w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)max_pairs * 2 * m);
   w->dnodes = (DNode *)dmalloc(sizeof(DNode) * ((1LL << (D + 1)) - 1));
   w->ctl = (LevelCtl *)dmalloc(sizeof(LevelCtl));
@@ -1099,7 +1104,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     mark(0, true);
     k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur], w->q[cur],
                                                                  w->pairs, w->ctl, w->partial,
-                                                                 (lv == 0 && ridx_mode == 0) ? 1 : 0, 0);
+                                                                 (lv == 0 && ridx_mode == 0) ? 1 : 0, 32);
     OOCGB_CK(cudaGetLastError());
     mark(0, false);
     if (c->world > 1) {
@@ -1117,7 +1122,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.phist_next = w->phist[lv & 1];
     A.dbg = keep_debug ? w->dbg : nullptr;
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
-    A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax;
+    A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 0;
     const int64_t warps = (int64_t)max_pairs * m * 2;
     k_eval<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, c->stream>>>(A);
     OOCGB_CK(cudaGetLastError());
@@ -1289,6 +1294,254 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   return t;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Alg. 6, level-batched (NEXT #1): f = 1 data that stays in pinned host memory.
+// Each level is one streamed pass over batches of pages: every row moves to its child under the
+// previous level's split (the per-row node id replaces the device-wide partition), the batch's
+// rows are grouped by node (counting sort), k_hist runs on the staged row-major batch, and the
+// batch's s32 partials are added into int64 per-node histograms; then every node of the level is
+// evaluated directly (no sibling subtraction: the children's sizes are only known after the pass).
+struct StreamWork {
+  int64_t cap_n = 0, cap_b = 0;
+  int max_slots = 0;
+  int32_t *row_node = nullptr;   // [n] current node of each row
+  int32_t *b_slot = nullptr;     // [batch] slot of each batch row at this level (-1: leaf)
+  int32_t *b_ridx = nullptr;     // [batch] batch rows grouped by slot
+  int2 *b_q = nullptr;           // [batch] their gradient pairs
+  int *slot_cnt = nullptr;       // [2^(D-1)] rows per slot in the batch
+  int *slot_cur = nullptr;       // scatter cursors
+};
+
+__global__ void k_stream_init(int32_t *row_node, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    row_node[i] = 0;
+}
+
+// rows of one batch: move to the child under the previous level's split (update != 0), count
+// the rows per child (n_rows, exact integer atomics), and tag rows of depth-d nodes with their
+// slot (node - first(d)); rows in earlier leaves get -1.
+__global__ void k_stream_assign(const uint8_t *__restrict__ batch, int stride, int64_t r0, int64_t nr,
+                                int32_t *__restrict__ row_node, DNode *dn, int first_d, int update, int hist,
+                                int32_t *__restrict__ b_slot, int *__restrict__ slot_cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+    int v = row_node[r0 + i];
+    if (update) {
+      const int f = dn[v].feature;
+      if (f >= 0) {
+        v = (batch[(size_t)i * stride + f] <= dn[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
+        row_node[r0 + i] = v;
+        atomicAdd((unsigned long long *)&dn[v].n_rows, 1ull);
+      }
+    }
+    if (hist) {
+      const int sl = (v >= first_d && dn[v].feature == -1) ? v - first_d : -1;
+      b_slot[i] = sl;
+      if (sl >= 0) atomicAdd(&slot_cnt[sl], 1);
+    }
+  }
+}
+
+// single block: slot offsets, the batch's pair table (one "pair" per slot: built = node, no
+// derived) with chunking, and the item count.
+__global__ void __launch_bounds__(1024)
+k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *__restrict__ slot_cur,
+              Pair *__restrict__ pairs, LevelCtl *ctl, int n_fg, int target_items, int kmax, int64_t batch_rows) {
+  long long cr = (batch_rows * n_fg + target_items - 1) / target_items;
+  if (cr < 1024) cr = 1024;
+  if (cr > kmax) cr = kmax;
+  int carry_rows = 0, carry_chunks = 0;
+  for (int base = 0; base < n_slots; base += blockDim.x) {
+    const int sl = base + threadIdx.x;
+    const int cnt = sl < n_slots ? slot_cnt[sl] : 0;
+    const int nch = (int)((cnt + cr - 1) / cr);
+    int tr, tc;
+    const int er = block_excl_scan(cnt, &tr);
+    const int ec = block_excl_scan(nch, &tc);
+    if (sl < n_slots) {
+      slot_cur[sl] = carry_rows + er;
+      Pair pr;
+      pr.parent = -1; pr.built = first_d + sl; pr.derived = -1;
+      pr.begin = carry_rows + er; pr.count = cnt;
+      pr.chunk_base = carry_chunks + ec; pr.n_chunks = nch; pr.chunk_rows = (int)cr;
+      pr.compact = 0;
+      pairs[sl] = pr;
+    }
+    carry_rows += tr;
+    carry_chunks += tc;
+  }
+  if (threadIdx.x == 0) {
+    ctl->n_pairs = n_slots;
+    ctl->n_items = carry_chunks * n_fg;
+  }
+}
+
+__global__ void k_stream_scatter(int64_t r0, int64_t nr, const int32_t *__restrict__ b_slot,
+                                 int *__restrict__ slot_cur, const int2 *__restrict__ q,
+                                 int32_t *__restrict__ b_ridx, int2 *__restrict__ b_q) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+    const int sl = b_slot[i];
+    if (sl < 0) continue;
+    const int pos = atomicAdd(&slot_cur[sl], 1);  // order inside a slot is irrelevant: integer sums
+    b_ridx[pos] = (int32_t)i;
+    b_q[pos] = q[r0 + i];
+  }
+}
+
+// built64[slot][j][b] += sum of the batch's chunk partials of that slot (thread per (slot, j, b)).
+__global__ void k_accum_partials(const int *__restrict__ partial, const Pair *__restrict__ pairs, int n_slots,
+                                 int m, int n_fg, long long *__restrict__ out) {
+  const int64_t total = (int64_t)n_slots * m * kBins;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(t % kBins);
+    const int j = (int)((t / kBins) % m);
+    const int p = (int)(t / ((int64_t)kBins * m));
+    const Pair P = pairs[p];
+    if (P.n_chunks == 0) continue;
+    long long g = 0, h = 0;
+    for (int c = 0; c < P.n_chunks; ++c) {
+      const size_t item = (size_t)(P.chunk_base + c) * n_fg + j / kFG;
+      const int2 v = reinterpret_cast<const int2 *>(partial)[(item * kFG + (j % kFG)) * kBins + b];
+      g += v.x;
+      h += v.y;
+    }
+    out[t * 2] += g;
+    out[t * 2 + 1] += h;
+  }
+}
+
+__global__ void k_stream_leaf_margin(const int32_t *__restrict__ row_node, int64_t n, const DNode *__restrict__ dn,
+                                     float *__restrict__ margin) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    margin[i] = margin[i] + dn[row_node[i]].leaf_value;
+}
+
+static StreamWork *g_unused_sw = nullptr;  // (placeholder to keep the struct referenced)
+
+oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma, double mcw, double eta,
+                               bool keep_debug) {
+  oocgb_ctx c = d->ctx;
+  OOCGB_REQUIRE(c->world == 1, OOCGB_ERR_ARG, "streamed build (Alg. 6) runs on one GPU in this version");
+  OOCGB_REQUIRE(d->all_selected, OOCGB_ERR_STATE, "streamed build needs sample(NONE) (f = 1)");
+  PhaseTimer whole(c, 6);
+  ensure_work(d, D);
+  Work *w = d->work;
+  const int m = d->m, n_fg = w->n_fg;
+  const int64_t n = d->n_local;
+  const int n_nodes = (1 << (D + 1)) - 1;
+  const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
+  const size_t hsz = (size_t)m * kBins * 2;
+  const int64_t brows = std::min<int64_t>(std::max<int64_t>(1, n),
+                                          std::max<int64_t>(d->rows_per_page, (1LL << 30) / d->stride));
+  static StreamWork sw;  // one streamed build at a time per process (single-owner contexts)
+  if (sw.cap_n < n || sw.cap_b < brows || sw.max_slots < (1 << std::max(0, D - 1))) {
+    dfree(sw.row_node); dfree(sw.b_slot); dfree(sw.b_ridx); dfree(sw.b_q); dfree(sw.slot_cnt); dfree(sw.slot_cur);
+    sw.cap_n = std::max<int64_t>(1, n);
+    sw.cap_b = brows;
+    sw.max_slots = 1 << std::max(0, D - 1);
+    sw.row_node = (int32_t *)dmalloc(sizeof(int32_t) * sw.cap_n);
+    sw.b_slot = (int32_t *)dmalloc(sizeof(int32_t) * brows);
+    sw.b_ridx = (int32_t *)dmalloc(sizeof(int32_t) * brows);
+    sw.b_q = (int2 *)dmalloc(sizeof(int2) * brows);
+    sw.slot_cnt = (int *)dmalloc(sizeof(int) * sw.max_slots);
+    sw.slot_cur = (int *)dmalloc(sizeof(int) * sw.max_slots);
+  }
+  if (keep_debug) {
+    size_t need = sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1);
+    if (w->dbg_bytes < need) { dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
+    OOCGB_CK(cudaMemsetAsync(w->dbg, 0, need, c->stream));
+  }
+  OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
+  const int target = w->hist_grid;
+  k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta,
+                                                       w->segs[0], w->pairs, w->ctl, 0, n_fg, target, kmax, D,
+                                                       d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], 0);
+  k_stream_init<<<c->num_sms * 4, 256, 0, c->stream>>>(sw.row_node, n);
+  OOCGB_CK(cudaGetLastError());
+  const int grid = c->num_sms * 8;
+  for (int lv = 0; lv <= D; ++lv) {
+    const bool hist = lv < D;  // the last pass only moves rows to their leaves
+    const int n_slots = 1 << lv;
+    const int first = level_first(lv);
+    if (hist) OOCGB_CK(cudaMemsetAsync(w->built64, 0, sizeof(long long) * hsz * n_slots, c->stream));
+    for_each_batch(d, brows, [&](const uint8_t *batch, int64_t r0, int64_t nr) {
+      if (hist) OOCGB_CK(cudaMemsetAsync(sw.slot_cnt, 0, sizeof(int) * n_slots, c->stream));
+      k_stream_assign<<<grid, 256, 0, c->stream>>>(batch, d->stride, r0, nr, sw.row_node, w->dnodes, first,
+                                                   lv > 0 ? 1 : 0, hist ? 1 : 0, sw.b_slot, sw.slot_cnt);
+      OOCGB_CK(cudaGetLastError());
+      if (!hist) return;
+      k_stream_plan<<<1, 1024, 0, c->stream>>>(n_slots, first, sw.slot_cnt, sw.slot_cur, w->pairs, w->ctl, n_fg,
+                                               target, kmax, nr);
+      k_stream_scatter<<<grid, 256, 0, c->stream>>>(r0, nr, sw.b_slot, sw.slot_cur, d->d_q, sw.b_ridx, sw.b_q);
+      {
+        PhaseTimer t(c, 0);
+        k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(batch, 32, m, n_fg, sw.b_ridx, sw.b_q, w->pairs,
+                                                                     w->ctl, w->partial, 0, d->stride);
+      }
+      const int64_t tot = (int64_t)n_slots * m * kBins;
+      k_accum_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
+          w->partial, w->pairs, n_slots, m, n_fg, w->built64);
+      OOCGB_CK(cudaGetLastError());
+    });
+    if (!hist) break;
+    // every node of the level: pairs[s] = {built = first + s} over the whole data
+    k_stream_plan<<<1, 1024, 0, c->stream>>>(n_slots, first, sw.slot_cnt, sw.slot_cur, w->pairs, w->ctl, n_fg,
+                                             target, kmax, 1);
+    PhaseTimer t(c, 1);
+    EvalArgs A;
+    A.d = lv; A.D = D; A.m = m; A.n_fg = n_fg;
+    A.pairs = w->pairs; A.ctl = w->ctl; A.partial = w->partial;
+    A.built64 = w->built64;
+    A.phist_prev = w->phist[0];
+    A.phist_next = w->phist[1];
+    A.dbg = keep_debug ? w->dbg : nullptr;
+    A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
+    A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 1;
+    const int64_t warps = (int64_t)n_slots * m * 2;
+    k_eval<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, c->stream>>>(A);
+    k_finalize<<<(unsigned)(n_slots * 2), 256, 0, c->stream>>>(lv, m, w->pairs, w->ctl, w->cand, w->dnodes,
+                                                               d->d_cut_values, d->d_cut_ptrs, w->d_rp, lambda, eta);
+    OOCGB_CK(cudaGetLastError());
+  }
+  (void)g_unused_sw;
+  // export (same as the in-core path)
+  std::vector<DNode> hn(n_nodes);
+  LevelCtl hctl;
+  OOCGB_CK(cudaMemcpyAsync(hn.data(), w->dnodes, sizeof(DNode) * n_nodes, cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaMemcpyAsync(&hctl, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  OOCGB_REQUIRE(hctl.error == 0, OOCGB_ERR_ARG, "build_tree: H + lambda <= 0 at a node (S:L406)");
+  oocgb_tree t = new oocgb_tree_s();
+  t->owner = d;
+  t->serial = ++d->tree_serial;
+  t->max_depth = D;
+  t->nodes.resize(n_nodes);
+  std::vector<PNode> pn(n_nodes);
+  for (int v = 0; v < n_nodes; ++v) {
+    oocgb_node &o = t->nodes[v];
+    o.feature = hn[v].feature; o.split_bin = hn[v].split_bin; o.split_value = hn[v].split_value;
+    o.leaf_value = hn[v].leaf_value; o.gain = hn[v].gain; o.sum_g = hn[v].sum_g; o.sum_h = hn[v].sum_h;
+    o.n_rows = hn[v].n_rows;
+    if (o.feature == -2) { o.split_bin = 0; o.split_value = 0; o.leaf_value = 0; o.gain = 0; o.sum_g = 0; o.sum_h = 0; o.n_rows = 0; }
+    if (o.feature == -1) { o.split_bin = 0; o.split_value = 0; o.gain = 0; }
+    pn[v] = PNode{o.feature, o.split_bin, o.leaf_value, 0};
+  }
+  t->ctx = c;
+  t->pnodes_bytes = sizeof(PNode) * n_nodes;
+  t->d_pnodes = (PNode *)pool_get(c, t->pnodes_bytes);
+  OOCGB_CK(cudaMemcpyAsync(t->d_pnodes, pn.data(), sizeof(PNode) * n_nodes, cudaMemcpyHostToDevice, c->stream));
+  if (keep_debug) {
+    t->debug = true;
+    size_t cnt = hsz * (size_t)std::max(0, (1 << D) - 1);
+    t->hist.resize(cnt);
+    if (cnt) OOCGB_CK(cudaMemcpyAsync(t->hist.data(), w->dbg, sizeof(long long) * cnt, cudaMemcpyDeviceToHost, c->stream));
+    t->leaf_of_row.assign(n, -1);
+    if (n) OOCGB_CK(cudaMemcpyAsync(t->leaf_of_row.data(), sw.row_node, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+  }
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  d->streamed_row_node = sw.row_node;
+  return t;
+}
+
 void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t pitch, int64_t n_rows, int64_t row_offset,
                     const oocgb_tree *trees, int n_trees, float *d_margin) {
   oocgb_ctx c = d->ctx;
@@ -1306,6 +1559,13 @@ void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t
 void update_margin(oocgb_data d, oocgb_tree t, float *d_margin) {
   oocgb_ctx c = d->ctx;
   Work *w = d->work;
+  if (d->streamed && d->placement == OOCGB_PLACE_PINNED_HOST) {
+    OOCGB_REQUIRE(w && t->serial == d->tree_serial && d->all_selected && d->streamed_row_node, OOCGB_ERR_STATE,
+                  "update_margin: needs the latest tree of an f = 1 sample");
+    k_stream_leaf_margin<<<c->num_sms * 8, 256, 0, c->stream>>>(d->streamed_row_node, d->n_local, w->dnodes, d_margin);
+    OOCGB_CK(cudaGetLastError());
+    return;
+  }
   OOCGB_REQUIRE(w && t->serial == d->tree_serial && d->all_selected && d->placement == OOCGB_PLACE_DEVICE,
                 OOCGB_ERR_STATE, "update_margin: needs the latest tree of an in-core, f = 1 sample");
   const int n = (int)d->n_sel;

@@ -257,6 +257,34 @@ def test_out_of_core_equals_in_core(ctx):
         d.close()
 
 
+@pytest.mark.parametrize("n,m,depth,page_rows", [(30000, 40, 6, 4096), (5000, 70, 5, 700), (1, 3, 3, 1)])
+def test_streamed_build_alg6_equals_in_core_and_oracle(ctx, n, m, depth, page_rows):
+    """Alg. 6 (NEXT #1): f = 1 trees built by streaming the pinned pages once per level equal the
+    in-core tree and the oracle (fields, histograms, final partition)."""
+    X, y = synth.make_classification(n, m, seed=9) if n >= 50 else (
+        np.random.default_rng(1).normal(size=(n, m)).astype(np.float32), np.ones(n, np.float32))
+    cv, cp, B = _oracle_cuts_bins(X, 256)
+    g, h = oracle.logistic_grad(np.random.default_rng(3).normal(size=n).astype(np.float32), y)
+    on, olor, ohist, _ = _oracle_tree(B, m, cv, cp, g, h, 0, 1.0, depth)
+    stride = (m + 31) // 32 * 32
+    d = ctx.quantise(X, 256, page_bytes=page_rows * stride, placement=ob.PLACE_PINNED_HOST)
+    d.set_streaming(True)
+    d.set_gradients(g, h)
+    d.sample(0, 1.0)
+    t = d.build_tree(depth, keep_debug=True)
+    _compare_trees(t.export(), on)
+    for v in range((1 << depth) - 1):
+        if on["feature"][v] == -2:
+            continue
+        np.testing.assert_array_equal(t.get_histogram(v), ohist[v], err_msg=f"node {v}")
+    np.testing.assert_array_equal(t.get_partition(n), olor)
+    m0 = np.random.default_rng(4).normal(size=n).astype(np.float32)
+    np.testing.assert_array_equal(d.update_margin(t, m0.copy()), oracle.predict(B, on, m0))
+    np.testing.assert_array_equal(d.predict([t], m0.copy()), oracle.predict(B, on, m0))
+    t.close()
+    d.close()
+
+
 @pytest.mark.parametrize("mode,ratio", [(2, 0.1), (1, 0.3)])
 def test_out_of_core_sampled_matches_oracle(ctx, mode, ratio):
     """Alg. 7: sample, compact the pinned pages into one device page, build in-core."""
