@@ -50,6 +50,8 @@ def parse():
                     help="2: 1M x 500 in-core f=1 (the driver's bench); 3: 20M x 500 out-of-core, "
                          "32 MiB pinned pages, MVS f=0.1")
     ap.add_argument("--rows3", type=int, default=20_000_000, help="config 3 rows")
+    ap.add_argument("--stream-f1", action="store_true",
+                    help="config 3 without sampling: Alg. 6 streamed build (one page pass per level)")
     ap.add_argument("--rows4", type=int, default=100_000_000, help="config 4 training rows")
     ap.add_argument("--rounds4", type=int, default=50, help="config 4 boosting rounds per setting")
     return ap.parse_args()
@@ -250,6 +252,8 @@ def run_config3(args, rank, world, local):
     torch.cuda.synchronize()
     prep_s = time.perf_counter() - t0
     info = d.info()
+    if args.stream_f1:
+        d.set_streaming(True)
     margin = torch.zeros(n, dtype=torch.float32, device="cuda")
     tree = None
     sel = []
@@ -259,7 +263,10 @@ def run_config3(args, rank, world, local):
             d.predict([prev], margin)     # streams all pages
             prev.close()
         d.set_logistic_gradients(margin, labels)
-        si = d.sample(ob.SAMPLE_MVS, 0.1, 1.0, seed=1, round=r, quant_bits=QBITS)  # + Compact
+        if args.stream_f1:
+            si = d.sample(ob.SAMPLE_NONE, 1.0, round=r, quant_bits=QBITS)
+        else:
+            si = d.sample(ob.SAMPLE_MVS, 0.1, 1.0, seed=1, round=r, quant_bits=QBITS)  # + Compact
         sel.append(si["n_selected_global"])
         return d.build_tree(DEPTH, LAMBDA, GAMMA, MCW, ETA)
 
@@ -282,17 +289,23 @@ def run_config3(args, rank, world, local):
     ms = e0.elapsed_time(e1) / args.steps
     tm = ctx.get_timings()
     page_bytes_per_pass = n * info["row_stride"]
-    # predict streams every page; Compact gathers only the selected rows (zero-copy, NEXT #2)
-    copied = page_bytes_per_pass + int(statistics.mean(sel[-args.steps:])) * info["row_stride"]
+    # predict streams every page; Compact gathers only the selected rows (zero-copy, NEXT #2);
+    # the Alg. 6 streamed build makes one more full pass per level plus the final leaf pass
+    if args.stream_f1:
+        copied = page_bytes_per_pass * (1 + DEPTH + 1)
+    else:
+        copied = page_bytes_per_pass + int(statistics.mean(sel[-args.steps:])) * info["row_stride"]
     h2d_ms = tm["h2d_ms"] / args.steps
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8 symbols, int32/int64 fixed-point sums, f64 gains",
         "data": "synthetic (make_classification-style, generated on the GPU per chunk, seeded)",
-        "config": {"workload": "config 3: 20M x 500 out-of-core, 32 MiB pinned-host ELLPACK pages, MVS f=0.1, depth 8",
+        "config": {"workload": ("config 3 variant: 20M x 500 out-of-core, 32 MiB pinned-host pages, f=1, Alg. 6 "
+                                "streamed build (one page pass per level)") if args.stream_f1 else
+                               "config 3: 20M x 500 out-of-core, 32 MiB pinned-host ELLPACK pages, MVS f=0.1, depth 8",
                    "rows": n, "n_features": m, "n_pages": info["n_pages"], "rows_per_page": info["rows_per_page"],
-                   "max_depth": DEPTH, "sample": "MVS", "ratio": 0.1},
+                   "max_depth": DEPTH, "sample": "none" if args.stream_f1 else "MVS", "ratio": 1.0 if args.stream_f1 else 0.1},
         "link": {"bytes_per_round": copied, "h2d_ms_per_round": h2d_ms,
                  "gbps_while_copying": copied / (h2d_ms * 1e-3) / 1e9 if h2d_ms > 0 else None,
                  "busy_frac": h2d_ms / ms, "effective_gbps": copied / (ms * 1e-3) / 1e9},

@@ -46,6 +46,18 @@ struct GraphKey {
   }
 };
 
+// buffers of the Alg. 6 streamed build (build_tree_streamed), owned by the data's Work
+struct StreamWork {
+  int64_t cap_n = 0, cap_b = 0;
+  int max_slots = 0;
+  int32_t *row_node = nullptr;   // [n] current node of each row
+  int32_t *b_slot = nullptr;     // [batch] slot of each batch row at this level (-1: leaf)
+  int32_t *b_ridx = nullptr;     // [batch] batch rows grouped by slot
+  int2 *b_q = nullptr;           // [batch] their gradient pairs
+  int *slot_cnt = nullptr;       // [2^(D-1)] rows per slot in the batch
+  int *slot_cur = nullptr;       // scatter cursors
+};
+
 struct Work {
   int64_t cap_rows = 0;
   int max_depth = -1, m = 0, n_fg = 0;
@@ -74,6 +86,7 @@ struct Work {
   cudaGraphExec_t graph = nullptr; // captured level loop of the last key
   GraphKey key{};
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> graph_events;  // profiling
+  StreamWork sw;                   // streamed build only
 };
 
 namespace oocgb {
@@ -1059,6 +1072,9 @@ void free_work(oocgb_data d) {
   dfree(w->flagbits); dfree(w->tile_cnt); dfree(w->tile_off); dfree(w->bpart); dfree(w->seg_nr);
   dfree(w->seg_grb); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
   dfree(w->cand); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg); dfree(w->d_rp);
+  dfree(w->sw.row_node); dfree(w->sw.b_slot); dfree(w->sw.b_ridx); dfree(w->sw.b_q); dfree(w->sw.slot_cnt);
+  dfree(w->sw.slot_cur);
+  d->streamed_row_node = nullptr;
   if (w->h_rp) cudaFreeHost(w->h_rp);
   drop_graph(w);
   delete w;
@@ -1301,17 +1317,6 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
 // rows are grouped by node (counting sort), k_hist runs on the staged row-major batch, and the
 // batch's s32 partials are added into int64 per-node histograms; then every node of the level is
 // evaluated directly (no sibling subtraction: the children's sizes are only known after the pass).
-struct StreamWork {
-  int64_t cap_n = 0, cap_b = 0;
-  int max_slots = 0;
-  int32_t *row_node = nullptr;   // [n] current node of each row
-  int32_t *b_slot = nullptr;     // [batch] slot of each batch row at this level (-1: leaf)
-  int32_t *b_ridx = nullptr;     // [batch] batch rows grouped by slot
-  int2 *b_q = nullptr;           // [batch] their gradient pairs
-  int *slot_cnt = nullptr;       // [2^(D-1)] rows per slot in the batch
-  int *slot_cur = nullptr;       // scatter cursors
-};
-
 __global__ void k_stream_init(int32_t *row_node, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     row_node[i] = 0;
@@ -1415,8 +1420,6 @@ __global__ void k_stream_leaf_margin(const int32_t *__restrict__ row_node, int64
     margin[i] = margin[i] + dn[row_node[i]].leaf_value;
 }
 
-static StreamWork *g_unused_sw = nullptr;  // (placeholder to keep the struct referenced)
-
 oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma, double mcw, double eta,
                                bool keep_debug) {
   oocgb_ctx c = d->ctx;
@@ -1432,7 +1435,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   const size_t hsz = (size_t)m * kBins * 2;
   const int64_t brows = std::min<int64_t>(std::max<int64_t>(1, n),
                                           std::max<int64_t>(d->rows_per_page, (1LL << 30) / d->stride));
-  static StreamWork sw;  // one streamed build at a time per process (single-owner contexts)
+  StreamWork &sw = w->sw;
   if (sw.cap_n < n || sw.cap_b < brows || sw.max_slots < (1 << std::max(0, D - 1))) {
     dfree(sw.row_node); dfree(sw.b_slot); dfree(sw.b_ridx); dfree(sw.b_q); dfree(sw.slot_cnt); dfree(sw.slot_cur);
     sw.cap_n = std::max<int64_t>(1, n);
@@ -1502,7 +1505,6 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
                                                                d->d_cut_values, d->d_cut_ptrs, w->d_rp, lambda, eta);
     OOCGB_CK(cudaGetLastError());
   }
-  (void)g_unused_sw;
   // export (same as the in-core path)
   std::vector<DNode> hn(n_nodes);
   LevelCtl hctl;
