@@ -122,7 +122,8 @@ struct LevelCtl {       // device-resident control block of one build
   int n_segs;
   int n_splits;         // splits decided at the current level
   int error;            // 1: H + lambda <= 0 at a node
-  int pad[3];
+  int part_done;        // partition tiles finished (last-block ticket), reset by the last block
+  int pad[2];
 };
 
 // byte offset of symbol (row, f) in a tiled ELLPACK buffer of pages of rpp rows

@@ -3,9 +3,11 @@
 //                 [multi-GPU: k_reduce_partials + ncclAllReduce(int64), P:L188-190]
 //                 k_eval  (EvaluateSplit, L176-178; Eq. 8) -> per-(node, feature) best split,
 //                          sibling = parent - built (R17), parents kept for the next level
-//                 k_finalize (argmax over features, Eq. 6 leaf values, R13-R15)
-//                 k_part_flags / k_part_plan / k_part_scatter (RepartitionInstances, L172-173):
-//                          stable partition by one global scan; gradient pairs travel with rows
+//                 k_finalize (node decision: argmax over features,
+//                          Eq. 6 leaf values, R13-R15)
+//                 k_part_fused / k_part_plan (RepartitionInstances, L172-173):
+//                          one pass: per-(tile, node) atomic reservations, left rows forward,
+//                          right rows backward; gradient pairs travel with rows
 // Everything stays on the device: one host sync per tree (the export).
 //
 // Histogram kernel design (measured in tools/microbench):
@@ -64,11 +66,9 @@ struct Work {
   int64_t items_cap = 0;
   int32_t *ridx[2] = {nullptr, nullptr};
   int2 *q[2] = {nullptr, nullptr};
-  uint32_t *flagbits = nullptr;
-  int *tile_cnt = nullptr;
-  int *tile_off = nullptr;
   oocgb::Seg *segs[2] = {nullptr, nullptr};
-  int *bpart = nullptr, *seg_nr = nullptr, *seg_grb = nullptr;
+  int *seg_cur[2] = {nullptr, nullptr};  // per-segment (left, right) cursors, ping-pong by level
+  int *tile_seg = nullptr;               // partition tile -> first segment
   long long *seg_cnt = nullptr;
   oocgb::Pair *pairs = nullptr;
   int *partial = nullptr;
@@ -319,7 +319,7 @@ __global__ void k_reduce_partials(const int *__restrict__ partial, const Pair *_
 struct EvalArgs {
   int d, D, m, n_fg;
   const Pair *pairs;
-  const LevelCtl *ctl;
+  LevelCtl *ctl;
   const int *partial;
   const long long *built64;   // non-null: multi-GPU all-reduced built histograms
   const long long *phist_prev;
@@ -332,7 +332,20 @@ struct EvalArgs {
   const RoundParams *rp;
   long long kmax;  // nodes with <= kmax rows keep their parent histogram as exact s32 pairs
   int streamed;    // Alg. 6 mode: every node built directly, no parent histograms kept
+  const float *cut_values;
+  double eta;
 };
+
+__device__ __forceinline__ int warp_excl_scan_i(int v, int lane, int &total) {
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  total = __shfl_sync(0xffffffffu, incl, 31);
+  return incl - v;
+}
 
 __device__ __forceinline__ long long warp_excl_scan_ll(long long v, int lane, long long &total) {
   long long incl = v;
@@ -363,15 +376,27 @@ __device__ __forceinline__ double gain_exact(long long GL, long long HL, long lo
 // 3) exact double gains only for candidates with gain_f + tol >= L.  The exact argmax and all
 //    its exact ties always pass (gain_f + tol >= gain >= gain(c') >= gain_f(c') - tol(c')), so
 //    the result is identical to evaluating every candidate in double.
-__device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const long long (&g)[8],
-                          const long long (&h)[8], const RoundParams &rp, const long long G, const long long H) {
+// I = int for nodes with <= kmax rows (every partial sum is then exact in int32), else long long.
+// Returns the lane that owns the winning bin (it wrote the candidate), or 0.
+template <typename I>
+__device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (&g)[8], const I (&h)[8],
+                         const RoundParams &rp, const long long G_, const long long H_) {
   const int B = A.cut_ptrs[j + 1] - A.cut_ptrs[j];
-  long long lg = 0, lh = 0;
+  const I G = (I)G_, H = (I)H_;
+  I lg = 0, lh = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) { lg += g[i]; lh += h[i]; }
-  long long tg, th;
-  const long long eg = warp_excl_scan_ll(lg, lane, tg);
-  const long long eh = warp_excl_scan_ll(lh, lane, th);
+  I tg, th, eg, eh;
+  if constexpr (sizeof(I) == 4) {
+    eg = warp_excl_scan_i(lg, lane, tg);
+    eh = warp_excl_scan_i(lh, lane, th);
+  } else {
+    eg = warp_excl_scan_ll(lg, lane, tg);
+    eh = warp_excl_scan_ll(lh, lane, th);
+  }
+  // integer validity threshold in the node's width (|HL| <= H < 2^31 when I = int)
+  const I hmin = (sizeof(I) == 4) ? (I)(rp.h_min > INT_MAX ? INT_MAX : (rp.h_min < INT_MIN ? INT_MIN : rp.h_min))
+                                  : (I)rp.h_min;
   const float lamf = (float)A.lambda;
   const float gPf = (float)G * rp.sg_inv_f, hPf = (float)H * rp.sh_inv_f;
   const float tPf = __fdividef(gPf * gPf, hPf + lamf);
@@ -379,7 +404,7 @@ __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const lo
   // pass 1: float gains + bounds
   float gf[8], tf[8];
   unsigned vmask = 0;
-  long long GL = eg, HL = eh;
+  I GL = eg, HL = eh;
   float Lmax = -INFINITY;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -387,7 +412,7 @@ __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const lo
     HL += h[i];
     const int b = lane * 8 + i;
     // an empty bin repeats the previous candidate exactly, which wins the tie (lower bin)
-    const bool v = b <= B - 2 && (g[i] != 0 || h[i] != 0 || b == 0) && HL >= rp.h_min && (H - HL) >= rp.h_min;
+    const bool v = b <= B - 2 && (g[i] != 0 || h[i] != 0 || b == 0) && HL >= hmin && (H - HL) >= hmin;
     gf[i] = -INFINITY;
     tf[i] = 0.f;
     if (v) {
@@ -426,7 +451,7 @@ __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const lo
     HL += h[i];
     if (((vmask >> i) & 1u) && gf[i] + tf[i] >= Lmax) {
       const double gain = gain_exact(GL, HL, G, H, tP, rp.sg_inv, rp.sh_inv, A.lambda, A.gamma);
-      if (!have || gain > best) { have = 1; best = gain; bbin = lane * 8 + i; bGL = GL; bHL = HL; }
+      if (!have || gain > best) { have = 1; best = gain; bbin = lane * 8 + i; bGL = (long long)GL; bHL = (long long)HL; }
     }
   }
   // warp argmax over (gain, bin): larger gain, then lower bin; invalid = -inf.  Only the pair is
@@ -451,6 +476,7 @@ __device__ void eval_node(const EvalArgs &A, int node, int j, int lane, const lo
     cd.HL = any ? bHL : 0;
     A.cand[(size_t)slot * A.m + j] = cd;
   }
+  return owner;
 }
 
 __device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)[8], const long long (&h)[8]) {
@@ -482,6 +508,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 2) k_eval(EvalArgs A) {
   if (node < 0) return;
   if (A.streamed && A.dn[node].feature == -2) return;  // streamed levels list every slot
   const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;  // prefetched for eval_node
+  const long long nodeRows = A.dn[node].n_rows;
   long long g[8], h[8];  // strided: element i is bin 32 i + lane
   const size_t hsz = (size_t)A.m * kBins * 2;
   longlong2 par[8];
@@ -568,7 +595,14 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 2) k_eval(EvalArgs A) {
     h[i] = v.y;
   }
   const RoundParams rp = *A.rp;
-  eval_node(A, node, j, lane, g, h, rp, nodeG, nodeH);
+  if (nodeRows <= A.kmax) {  // every partial sum of the node is exact in int32
+    int g32[8], h32[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { g32[i] = (int)g[i]; h32[i] = (int)h[i]; }
+    eval_node<int>(A, node, j, lane, g32, h32, rp, nodeG, nodeH);
+  } else {
+    eval_node<long long>(A, node, j, lane, g, h, rp, nodeG, nodeH);
+  }
 }
 
 // Split decision per node at depth d: argmax over features (ties: lowest feature, R13),
@@ -640,11 +674,23 @@ k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Ca
   }
 }
 
+static void launch_eval(const EvalArgs &A, int max_pairs, cudaStream_t st) {
+  const int64_t warps = (int64_t)max_pairs * A.m * 2;
+  k_eval<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, st>>>(A);
+  k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, st>>>(A.d, A.m, A.pairs, A.ctl, A.cand, A.dn, A.cut_values,
+                                                         A.cut_ptrs, A.rp, A.lambda, A.eta);
+  OOCGB_CK(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------------------------------------
-// RepartitionInstances: stable partition of every split segment, by one global scan of the
-// "goes right" flags (bin > split_bin).  For position i in segment s:
-//   rr  = #right in [begin_s, i)            left  -> i - rr
-//   nL  = count_s - #right in s             right -> begin_s + nL + rr
+// RepartitionInstances (Alg. 1) in one pass per level.  Rows of a split segment s go
+// left (bin <= split_bin) or right; the order of rows inside a child is irrelevant to every
+// result (histograms are exact integer sums, the exports are per row), so no global scan is
+// needed: each tile reserves, with one atomic per (tile, segment) on the segment's cursors, a
+// block of its left rows growing forward from begin_s and a block of its right rows growing
+// backward from end_s; inside its blocks a tile keeps ascending position order (locality for the
+// next level's gathers).  At the end cur[2s], cur[2s+1] hold the segment's (left, right) counts.
+// Rows of unsplit segments stay in place.
 __device__ __forceinline__ int seg_of(const Seg *segs, int n_segs, int i) {
   int lo = 0, hi = n_segs - 1;  // last segment with begin <= i (non-empty one containing i)
   while (lo < hi) {
@@ -656,19 +702,25 @@ __device__ __forceinline__ int seg_of(const Seg *segs, int n_segs, int i) {
 }
 
 // Segments overlapping one partition tile, staged in shared memory (at most kTileSegs; a tile
-// that overlaps more falls back to global lookups).
+// that overlaps more takes the per-thread fallback).
 constexpr int kTileSegs = 256;
 struct TileSegs {
   int first, count;  // segment range overlapping the tile
   int begin[kTileSegs], end[kTileSegs];
   int feat[kTileSegs], sbin[kTileSegs];
+  int l0[kTileSegs], r0[kTileSegs];    // tile-prefix (left, right) at the segment's first position in the tile
+  int bl[kTileSegs], br[kTileSegs];    // reserved: left base, right base + count
 };
 
+// tile_seg[t] = the non-empty segment containing position t kPartTile (written by the previous
+// level's plan); the range may also include empty segments and the one starting at the next
+// tile, which no position maps to.
 __device__ __forceinline__ void load_tile_segs(TileSegs &T, const Seg *__restrict__ segs, int n_segs,
-                                               const DNode *__restrict__ dn, int t0, int t1) {
+                                               const DNode *__restrict__ dn, const int *__restrict__ tile_seg,
+                                               int tile, int n_tiles) {
   if (threadIdx.x == 0) {
-    const int f = seg_of(segs, n_segs, t0);
-    const int l = seg_of(segs, n_segs, t1 - 1);
+    const int f = tile_seg[tile];
+    const int l = tile + 1 < n_tiles ? tile_seg[tile + 1] : n_segs - 1;
     T.first = f;
     T.count = l - f + 1;
   }
@@ -684,85 +736,8 @@ __device__ __forceinline__ void load_tile_segs(TileSegs &T, const Seg *__restric
   __syncthreads();
 }
 
-// index (relative to T.first) of the segment containing position i, searching upward from k
-__device__ __forceinline__ int tile_seg(const TileSegs &T, int k, int i) {
-  while (T.end[k] <= i) ++k;
-  return k;
-}
-
-__global__ void __launch_bounds__(kPartThreads)
-k_part_flags(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
-             const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, size_t pitch,
-             const int32_t *__restrict__ ridx, uint32_t *__restrict__ flagbits, int *__restrict__ tile_cnt,
-             int *__restrict__ bpart) {
-  __shared__ uint32_t s_words[kPartTile / 32];
-  __shared__ TileSegs T;
-  const int n_segs = ctl->n_segs;
-  const int t0 = blockIdx.x * kPartTile;
-  const int t1 = min(n, t0 + kPartTile);
-  const int p0 = t0 + threadIdx.x * 8;
-  load_tile_segs(T, segs, n_segs, dn, t0, t1);
-  uint32_t bits = 0;
-  if (p0 < n) {
-    // 8 row ids (32 contiguous bytes per thread), their segments, then 8 independent gathers
-    int rows[8], feat[8], sbin[8];
-    const bool staged = T.count <= kTileSegs;
-    int k = 0, sg = 0;
-    if (staged) k = tile_seg(T, 0, p0); else sg = seg_of(segs, n_segs, p0);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = p0 + u;
-      rows[u] = (i < n) ? ridx[i] : 0;
-      feat[u] = -1;
-      sbin[u] = 0;
-      if (i < n) {
-        if (staged) {
-          k = tile_seg(T, k, i);
-          feat[u] = T.feat[k];
-          sbin[u] = T.sbin[k];
-        } else {
-          while (segs[sg].begin + segs[sg].count <= i) ++sg;
-          const DNode &nd = dn[segs[sg].node];
-          feat[u] = nd.feature;
-          sbin[u] = nd.split_bin;
-        }
-      }
-    }
-    uint8_t b[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      b[u] = feat[u] >= 0 ? bins[(size_t)(feat[u] >> 5) * pitch + (size_t)rows[u] * 32 + (feat[u] & 31)] : 0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) bits |= (uint32_t)(feat[u] >= 0 && b[u] > sbin[u]) << u;
-  }
-  reinterpret_cast<uint8_t *>(s_words)[threadIdx.x] = (uint8_t)bits;
-  __syncthreads();
-  const int nw = kPartTile / 32;
-  if (threadIdx.x < nw) flagbits[(size_t)blockIdx.x * nw + threadIdx.x] = s_words[threadIdx.x];
-  int c = __popc(bits);
-  for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
-  __shared__ int s_red[kPartThreads / 32];
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < kPartThreads / 32; ++w) t += s_red[w];
-    tile_cnt[blockIdx.x] = t;
-  }
-  // boundary partials for segments beginning inside this tile
-  int lo = 0, hi = n_segs;  // first segment with begin >= t0
-  while (lo < hi) { int mid = (lo + hi) >> 1; if (segs[mid].begin < t0) lo = mid + 1; else hi = mid; }
-  for (int sidx = lo + threadIdx.x; sidx < n_segs && segs[sidx].begin < t1; sidx += blockDim.x) {
-    const int off = segs[sidx].begin - t0;
-    int r = 0;
-    for (int w = 0; w < (off >> 5); ++w) r += __popc(s_words[w]);
-    if (off & 31) r += __popc(s_words[off >> 5] & ((1u << (off & 31)) - 1u));
-    bpart[sidx] = r;
-  }
-}
-
-// Block-wide exclusive scan (blockDim.x == 1024).  Returns the exclusive prefix of v and
-// writes the block total to *total.  Contains __syncthreads(); call from all threads.
+// Block-wide exclusive scan.  Returns the exclusive prefix of v and writes the block total to
+// *total.  Contains __syncthreads(); call from all threads.
 __device__ int block_excl_scan(int v, int *total) {
   __shared__ int s_w[32];
   __shared__ int s_tot;
@@ -793,46 +768,193 @@ __device__ int block_excl_scan(int v, int *total) {
   return r;
 }
 
-// Single block, phase 1: tile scan, per-segment right counts (local), children row counts.
-// seg_cnt[2s], seg_cnt[2s+1] = (left, right) rows of segment s; all-reduced across ranks
-// between phase 1 and phase 2 when world > 1 (so every rank picks the same built child).
-__global__ void __launch_bounds__(1024)
-k_part_plan1(int n, int n_tiles, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
-             const int *__restrict__ tile_cnt, int *__restrict__ tile_off, const int *__restrict__ bpart,
-             int *__restrict__ seg_nr, int *__restrict__ seg_grb, long long *__restrict__ seg_cnt) {
-  const int T = blockDim.x;
-  int carry = 0;
-  for (int base = 0; base < n_tiles; base += T) {
-    const int i = base + threadIdx.x;
-    const int v = i < n_tiles ? tile_cnt[i] : 0;
-    int tot;
-    const int e = block_excl_scan(v, &tot);
-    if (i < n_tiles) tile_off[i] = carry + e;
-    carry += tot;
-  }
-  const int total_right = carry;
+struct PlanArgs {
+  const Seg *segs;
+  Seg *segs_next;
+  LevelCtl *ctl;
+  DNode *dn;
+  const int *cur;
+  const long long *seg_cnt;  // global (left, right) counts when world > 1, else null
+  int *cur_next;
+  Pair *pairs;
+  int *tile_seg;
+  int n, n_fg, target_items, kmax;
+};
+__device__ void plan_level(const PlanArgs &A);
+
+// One 2048-position tile per block; thread t handles positions t0 + 256 u + t (u < 8), so every
+// warp-wide load, gather and store touches consecutive positions (coalesced ridx / q, adjacent
+// 32-B rows for the bin gathers, consecutive destinations).  (u, thread) order is position order:
+// left/right ranks come from warp ballots plus a 64-entry (u, warp) scan.
+__global__ void __launch_bounds__(kPartThreads, 4)
+k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
+             const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, size_t pitch,
+             const int32_t *__restrict__ ridx, const int2 *__restrict__ q, int32_t *__restrict__ ridx_out,
+             int2 *__restrict__ q_out, int *__restrict__ cur, const int *__restrict__ tile_seg, int plan_inline,
+             PlanArgs PA) {
+  static_assert(kPartTile == 8 * kPartThreads, "8 positions per thread");
+  __shared__ TileSegs T;
+  __shared__ int s_pre[8][kPartThreads / 32];  // (left | right << 16) per (u, warp), then exclusive prefix
+  __shared__ int s_tot;
   const int n_segs = ctl->n_segs;
-  for (int s = threadIdx.x; s < n_segs; s += T) {
-    const int b = segs[s].begin;
-    seg_grb[s] = (b >= n) ? total_right : (tile_off[b / kPartTile] + bpart[s]);
+  const int t0 = blockIdx.x * kPartTile;
+  const int t1 = min(n, t0 + kPartTile);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int rows[8], sg[8];
+  int2 qs[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int p = t0 + u * kPartThreads + threadIdx.x;
+    if (p < t1) { rows[u] = ridx[p]; qs[u] = q[p]; }
   }
+  load_tile_segs(T, segs, n_segs, dn, tile_seg, blockIdx.x, gridDim.x);
+  const bool staged = T.count <= kTileSegs;
+  uint32_t rbits = 0, lbits = 0;  // right / left (of a split segment) per u
+  {
+    int k = staged ? 0 : -1;
+    uint8_t b[8];
+    int sb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = t0 + u * kPartThreads + threadIdx.x;
+      int f = -1;
+      sb[u] = 0;
+      sg[u] = 0;
+      if (p < t1) {
+        if (staged) {
+          while (T.end[k] <= p) ++k;
+          f = T.feat[k];
+          sb[u] = T.sbin[k];
+        } else {
+          k = k < 0 ? seg_of(segs, n_segs, p) : k;
+          while (segs[k].begin + segs[k].count <= p) ++k;
+          const DNode &nd = dn[segs[k].node];
+          f = nd.feature;
+          sb[u] = nd.split_bin;
+        }
+        sg[u] = k;
+      }
+      b[u] = f >= 0 ? bins[(size_t)(f >> 5) * pitch + (size_t)rows[u] * 32 + (f & 31)] : 0;
+      if (f >= 0) sb[u] |= 0x100;  // split marker
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (sb[u] & 0x100) {
+        if (b[u] > (sb[u] & 0xff)) rbits |= 1u << u; else lbits |= 1u << u;
+      }
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+  if (staged) {
+    uint32_t balL[8], balR[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      balL[u] = __ballot_sync(0xffffffffu, (lbits >> u) & 1);
+      balR[u] = __ballot_sync(0xffffffffu, (rbits >> u) & 1);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s_pre[u][wid] = __popc(balL[u]) | (__popc(balR[u]) << 16);
+    }
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of the 64 (u, warp) counts in position order
+      const int v0 = (&s_pre[0][0])[2 * lane], v1 = (&s_pre[0][0])[2 * lane + 1];
+      int incl = v0 + v1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int ex = incl - v0 - v1;
+      (&s_pre[0][0])[2 * lane] = ex;
+      (&s_pre[0][0])[2 * lane + 1] = ex + v0;
+      if (lane == 31) s_tot = incl;
+    }
+    __syncthreads();
+    int exL[8], exR[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int pre = s_pre[u][wid];
+      exL[u] = (pre & 0xffff) + __popc(balL[u] & lt);
+      exR[u] = (pre >> 16) + __popc(balR[u] & lt);
+      const int p = t0 + u * kPartThreads + threadIdx.x;
+      if (p < t1 && p == max(T.begin[sg[u]], t0)) {  // first position of the segment in this tile
+        T.l0[sg[u]] = exL[u];
+        T.r0[sg[u]] = exR[u];
+      }
+    }
+    __syncthreads();
+    // per segment: the tile's (left, right) rows = prefix difference to the next non-empty one
+    for (int k = threadIdx.x; k < T.count; k += blockDim.x) {
+      const int f0 = max(T.begin[k], t0);
+      if (T.feat[k] < 0 || f0 >= min(T.end[k], t1)) continue;
+      int k2 = k + 1;
+      while (k2 < T.count && max(T.begin[k2], t0) >= min(T.end[k2], t1)) ++k2;
+      const int nxt = k2 < T.count ? (T.l0[k2] | (T.r0[k2] << 16)) : s_tot;
+      const int cl = (nxt & 0xffff) - T.l0[k], cr = (nxt >> 16) - T.r0[k];
+      const int s = T.first + k;
+      T.bl[k] = cl ? atomicAdd(&cur[2 * s], cl) : 0;
+      T.br[k] = (cr ? atomicAdd(&cur[2 * s + 1], cr) : 0) + cr;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = t0 + u * kPartThreads + threadIdx.x;
+      if (p >= t1) break;
+      const int k = sg[u];
+      int pos = p;
+      if ((lbits >> u) & 1) pos = T.begin[k] + T.bl[k] + (exL[u] - T.l0[k]);
+      else if ((rbits >> u) & 1) pos = T.end[k] - T.br[k] + (exR[u] - T.r0[k]);
+      ridx_out[pos] = rows[u];
+      q_out[pos] = qs[u];
+    }
+  } else {
+    // many segments in the tile (deep trees, tiny nodes): one global reservation per row
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = t0 + u * kPartThreads + threadIdx.x;
+      if (p >= t1) break;
+      int pos = p;
+      if ((lbits >> u) & 1) pos = segs[sg[u]].begin + atomicAdd(&cur[2 * sg[u]], 1);
+      else if ((rbits >> u) & 1)
+        pos = segs[sg[u]].begin + segs[sg[u]].count - 1 - atomicAdd(&cur[2 * sg[u] + 1], 1);
+      ridx_out[pos] = rows[u];
+      q_out[pos] = qs[u];
+    }
+  }
+  if (!plan_inline) return;
+  // world == 1: the last tile to finish plans the next level (its cursors are final)
+  __shared__ int s_last;
+  __threadfence();
   __syncthreads();
-  for (int s = threadIdx.x; s < n_segs; s += T) {
-    const int e = (s + 1 < n_segs) ? seg_grb[s + 1] : total_right;
-    const int nr = e - seg_grb[s];
-    seg_nr[s] = nr;
-    seg_cnt[2 * s] = segs[s].count - nr;
-    seg_cnt[2 * s + 1] = nr;
-  }
+  if (threadIdx.x == 0) s_last = atomicAdd(&PA.ctl->part_done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  plan_level(PA);
+  if (threadIdx.x == 0) PA.ctl->part_done = 0;
 }
 
-// Single block, phase 2: children n_rows (global counts), next level's segments (split -> 2,
-// leaf -> pass-through 1) and sibling pairs (built = child with fewer global rows, ties
-// left, R17), histogram chunking.  Saves the old segment count for k_part_scatter.
-__global__ void __launch_bounds__(1024)
-k_part_plan2(const Seg *__restrict__ segs, Seg *__restrict__ segs_next, LevelCtl *ctl, DNode *dn,
-             const int *__restrict__ seg_nr, const long long *__restrict__ seg_cnt, Pair *__restrict__ pairs,
-             int n_fg, int target_items, int kmax) {
+// world > 1: the local (left, right) counts of the level's segments, widened for the all-reduce
+// (entries past n_segs are zero on every rank).
+__global__ void k_part_counts(const int *__restrict__ cur, const LevelCtl *__restrict__ ctl, int len,
+                              long long *__restrict__ seg_cnt) {
+  const int n2 = 2 * ctl->n_segs;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+    seg_cnt[i] = i < n2 ? cur[i] : 0;
+}
+
+// Single block, after the partition: children n_rows (global counts: seg_cnt when world > 1,
+// else the local cursors), next level's segments (split -> 2, leaf -> pass-through 1) and sibling
+// pairs (built = child with fewer global rows, ties left, R17), histogram chunking; zeroes the
+// next level's cursors.
+__device__ void plan_level(const PlanArgs &A) {
+  const Seg *__restrict__ segs = A.segs;
+  Seg *__restrict__ segs_next = A.segs_next;
+  LevelCtl *ctl = A.ctl;
+  DNode *dn = A.dn;
+  const long long *__restrict__ seg_cnt = A.seg_cnt;
+  Pair *__restrict__ pairs = A.pairs;
+  const int n_fg = A.n_fg, target_items = A.target_items, kmax = A.kmax;
   const int T = blockDim.x;
   const int n_segs = ctl->n_segs;
   int nseg_carry = 0, npair_carry = 0;
@@ -848,8 +970,8 @@ k_part_plan2(const Seg *__restrict__ segs, Seg *__restrict__ segs_next, LevelCtl
       const Seg S = segs[s];
       const int ns = nseg_carry + es, np = npair_carry + ep;
       if (split) {
-        const int nr = seg_nr[s], nl = S.count - nr;
-        const long long gl = seg_cnt[2 * s], gr = seg_cnt[2 * s + 1];
+        const int nl = __ldcg(A.cur + 2 * s), nr = __ldcg(A.cur + 2 * s + 1);  // final atomics (L2)
+        const long long gl = seg_cnt ? seg_cnt[2 * s] : nl, gr = seg_cnt ? seg_cnt[2 * s + 1] : nr;
         dn[2 * S.node + 1].n_rows = gl;
         dn[2 * S.node + 2].n_rows = gr;
         segs_next[ns] = Seg{S.begin, nl, 2 * S.node + 1, 0};
@@ -870,6 +992,16 @@ k_part_plan2(const Seg *__restrict__ segs, Seg *__restrict__ segs_next, LevelCtl
     }
     nseg_carry += tot_s;
     npair_carry += tot_p;
+  }
+  for (int i = threadIdx.x; i < 2 * nseg_carry; i += T) A.cur_next[i] = 0;
+  // tile -> first segment table of the next level (segs_next written above by this block)
+  __syncthreads();
+  const int n_tiles = (A.n + kPartTile - 1) / kPartTile;
+  for (int sn = threadIdx.x; sn < nseg_carry; sn += T) {
+    const Seg S = segs_next[sn];
+    if (S.count == 0) continue;
+    for (int t = (S.begin + kPartTile - 1) / kPartTile; t < n_tiles && t * kPartTile < S.begin + S.count; ++t)
+      A.tile_seg[t] = sn;
   }
   // chunk size: about target_items items per level, within [1024, kmax] rows (s32 bound)
   __shared__ unsigned long long s_rows;
@@ -895,7 +1027,6 @@ k_part_plan2(const Seg *__restrict__ segs, Seg *__restrict__ segs_next, LevelCtl
     chunk_carry += tot;
   }
   if (threadIdx.x == 0) {
-    ctl->pad[0] = n_segs;  // segment count of the level being scattered
     ctl->n_pairs = n_pairs;
     ctl->n_items = chunk_carry * n_fg;
     ctl->n_segs = nseg_carry;
@@ -903,73 +1034,7 @@ k_part_plan2(const Seg *__restrict__ segs, Seg *__restrict__ segs_next, LevelCtl
   }
 }
 
-__global__ void __launch_bounds__(kPartThreads)
-k_part_scatter(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
-               const uint32_t *__restrict__ flagbits, const int *__restrict__ tile_off,
-               const int *__restrict__ seg_nr, const int *__restrict__ seg_grb,
-               const int32_t *__restrict__ ridx, const int2 *__restrict__ q, int32_t *__restrict__ ridx_out,
-               int2 *__restrict__ q_out) {
-  __shared__ uint32_t s_words[kPartTile / 32];
-  __shared__ int s_first, s_count;
-  __shared__ int s_begin[kTileSegs], s_end[kTileSegs], s_nl[kTileSegs], s_grb[kTileSegs];
-  const int nw = kPartTile / 32;
-  const int t0 = blockIdx.x * kPartTile;
-  const int t1 = min(n, t0 + kPartTile);
-  const int n_segs = ctl->pad[0];
-  if (threadIdx.x < nw) s_words[threadIdx.x] = flagbits[(size_t)blockIdx.x * nw + threadIdx.x];
-  if (threadIdx.x == 0) {
-    const int f = seg_of(segs, n_segs, t0);
-    s_first = f;
-    s_count = seg_of(segs, n_segs, t1 - 1) - f + 1;
-  }
-  __syncthreads();
-  const bool staged = s_count <= kTileSegs;
-  if (staged)
-    for (int k = threadIdx.x; k < s_count; k += blockDim.x) {
-      const Seg S = segs[s_first + k];
-      s_begin[k] = S.begin;
-      s_end[k] = S.begin + S.count;
-      s_nl[k] = S.count - seg_nr[s_first + k];
-      s_grb[k] = seg_grb[s_first + k];
-    }
-  __syncthreads();
-  const int p0 = t0 + threadIdx.x * 8;
-  if (p0 >= n) return;
-  // rights in this tile before p0
-  const int off = threadIdx.x * 8;
-  int r = 0;
-  for (int w = 0; w < (off >> 5); ++w) r += __popc(s_words[w]);
-  if (off & 31) r += __popc(s_words[off >> 5] & ((1u << (off & 31)) - 1u));
-  const uint32_t bits = (s_words[off >> 5] >> (off & 31)) & 0xffu;
-  int gr = tile_off[blockIdx.x] + r;  // global right rank at p0
-  int rows[8];
-  int2 qs[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    if (p0 + u < n) { rows[u] = ridx[p0 + u]; qs[u] = q[p0 + u]; }
-  }
-  int k = 0, sg = 0;
-  if (staged) { while (s_end[k] <= p0) ++k; } else { sg = seg_of(segs, n_segs, p0); }
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int i = p0 + u;
-    if (i >= n) break;
-    int begin, nl, grb;
-    if (staged) {
-      while (s_end[k] <= i) ++k;
-      begin = s_begin[k]; nl = s_nl[k]; grb = s_grb[k];
-    } else {
-      while (segs[sg].begin + segs[sg].count <= i) ++sg;
-      begin = segs[sg].begin; nl = segs[sg].count - seg_nr[sg]; grb = seg_grb[sg];
-    }
-    const int rr = gr - grb;
-    const int right = (bits >> u) & 1;
-    const int pos = right ? begin + nl + rr : i - rr;
-    ridx_out[pos] = rows[u];
-    q_out[pos] = qs[u];
-    gr += right;
-  }
-}
+__global__ void __launch_bounds__(1024) k_part_plan(PlanArgs A) { plan_level(A); }
 
 // ---------------------------------------------------------------------------------------------
 // Prediction (Eq. 1): margin[row] += leaf(tree, bins_row), binned traversal, per tree in order.
@@ -1042,12 +1107,8 @@ static void ensure_work(oocgb_data d, int D) {
     w->q[i] = (int2 *)dmalloc(sizeof(int2) * n);
     w->segs[i] = (Seg *)dmalloc(sizeof(Seg) * max_segs);
   }
-  w->flagbits = (uint32_t *)dmalloc(sizeof(uint32_t) * tiles * (kPartTile / 32));
-  w->tile_cnt = (int *)dmalloc(sizeof(int) * tiles);
-  w->tile_off = (int *)dmalloc(sizeof(int) * tiles);
-  w->bpart = (int *)dmalloc(sizeof(int) * max_segs);
-  w->seg_nr = (int *)dmalloc(sizeof(int) * max_segs);
-  w->seg_grb = (int *)dmalloc(sizeof(int) * max_segs);
+  for (int i = 0; i < 2; ++i) w->seg_cur[i] = (int *)dmalloc(sizeof(int) * 2 * max_segs);
+  w->tile_seg = (int *)dmalloc(sizeof(int) * std::max<int64_t>(1, tiles));
   w->seg_cnt = (long long *)dmalloc(sizeof(long long) * 2 * max_segs);
   w->pairs = (Pair *)dmalloc(sizeof(Pair) * max_pairs);
   w->partial = (int *)dmalloc((size_t)items * kFG * kBins * 2 * sizeof(int));
@@ -1069,8 +1130,7 @@ void free_work(oocgb_data d) {
   Work *w = d->work;
   if (!w) return;
   for (int i = 0; i < 2; ++i) { dfree(w->ridx[i]); dfree(w->q[i]); dfree(w->segs[i]); dfree(w->phist[i]); }
-  dfree(w->flagbits); dfree(w->tile_cnt); dfree(w->tile_off); dfree(w->bpart); dfree(w->seg_nr);
-  dfree(w->seg_grb); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
+  dfree(w->seg_cur[0]); dfree(w->seg_cur[1]); dfree(w->tile_seg); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
   dfree(w->cand); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg); dfree(w->d_rp);
   dfree(w->sw.row_node); dfree(w->sw.b_slot); dfree(w->sw.b_ridx); dfree(w->sw.b_q); dfree(w->sw.slot_cnt);
   dfree(w->sw.slot_cur);
@@ -1115,6 +1175,8 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   OOCGB_CK(cudaGetLastError());
   int cur = 0;
   const int tiles = (n + kPartTile - 1) / kPartTile;
+  OOCGB_CK(cudaMemsetAsync(w->seg_cur[0], 0, 2 * sizeof(int), c->stream));  // the root segment's cursors
+  if (tiles > 0) OOCGB_CK(cudaMemsetAsync(w->tile_seg, 0, sizeof(int) * tiles, c->stream));  // one root segment
   for (int lv = 0; lv < D; ++lv) {
     const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
     mark(0, true);
@@ -1139,31 +1201,29 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.dbg = keep_debug ? w->dbg : nullptr;
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 0;
-    const int64_t warps = (int64_t)max_pairs * m * 2;
-    k_eval<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, c->stream>>>(A);
-    OOCGB_CK(cudaGetLastError());
-    k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, c->stream>>>(lv, m, w->pairs, w->ctl, w->cand, w->dnodes,
-                                                                 d->d_cut_values, d->d_cut_ptrs, w->d_rp, lambda,
-                                                                 eta);
-    OOCGB_CK(cudaGetLastError());
+    A.cut_values = d->d_cut_values; A.eta = eta;
+    launch_eval(A, max_pairs, c->stream);
     mark(1, false);
     mark(2, true);
+    PlanArgs PA;
+    PA.segs = w->segs[cur]; PA.segs_next = w->segs[cur ^ 1]; PA.ctl = w->ctl; PA.dn = w->dnodes;
+    PA.cur = w->seg_cur[lv & 1]; PA.seg_cnt = c->world > 1 ? w->seg_cnt : nullptr;
+    PA.cur_next = w->seg_cur[(lv + 1) & 1]; PA.pairs = w->pairs; PA.tile_seg = w->tile_seg;
+    PA.n = n; PA.n_fg = n_fg; PA.target_items = target; PA.kmax = kmax;
+    const bool inline_plan = c->world == 1 && n > 0;
     if (n > 0) {
-      k_part_flags<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
-                                                          w->ridx[cur], w->flagbits, w->tile_cnt, w->bpart);
+      k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
+                                                          w->ridx[cur], w->q[cur], w->ridx[cur ^ 1], w->q[cur ^ 1],
+                                                          w->seg_cur[lv & 1], w->tile_seg, inline_plan ? 1 : 0, PA);
       OOCGB_CK(cudaGetLastError());
     }
-    k_part_plan1<<<1, 1024, 0, c->stream>>>(n, tiles, w->segs[cur], w->ctl, w->tile_cnt, w->tile_off, w->bpart,
-                                            w->seg_nr, w->seg_grb, w->seg_cnt);
-    OOCGB_CK(cudaGetLastError());
-    if (c->world > 1) allreduce_sum_i64(c, w->seg_cnt, 2 * (size_t)(1 << lv));
-    k_part_plan2<<<1, 1024, 0, c->stream>>>(w->segs[cur], w->segs[cur ^ 1], w->ctl, w->dnodes, w->seg_nr,
-                                            w->seg_cnt, w->pairs, n_fg, target, kmax);
-    OOCGB_CK(cudaGetLastError());
-    if (n > 0) {
-      k_part_scatter<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->flagbits, w->tile_off,
-                                                            w->seg_nr, w->seg_grb, w->ridx[cur], w->q[cur],
-                                                            w->ridx[cur ^ 1], w->q[cur ^ 1]);
+    if (c->world > 1) {
+      const int len = 2 * (1 << lv);
+      k_part_counts<<<(len + 255) / 256, 256, 0, c->stream>>>(w->seg_cur[lv & 1], w->ctl, len, w->seg_cnt);
+      allreduce_sum_i64(c, w->seg_cnt, (size_t)len);
+    }
+    if (!inline_plan) {
+      k_part_plan<<<1, 1024, 0, c->stream>>>(PA);
       OOCGB_CK(cudaGetLastError());
     }
     mark(2, false);
@@ -1499,11 +1559,8 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     A.dbg = keep_debug ? w->dbg : nullptr;
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 1;
-    const int64_t warps = (int64_t)n_slots * m * 2;
-    k_eval<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, c->stream>>>(A);
-    k_finalize<<<(unsigned)(n_slots * 2), 256, 0, c->stream>>>(lv, m, w->pairs, w->ctl, w->cand, w->dnodes,
-                                                               d->d_cut_values, d->d_cut_ptrs, w->d_rp, lambda, eta);
-    OOCGB_CK(cudaGetLastError());
+    A.cut_values = d->d_cut_values; A.eta = eta;
+    launch_eval(A, n_slots, c->stream);
   }
   // export (same as the in-core path)
   std::vector<DNode> hn(n_nodes);
