@@ -69,6 +69,7 @@ struct Work {
   oocgb::Seg *segs[2] = {nullptr, nullptr};
   int *seg_cur[2] = {nullptr, nullptr};  // per-segment (left, right) cursors, ping-pong by level
   int *tile_seg = nullptr;               // partition tile -> first segment
+  int *chunk_pair = nullptr;             // histogram chunk -> pair
   long long *seg_cnt = nullptr;
   oocgb::Pair *pairs = nullptr;
   int *partial = nullptr;
@@ -119,9 +120,16 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
                              double lambda, double mcw, double eta, Seg *segs,
                              Pair *pairs, LevelCtl *ctl, int n_sel, int n_fg, int target_items,
                              int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
-                             const int2 *q_in, int2 *q_out, int ridx_mode) {
+                             const int2 *q_in, int2 *q_out, int ridx_mode, int *chunk_pair) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nth = gridDim.x * blockDim.x;
+  {
+    long long cr = ((long long)n_sel * n_fg + target_items - 1) / target_items;
+    if (cr < 1024) cr = 1024;
+    if (cr > kmax) cr = kmax;
+    const int nch = (int)((n_sel + cr - 1) / cr);
+    for (int c = tid; c < nch; c += nth) chunk_pair[c] = 0;  // every root chunk belongs to pair 0
+  }
   for (int v = tid; v < n_nodes; v += nth) {
     DNode nd{};
     nd.feature = -2;
@@ -179,11 +187,11 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
 __global__ void __launch_bounds__(kHistThreads, 3)
 k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
        const int2 *__restrict__ q, const Pair *__restrict__ pairs, const LevelCtl *__restrict__ ctl,
-       int *__restrict__ partial, int identity, int row_step) {
+       const int *__restrict__ chunk_pair, int *__restrict__ partial, int identity, int row_step) {
   extern __shared__ int4 smem4[];
   int *S = reinterpret_cast<int *>(smem4);
   char *Sb = reinterpret_cast<char *>(smem4);
-  const int n_items = ctl->n_items, n_pairs = ctl->n_pairs;
+  const int n_items = ctl->n_items;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int half = lane & 1, rslot = lane >> 1;
   const int wq = rslot >> 2, bq = (rslot & 3) * 8;
@@ -198,12 +206,7 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
   // tiled device pages, the row stride for a row-major (streamed) page with pitch 32
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int fg = item % n_fg, cg = item / n_fg;
-    int lo = 0, hi = n_pairs - 1;  // largest p with chunk_base <= cg
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (pairs[mid].chunk_base <= cg) lo = mid; else hi = mid - 1;
-    }
-    const Pair P = pairs[lo];
+    const Pair P = pairs[chunk_pair[cg]];
     const int c = cg - P.chunk_base;
     const int r0 = P.begin + c * P.chunk_rows;
     const int r1 = min(P.begin + P.count, r0 + P.chunk_rows);
@@ -778,6 +781,7 @@ struct PlanArgs {
   int *cur_next;
   Pair *pairs;
   int *tile_seg;
+  int *chunk_pair;  // histogram chunk -> pair (k_hist's item lookup)
   int n, n_fg, target_items, kmax;
 };
 __device__ void plan_level(const PlanArgs &A);
@@ -1023,6 +1027,7 @@ __device__ void plan_level(const PlanArgs &A) {
       pairs[p].chunk_base = chunk_carry + e;
       pairs[p].n_chunks = nch;
       pairs[p].chunk_rows = (int)cr;
+      for (int c = 0; c < nch; ++c) A.chunk_pair[chunk_carry + e + c] = p;
     }
     chunk_carry += tot;
   }
@@ -1109,6 +1114,7 @@ static void ensure_work(oocgb_data d, int D) {
   }
   for (int i = 0; i < 2; ++i) w->seg_cur[i] = (int *)dmalloc(sizeof(int) * 2 * max_segs);
   w->tile_seg = (int *)dmalloc(sizeof(int) * std::max<int64_t>(1, tiles));
+  w->chunk_pair = (int *)dmalloc(sizeof(int) * items);  // chunks <= items
   w->seg_cnt = (long long *)dmalloc(sizeof(long long) * 2 * max_segs);
   w->pairs = (Pair *)dmalloc(sizeof(Pair) * max_pairs);
   w->partial = (int *)dmalloc((size_t)items * kFG * kBins * 2 * sizeof(int));
@@ -1130,7 +1136,7 @@ void free_work(oocgb_data d) {
   Work *w = d->work;
   if (!w) return;
   for (int i = 0; i < 2; ++i) { dfree(w->ridx[i]); dfree(w->q[i]); dfree(w->segs[i]); dfree(w->phist[i]); }
-  dfree(w->seg_cur[0]); dfree(w->seg_cur[1]); dfree(w->tile_seg); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
+  dfree(w->seg_cur[0]); dfree(w->seg_cur[1]); dfree(w->tile_seg); dfree(w->chunk_pair); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
   dfree(w->cand); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg); dfree(w->d_rp);
   dfree(w->sw.row_node); dfree(w->sw.b_slot); dfree(w->sw.b_ridx); dfree(w->sw.b_q); dfree(w->sw.slot_cnt);
   dfree(w->sw.slot_cur);
@@ -1171,7 +1177,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
       w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta, w->segs[0], w->pairs, w->ctl, n, n_fg, target, kmax,
-      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode);
+      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode, w->chunk_pair);
   OOCGB_CK(cudaGetLastError());
   int cur = 0;
   const int tiles = (n + kPartTile - 1) / kPartTile;
@@ -1181,7 +1187,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
     mark(0, true);
     k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur], w->q[cur],
-                                                                 w->pairs, w->ctl, w->partial,
+                                                                 w->pairs, w->ctl, w->chunk_pair, w->partial,
                                                                  (lv == 0 && ridx_mode == 0) ? 1 : 0, 32);
     OOCGB_CK(cudaGetLastError());
     mark(0, false);
@@ -1209,6 +1215,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     PA.segs = w->segs[cur]; PA.segs_next = w->segs[cur ^ 1]; PA.ctl = w->ctl; PA.dn = w->dnodes;
     PA.cur = w->seg_cur[lv & 1]; PA.seg_cnt = c->world > 1 ? w->seg_cnt : nullptr;
     PA.cur_next = w->seg_cur[(lv + 1) & 1]; PA.pairs = w->pairs; PA.tile_seg = w->tile_seg;
+    PA.chunk_pair = w->chunk_pair;
     PA.n = n; PA.n_fg = n_fg; PA.target_items = target; PA.kmax = kmax;
     const bool inline_plan = c->world == 1 && n > 0;
     if (n > 0) {
@@ -1407,10 +1414,11 @@ __global__ void k_stream_assign(const uint8_t *__restrict__ batch, int stride, i
 }
 
 // single block: slot offsets, the batch's pair table (one "pair" per slot: built = node, no
-// derived) with chunking, and the item count.
+// derived) with chunking, and the item count (batch_rows = 0: the pair list alone).
 __global__ void __launch_bounds__(1024)
 k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *__restrict__ slot_cur,
-              Pair *__restrict__ pairs, LevelCtl *ctl, int n_fg, int target_items, int kmax, int64_t batch_rows) {
+              Pair *__restrict__ pairs, LevelCtl *ctl, int n_fg, int target_items, int kmax, int64_t batch_rows,
+              int *__restrict__ chunk_pair) {
   long long cr = (batch_rows * n_fg + target_items - 1) / target_items;
   if (cr < 1024) cr = 1024;
   if (cr > kmax) cr = kmax;
@@ -1418,7 +1426,7 @@ k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *_
   for (int base = 0; base < n_slots; base += blockDim.x) {
     const int sl = base + threadIdx.x;
     const int cnt = sl < n_slots ? slot_cnt[sl] : 0;
-    const int nch = (int)((cnt + cr - 1) / cr);
+    const int nch = batch_rows > 0 ? (int)((cnt + cr - 1) / cr) : 0;  // 0: pair list only (evaluation)
     int tr, tc;
     const int er = block_excl_scan(cnt, &tr);
     const int ec = block_excl_scan(nch, &tc);
@@ -1430,6 +1438,7 @@ k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *_
       pr.chunk_base = carry_chunks + ec; pr.n_chunks = nch; pr.chunk_rows = (int)cr;
       pr.compact = 0;
       pairs[sl] = pr;
+      for (int c = 0; c < nch; ++c) chunk_pair[carry_chunks + ec + c] = sl;
     }
     carry_rows += tr;
     carry_chunks += tc;
@@ -1517,7 +1526,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   const int target = w->hist_grid;
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta,
                                                        w->segs[0], w->pairs, w->ctl, 0, n_fg, target, kmax, D,
-                                                       d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], 0);
+                                                       d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], 0, w->chunk_pair);
   k_stream_init<<<c->num_sms * 4, 256, 0, c->stream>>>(sw.row_node, n);
   OOCGB_CK(cudaGetLastError());
   const int grid = c->num_sms * 8;
@@ -1533,12 +1542,12 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
       OOCGB_CK(cudaGetLastError());
       if (!hist) return;
       k_stream_plan<<<1, 1024, 0, c->stream>>>(n_slots, first, sw.slot_cnt, sw.slot_cur, w->pairs, w->ctl, n_fg,
-                                               target, kmax, nr);
+                                               target, kmax, nr, w->chunk_pair);
       k_stream_scatter<<<grid, 256, 0, c->stream>>>(r0, nr, sw.b_slot, sw.slot_cur, d->d_q, sw.b_ridx, sw.b_q);
       {
         PhaseTimer t(c, 0);
         k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(batch, 32, m, n_fg, sw.b_ridx, sw.b_q, w->pairs,
-                                                                     w->ctl, w->partial, 0, d->stride);
+                                                                     w->ctl, w->chunk_pair, w->partial, 0, d->stride);
       }
       const int64_t tot = (int64_t)n_slots * m * kBins;
       k_accum_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
@@ -1548,7 +1557,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     if (!hist) break;
     // every node of the level: pairs[s] = {built = first + s} over the whole data
     k_stream_plan<<<1, 1024, 0, c->stream>>>(n_slots, first, sw.slot_cnt, sw.slot_cur, w->pairs, w->ctl, n_fg,
-                                             target, kmax, 1);
+                                             target, kmax, 0, w->chunk_pair);
     PhaseTimer t(c, 1);
     EvalArgs A;
     A.d = lv; A.D = D; A.m = m; A.n_fg = n_fg;
