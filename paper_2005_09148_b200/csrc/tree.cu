@@ -184,7 +184,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
 // distinct banks (h picks the bank half, the rotation a bank inside it) -> conflict-free ATOMS.
 // Per symbol: one PRMT (bin * 256 straight from the packed word), one IADD3 (+ the lane's
 // precomputed feature offset and the shared base), two ATOMS.
-__global__ void __launch_bounds__(kHistThreads, 3)
+__global__ void __launch_bounds__(kHistThreads, 2)
 k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
        const int2 *__restrict__ q, const Pair *__restrict__ pairs, const LevelCtl *__restrict__ ctl,
        const int *__restrict__ chunk_pair, int *__restrict__ partial, int identity, int row_step) {
@@ -243,7 +243,7 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
     // is unrolled by kDepth); a set is consumed (rotation + reductions) and only then refilled
     // with the row kDepth steps ahead, so no in-flight register is ever copied; the row id for
     // a refill is loaded one round earlier still.
-    constexpr int kDepth = 5;
+    constexpr int kDepth = 3;
     int k = r0 + (threadIdx.x >> 1);
     uint4 xs[kDepth];
     int2 qs[kDepth];
@@ -1092,7 +1092,7 @@ static void ensure_work(oocgb_data d, int D) {
   const int n_fg = (m + kFG - 1) / kFG;
   const int64_t n = std::max<int64_t>(1, d->n_sel);
   const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
-  const int hist_grid = c->num_sms * 3;
+  const int hist_grid = c->num_sms * 2;
   const int target = hist_grid;
   const int64_t max_pairs = D > 0 ? (1LL << (D - 1)) : 1;
   int64_t items = std::max<int64_t>(target, (int64_t)n_fg * ((n + kmax - 1) / kmax)) + (int64_t)n_fg * (1 + max_pairs) + n_fg;
