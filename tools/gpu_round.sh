@@ -12,7 +12,7 @@ timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/
 if [ -z "$SKIP_NCU" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
      python bench.py --profile-only --steps 2 --warmup 1 > gpurun_out/ncu_launch.log 2>&1; tail -2 gpurun_out/ncu_launch.log
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist -s 8 -c 2 -o gpurun_out/prof_hist -f \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hist -s 8 -c ${HIST_COUNT:-8} -o gpurun_out/prof_hist -f \
      python bench.py --profile-only --steps 1 --warmup 1 > gpurun_out/ncu_full.log 2>&1; tail -2 gpurun_out/ncu_full.log
 fi
 ls -la gpurun_out
