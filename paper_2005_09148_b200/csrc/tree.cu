@@ -784,7 +784,7 @@ struct PlanArgs {
   int *chunk_pair;  // histogram chunk -> pair (k_hist's item lookup)
   int n, n_fg, target_items, kmax;
 };
-__device__ void plan_level(const PlanArgs &A);
+__device__ void plan_level(const PlanArgs &A, int n_segs);
 
 // One 2048-position tile per block; thread t handles positions t0 + 256 u + t (u < 8), so every
 // warp-wide load, gather and store touches consecutive positions (coalesced ridx / q, adjacent
@@ -926,15 +926,19 @@ k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
     }
   }
   if (!plan_inline) return;
-  // world == 1: the last tile to finish plans the next level (its cursors are final)
+  // world == 1: the last tile to finish plans the next level (its cursors are final).  The plan
+  // reads only the cursors (atomics, at L2); the barrier + one thread's fence order this block's
+  // cursor atomics before its ticket (fences are cumulative over the barrier).
   __shared__ int s_last;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&PA.ctl->part_done, 1) == (int)gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&PA.ctl->part_done, 1) == (int)gridDim.x - 1;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  plan_level(PA);
+  plan_level(PA, n_segs);
   if (threadIdx.x == 0) PA.ctl->part_done = 0;
 }
 
@@ -951,7 +955,8 @@ __global__ void k_part_counts(const int *__restrict__ cur, const LevelCtl *__res
 // else the local cursors), next level's segments (split -> 2, leaf -> pass-through 1) and sibling
 // pairs (built = child with fewer global rows, ties left, R17), histogram chunking; zeroes the
 // next level's cursors.
-__device__ void plan_level(const PlanArgs &A) {
+// General plan (any number of segments): block-strided loops; reads back what it wrote.
+__device__ void plan_level_loop(const PlanArgs &A) {
   const Seg *__restrict__ segs = A.segs;
   Seg *__restrict__ segs_next = A.segs_next;
   LevelCtl *ctl = A.ctl;
@@ -1039,7 +1044,105 @@ __device__ void plan_level(const PlanArgs &A) {
   }
 }
 
-__global__ void __launch_bounds__(1024) k_part_plan(PlanArgs A) { plan_level(A); }
+
+// Plan with one thread per segment (n_segs <= blockDim.x, every level of a depth <= 9 tree at
+// the last-block size of 256): each thread loads its segment, cursors and node decision once and
+// writes what derives from them (children segments and cursors, its pair with chunking) without
+// reading back global memory: three dependent round trips; then the tile -> segment and chunk ->
+// pair tables are filled block-wide (a single thread filling a shallow level's ~250 tiles per
+// segment serially was ~19 us of tail on one SM).
+__device__ void plan_level(const PlanArgs &A, int n_segs) {
+  if (n_segs > (int)blockDim.x) {
+    plan_level_loop(A);
+    return;
+  }
+  const int s = threadIdx.x;
+  Seg S{};
+  int split = 0, nl = 0, nr = 0;
+  long long gl = 0, gr = 0;
+  if (s < n_segs) {
+    S = A.segs[s];
+    nl = __ldcg(A.cur + 2 * s);  // final cursor atomics (L2)
+    nr = __ldcg(A.cur + 2 * s + 1);
+    if (A.seg_cnt) { gl = A.seg_cnt[2 * s]; gr = A.seg_cnt[2 * s + 1]; }
+    split = A.dn[S.node].feature >= 0;
+  }
+  if (!A.seg_cnt) { gl = nl; gr = nr; }
+  int tot_s, tot_p;
+  const int ns = block_excl_scan(s < n_segs ? 1 + split : 0, &tot_s);
+  const int np = block_excl_scan(split, &tot_p);
+  Pair pr{};
+  const int n_tiles = (A.n + kPartTile - 1) / kPartTile;
+  // next-level segment starts staged in shared memory for the tile table (filled block-wide below)
+  __shared__ int s_begin[2 * 1024];
+  auto emit = [&](int idx, const Seg &C) {
+    A.segs_next[idx] = C;
+    A.cur_next[2 * idx] = 0;
+    A.cur_next[2 * idx + 1] = 0;
+    s_begin[idx] = C.begin;
+  };
+  if (s < n_segs) {
+    if (split) {
+      A.dn[2 * S.node + 1].n_rows = gl;
+      A.dn[2 * S.node + 2].n_rows = gr;
+      emit(ns, Seg{S.begin, nl, 2 * S.node + 1, 0});
+      emit(ns + 1, Seg{S.begin + nl, nr, 2 * S.node + 2, 0});
+      pr.parent = S.node;
+      long long gb, gd;
+      if (gl <= gr) { pr.built = 2 * S.node + 1; pr.derived = 2 * S.node + 2; pr.begin = S.begin; pr.count = nl; gb = gl; gd = gr; }
+      else { pr.built = 2 * S.node + 2; pr.derived = 2 * S.node + 1; pr.begin = S.begin + nl; pr.count = nr; gb = gr; gd = gl; }
+      // s32 histograms are exact for nodes with <= kmax rows (|q| <= 2^quant_bits)
+      pr.compact = ((gl + gr) <= A.kmax ? 1 : 0) | (gb <= A.kmax ? 2 : 0) | (gd <= A.kmax ? 4 : 0);
+    } else {
+      emit(ns, S);
+    }
+  }
+  // chunk size from the level's built rows, then each pair's chunks
+  int tot_rows;
+  block_excl_scan(split ? pr.count : 0, &tot_rows);
+  long long cr = ((long long)tot_rows * A.n_fg + A.target_items - 1) / A.target_items;
+  if (cr < 1024) cr = 1024;
+  if (cr > A.kmax) cr = A.kmax;
+  const int nch = split ? (int)((pr.count + cr - 1) / cr) : 0;
+  int tot_c;
+  const int cb = block_excl_scan(nch, &tot_c);
+  __shared__ int s_cbase[1024];
+  if (split) {
+    pr.chunk_base = cb;
+    pr.n_chunks = nch;
+    pr.chunk_rows = (int)cr;
+    A.pairs[np] = pr;
+    s_cbase[np] = cb;
+  }
+  __syncthreads();
+  // tile -> segment containing the tile's first position: the last segment starting at or
+  // before it (that one is non-empty); chunk -> pair: the last pair whose chunks start at or
+  // before it.  Block-wide binary searches in shared memory.
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    int lo = 0, hi = tot_s - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_begin[mid] <= t * kPartTile) lo = mid; else hi = mid - 1;
+    }
+    A.tile_seg[t] = lo;
+  }
+  for (int c = threadIdx.x; c < tot_c; c += blockDim.x) {
+    int lo = 0, hi = tot_p - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_cbase[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    A.chunk_pair[c] = lo;
+  }
+  if (threadIdx.x == 0) {
+    A.ctl->n_pairs = tot_p;
+    A.ctl->n_items = tot_c * A.n_fg;
+    A.ctl->n_segs = tot_s;
+    A.ctl->n_splits = 0;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_part_plan(PlanArgs A) { plan_level(A, A.ctl->n_segs); }
 
 // ---------------------------------------------------------------------------------------------
 // Prediction (Eq. 1): margin[row] += leaf(tree, bins_row), binned traversal, per tree in order.
