@@ -397,15 +397,25 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
     eg = warp_excl_scan_ll(lg, lane, tg);
     eh = warp_excl_scan_ll(lh, lane, th);
   }
-  // integer validity threshold in the node's width (|HL| <= H < 2^31 when I = int)
-  const I hmin = (sizeof(I) == 4) ? (I)(rp.h_min > INT_MAX ? INT_MAX : (rp.h_min < INT_MIN ? INT_MIN : rp.h_min))
-                                  : (I)rp.h_min;
+  // integer validity (R13) in the node's width: hmin <= HL and H - HL >= h_min <=> HL <= hmax,
+  // the thresholds clamped to I (|HL| <= H < 2^31 when I = int, so clamping never flips a test)
+  auto clampI = [](long long x) -> I {
+    if (sizeof(I) == 4) return (I)(x > INT_MAX ? INT_MAX : (x < INT_MIN ? INT_MIN : x));
+    return (I)x;
+  };
+  const I hmin = clampI(rp.h_min);
+  const I hmax = clampI((long long)H_ - rp.h_min);
   const float lamf = (float)A.lambda;
   const float gPf = (float)G * rp.sg_inv_f, hPf = (float)H * rp.sh_inv_f;
   const float tPf = __fdividef(gPf * gPf, hPf + lamf);
   const float gamf = (float)A.gamma;
-  // pass 1: float gains + bounds
-  float gf[8], tf[8];
+  // Error bound of the float gain: each float op adds <= 2^-24 relative error (the two divisions
+  // <= 2 ulp), so every term carries <= ~10 2^-24 and 2^-18 (tL + tR + tP + |gamma|) bounds the
+  // error with a >= 6x margin (tL, tR, tP >= 0: squares over positive denominators).  Its per-node
+  // part is hoisted; with the pre-filter off every valid candidate survives (tol = inf).
+  const float tol0 = rp.prefilter ? 0x1p-18f * (tPf + fabsf(gamf)) + 0x1p-100f : INFINITY;
+  // pass 1: float gains; ub = gain + tol (inf for a non-finite term: always re-evaluated)
+  float ub[8];
   unsigned vmask = 0;
   I GL = eg, HL = eh;
   float Lmax = -INFINITY;
@@ -415,24 +425,23 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
     HL += h[i];
     const int b = lane * 8 + i;
     // an empty bin repeats the previous candidate exactly, which wins the tie (lower bin)
-    const bool v = b <= B - 2 && (g[i] != 0 || h[i] != 0 || b == 0) && HL >= hmin && (H - HL) >= hmin;
-    gf[i] = -INFINITY;
-    tf[i] = 0.f;
+    const bool v = b <= B - 2 && ((g[i] | h[i]) != 0 || b == 0) && HL >= hmin && HL <= hmax;
+    ub[i] = -INFINITY;
     if (v) {
       vmask |= 1u << i;
       const float gl = (float)GL * rp.sg_inv_f, hl = (float)HL * rp.sh_inv_f;
       const float gr = (float)(G - GL) * rp.sg_inv_f, hr = (float)(H - HL) * rp.sh_inv_f;
       const float tL = __fdividef(gl * gl, hl + lamf);  // <= 2 ulp (denominator in range, see guard)
       const float tR = __fdividef(gr * gr, hr + lamf);
-      const float gain = 0.5f * ((tL + tR) - tPf) - gamf;
-      // each float op adds <= 2^-24 relative error (the two divisions <= 2 ulp), so every term
-      // carries <= ~10 2^-24: 2^-18 is >= 6x that bound on |tL| + |tR| + |tP| + |gamma|;
-      // non-finite (overflow, division by 0) -> always re-evaluate exactly
-      float tol = 0x1p-18f * (fabsf(tL) + fabsf(tR) + fabsf(tPf) + fabsf(gamf)) + 0x1p-100f;
-      if (!isfinite(gain) || !isfinite(tol) || !rp.prefilter) tol = INFINITY;
-      gf[i] = gain;
-      tf[i] = tol;
-      Lmax = fmaxf(Lmax, gain - tol);
+      const float S = tL + tR;
+      const float gain = 0.5f * (S - tPf) - gamf;
+      const float tol = 0x1p-18f * S + tol0;  // NaN / inf when a term is not finite
+      if (tol < INFINITY) {
+        ub[i] = gain + tol;
+        Lmax = fmaxf(Lmax, gain - tol);
+      } else {
+        ub[i] = INFINITY;
+      }
     }
   }
 #pragma unroll
@@ -452,7 +461,7 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
   for (int i = 0; i < 8; ++i) {
     GL += g[i];
     HL += h[i];
-    if (((vmask >> i) & 1u) && gf[i] + tf[i] >= Lmax) {
+    if (((vmask >> i) & 1u) && ub[i] >= Lmax) {
       const double gain = gain_exact(GL, HL, G, H, tP, rp.sg_inv, rp.sh_inv, A.lambda, A.gamma);
       if (!have || gain > best) { have = 1; best = gain; bbin = lane * 8 + i; bGL = (long long)GL; bHL = (long long)HL; }
     }
