@@ -123,8 +123,27 @@ struct LevelCtl {       // device-resident control block of one build
   int n_splits;         // splits decided at the current level
   int error;            // 1: H + lambda <= 0 at a node
   int part_done;        // partition tiles finished (last-block ticket), reset by the last block
-  int pad[2];
+  int hist_next;        // k_hist dynamic item counter, zeroed by whoever writes the level's chunk plan
+  int pad;
 };
+
+// Histogram chunk size (rows) for a level with tot_rows built rows in n_pairs pairs, k_hist run
+// by `grid` persistent CTAs over (chunk, feature group) items: the smallest number of waves w
+// such that C = floor(w grid / n_fg) chunks of at most kmax rows (the s32 bound) hold every pair
+// (sum_p ceil(count_p / cr) <= tot/cr + n_pairs - n_pairs/cr < C + 1 with cr = ceil(tot / (C -
+// n_pairs + 1))), so the items fill w whole waves (config 2 root: 37 equal chunks = 2 x 296 items
+// instead of 31 chunks = 1.68 waves).
+__host__ __device__ __forceinline__ long long hist_chunk_rows(long long tot, int n_pairs, int n_fg, int grid,
+                                                               long long kmax) {
+  const long long lo = kmax < 1024 ? kmax : 1024;
+  if (tot <= 0) return lo;
+  for (long long w = 1;; ++w) {
+    const long long C = w * grid / n_fg;
+    if (C < n_pairs || C < 1) continue;
+    const long long cr = (tot + (C - n_pairs + 1) - 1) / (C - n_pairs + 1);
+    if (cr <= kmax) return cr < lo ? lo : cr;
+  }
+}
 
 // byte offset of symbol (row, f) in a tiled ELLPACK buffer of pages of rpp rows
 __host__ __device__ __forceinline__ size_t ell_off(int64_t row, int f, int64_t rpp, int n_fg) {

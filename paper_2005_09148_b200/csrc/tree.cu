@@ -124,9 +124,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nth = gridDim.x * blockDim.x;
   {
-    long long cr = ((long long)n_sel * n_fg + target_items - 1) / target_items;
-    if (cr < 1024) cr = 1024;
-    if (cr > kmax) cr = kmax;
+    const long long cr = hist_chunk_rows(n_sel, 1, n_fg, target_items, kmax);
     const int nch = (int)((n_sel + cr - 1) / cr);
     for (int c = tid; c < nch; c += nth) chunk_pair[c] = 0;  // every root chunk belongs to pair 0
   }
@@ -161,11 +159,11 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
     node_fill(r, P.G, P.H, P.sg_inv, P.sh_inv, lambda, eta, &ctl->error);
     dn[0] = r;
     segs[0] = Seg{0, n_sel, 0, 0};
-    long long cr = ((long long)n_sel * n_fg + target_items - 1) / target_items;
-    if (cr < 1024) cr = 1024;
-    if (cr > kmax) cr = kmax;
-    int nch = (int)((n_sel + cr - 1) / cr);
-    pairs[0] = Pair{-1, 0, -1, 0, n_sel, 0, nch, (int)cr, (P.n_rows_global <= kmax) ? 2 : 0, {0, 0, 0}};
+    const long long cr = hist_chunk_rows(n_sel, 1, n_fg, target_items, kmax);
+    const int nch = (int)((n_sel + cr - 1) / cr);
+    const int crq = nch > 0 ? (int)((n_sel + nch - 1) / nch) : (int)cr;  // equal chunks
+    pairs[0] = Pair{-1, 0, -1, 0, n_sel, 0, nch, crq, (P.n_rows_global <= kmax) ? 2 : 0, {0, 0, 0}};
+    ctl->hist_next = 0;
     ctl->n_pairs = max_depth > 0 ? 1 : 0;
     ctl->n_items = max_depth > 0 ? nch * n_fg : 0;
     ctl->n_segs = 1;
@@ -186,7 +184,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
 // precomputed feature offset and the shared base), two ATOMS.
 __global__ void __launch_bounds__(kHistThreads, 2)
 k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
-       const int2 *__restrict__ q, const Pair *__restrict__ pairs, const LevelCtl *__restrict__ ctl,
+       const int2 *__restrict__ q, const Pair *__restrict__ pairs, LevelCtl *ctl,
        const int *__restrict__ chunk_pair, int *__restrict__ partial, int identity, int row_step) {
   extern __shared__ int4 smem4[];
   int *S = reinterpret_cast<int *>(smem4);
@@ -204,7 +202,14 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
   constexpr int RT = kHistThreads / 2;  // rows per CTA step
   // symbol (row, f) at bins + (f / 32) * pitch + row * row_step + f % 32: row_step 32 for the
   // tiled device pages, the row stride for a row-major (streamed) page with pitch 32
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  // items: the first from blockIdx, then dynamically from ctl->hist_next (chunks are numbered
+  // largest first by the plan, so this is longest-processing-time-first list scheduling); the
+  // next item is fetched while the current one runs (double-buffered slot, read after the
+  // item's closing barrier)
+  __shared__ int s_next[2];
+  int par = 0;
+  for (int item = blockIdx.x; item < n_items; par ^= 1) {
+    if (threadIdx.x == 0) s_next[par] = (int)gridDim.x + atomicAdd(&ctl->hist_next, 1);
     const int fg = item % n_fg, cg = item / n_fg;
     const Pair P = pairs[chunk_pair[cg]];
     const int c = cg - P.chunk_base;
@@ -289,6 +294,7 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
       }
     }
     __syncthreads();
+    item = s_next[par];
   }
 }
 
@@ -1021,26 +1027,25 @@ __device__ void plan_level_loop(const PlanArgs &A) {
     for (int t = (S.begin + kPartTile - 1) / kPartTile; t < n_tiles && t * kPartTile < S.begin + S.count; ++t)
       A.tile_seg[t] = sn;
   }
-  // chunk size: about target_items items per level, within [1024, kmax] rows (s32 bound)
+  // chunk size: whole waves of k_hist items, within [1024, kmax] rows (s32 bound)
   __shared__ unsigned long long s_rows;
   if (threadIdx.x == 0) s_rows = 0;
   __syncthreads();
   atomicAdd(&s_rows, (unsigned long long)rows_local);
   __syncthreads();
-  long long cr = ((long long)s_rows * n_fg + target_items - 1) / target_items;
-  if (cr < 1024) cr = 1024;
-  if (cr > kmax) cr = kmax;
   const int n_pairs = npair_carry;
+  const long long cr = hist_chunk_rows((long long)s_rows, n_pairs, n_fg, target_items, kmax);
   int chunk_carry = 0;
   for (int base = 0; base < n_pairs; base += T) {
     const int p = base + threadIdx.x;
-    const int nch = p < n_pairs ? (int)((pairs[p].count + cr - 1) / cr) : 0;
+    const int cnt = p < n_pairs ? pairs[p].count : 0;
+    const int nch = (int)((cnt + cr - 1) / cr);
     int tot;
     const int e = block_excl_scan(nch, &tot);
     if (p < n_pairs) {
       pairs[p].chunk_base = chunk_carry + e;
       pairs[p].n_chunks = nch;
-      pairs[p].chunk_rows = (int)cr;
+      pairs[p].chunk_rows = nch > 0 ? (cnt + nch - 1) / nch : (int)cr;  // equal chunks
       for (int c = 0; c < nch; ++c) A.chunk_pair[chunk_carry + e + c] = p;
     }
     chunk_carry += tot;
@@ -1050,6 +1055,7 @@ __device__ void plan_level_loop(const PlanArgs &A) {
     ctl->n_items = chunk_carry * n_fg;
     ctl->n_segs = nseg_carry;
     ctl->n_splits = 0;
+    ctl->hist_next = 0;
   }
 }
 
@@ -1106,22 +1112,37 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
       emit(ns, S);
     }
   }
-  // chunk size from the level's built rows, then each pair's chunks
+  // chunk size from the level's built rows (whole waves of k_hist items), equal chunks per pair;
+  // chunks are numbered in decreasing chunk size (longest-processing-time-first order for
+  // k_hist's dynamic item fetch; ties: pair order)
   int tot_rows;
   block_excl_scan(split ? pr.count : 0, &tot_rows);
-  long long cr = ((long long)tot_rows * A.n_fg + A.target_items - 1) / A.target_items;
-  if (cr < 1024) cr = 1024;
-  if (cr > A.kmax) cr = A.kmax;
+  const long long cr = hist_chunk_rows(tot_rows, tot_p, A.n_fg, A.target_items, A.kmax);
   const int nch = split ? (int)((pr.count + cr - 1) / cr) : 0;
-  int tot_c;
-  const int cb = block_excl_scan(nch, &tot_c);
-  __shared__ int s_cbase[1024];
+  const int crp = nch > 0 ? (pr.count + nch - 1) / nch : 0;
+  __shared__ int s_cbase[1024];  // by LPT rank: first chunk
+  __shared__ int s_key[1024];    // by pair: chunk rows; then by LPT rank: pair
+  if (split) s_key[np] = crp;
+  __syncthreads();
+  int rank = 0;
   if (split) {
-    pr.chunk_base = cb;
+    for (int q = 0; q < tot_p; ++q) {
+      const int kq = s_key[q];
+      rank += (kq > crp || (kq == crp && q < np)) ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (split) { s_key[rank] = np; s_cbase[rank] = nch; }
+  __syncthreads();
+  int tot_c;
+  const int cb = block_excl_scan(s < tot_p ? s_cbase[s] : 0, &tot_c);  // scan in rank order
+  if (s < tot_p) s_cbase[s] = cb;
+  __syncthreads();
+  if (split) {
+    pr.chunk_base = s_cbase[rank];
     pr.n_chunks = nch;
-    pr.chunk_rows = (int)cr;
+    pr.chunk_rows = nch > 0 ? crp : (int)cr;
     A.pairs[np] = pr;
-    s_cbase[np] = cb;
   }
   __syncthreads();
   // tile -> segment containing the tile's first position: the last segment starting at or
@@ -1141,13 +1162,14 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
       const int mid = (lo + hi + 1) >> 1;
       if (s_cbase[mid] <= c) lo = mid; else hi = mid - 1;
     }
-    A.chunk_pair[c] = lo;
+    A.chunk_pair[c] = s_key[lo];
   }
   if (threadIdx.x == 0) {
     A.ctl->n_pairs = tot_p;
     A.ctl->n_items = tot_c * A.n_fg;
     A.ctl->n_segs = tot_s;
     A.ctl->n_splits = 0;
+    A.ctl->hist_next = 0;
   }
 }
 
@@ -1207,7 +1229,8 @@ static void ensure_work(oocgb_data d, int D) {
   const int hist_grid = c->num_sms * 2;
   const int target = hist_grid;
   const int64_t max_pairs = D > 0 ? (1LL << (D - 1)) : 1;
-  int64_t items = std::max<int64_t>(target, (int64_t)n_fg * ((n + kmax - 1) / kmax)) + (int64_t)n_fg * (1 + max_pairs) + n_fg;
+  // bound of hist_chunk_rows' item count: C <= n_pairs - 1 + ceil(rows / kmax) + ceil(grid / n_fg)
+  int64_t items = target + (int64_t)n_fg * (((n + kmax - 1) / kmax) + max_pairs + 2) + n_fg;
   if (w && w->cap_rows >= n && w->max_depth >= D && w->m == m && w->items_cap >= items) return;
   free_work(d);
   w = new Work();
@@ -1531,9 +1554,7 @@ __global__ void __launch_bounds__(1024)
 k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *__restrict__ slot_cur,
               Pair *__restrict__ pairs, LevelCtl *ctl, int n_fg, int target_items, int kmax, int64_t batch_rows,
               int *__restrict__ chunk_pair) {
-  long long cr = (batch_rows * n_fg + target_items - 1) / target_items;
-  if (cr < 1024) cr = 1024;
-  if (cr > kmax) cr = kmax;
+  const long long cr = hist_chunk_rows(batch_rows, n_slots, n_fg, target_items, kmax);
   int carry_rows = 0, carry_chunks = 0;
   for (int base = 0; base < n_slots; base += blockDim.x) {
     const int sl = base + threadIdx.x;
@@ -1547,7 +1568,8 @@ k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *_
       Pair pr;
       pr.parent = -1; pr.built = first_d + sl; pr.derived = -1;
       pr.begin = carry_rows + er; pr.count = cnt;
-      pr.chunk_base = carry_chunks + ec; pr.n_chunks = nch; pr.chunk_rows = (int)cr;
+      pr.chunk_base = carry_chunks + ec; pr.n_chunks = nch;
+      pr.chunk_rows = nch > 0 ? (cnt + nch - 1) / nch : (int)cr;  // equal chunks
       pr.compact = 0;
       pairs[sl] = pr;
       for (int c = 0; c < nch; ++c) chunk_pair[carry_chunks + ec + c] = sl;
@@ -1558,6 +1580,7 @@ k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *_
   if (threadIdx.x == 0) {
     ctl->n_pairs = n_slots;
     ctl->n_items = carry_chunks * n_fg;
+    ctl->hist_next = 0;
   }
 }
 
