@@ -31,7 +31,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
     tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *SRC, "-ldl"]
+    extra = os.environ.get("OOCGB_EXTRA_NVCC", "").split()  # tuning experiments (-D...)
+    cmd = [NVCC, *FLAGS, *extra, "-o", tmp, *SRC, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

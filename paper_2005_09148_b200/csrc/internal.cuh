@@ -124,6 +124,7 @@ struct LevelCtl {       // device-resident control block of one build
   int error;            // 1: H + lambda <= 0 at a node
   int part_done;        // partition tiles finished (last-block ticket), reset by the last block
   int hist_next;        // k_hist dynamic item counter, zeroed by whoever writes the level's chunk plan
+  int n_ew, n_en;       // eval work lists: (pair, side) entries of nodes with > kmax / <= kmax rows
   int pad;
 };
 

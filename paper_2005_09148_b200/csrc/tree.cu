@@ -76,6 +76,8 @@ struct Work {
   long long *phist[2] = {nullptr, nullptr};
   long long *built64 = nullptr;
   oocgb::Cand *cand = nullptr;
+  int2 *ent = nullptr;  // eval work lists [2][ent_cap]
+  int ent_cap = 0;
   oocgb::DNode *dnodes = nullptr;
   oocgb::LevelCtl *ctl = nullptr;
   long long *dbg = nullptr;
@@ -120,7 +122,8 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
                              double lambda, double mcw, double eta, Seg *segs,
                              Pair *pairs, LevelCtl *ctl, int n_sel, int n_fg, int target_items,
                              int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
-                             const int2 *q_in, int2 *q_out, int ridx_mode, int *chunk_pair) {
+                             const int2 *q_in, int2 *q_out, int ridx_mode, int *chunk_pair, int2 *ent,
+                             int ent_cap) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nth = gridDim.x * blockDim.x;
   {
@@ -168,6 +171,10 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
     ctl->n_items = max_depth > 0 ? nch * n_fg : 0;
     ctl->n_segs = 1;
     ctl->n_splits = 0;
+    const bool narrow = P.n_rows_global <= kmax;  // eval work list of the root (pair 0, side 0)
+    ent[narrow ? ent_cap : 0] = make_int2(0, 0);
+    ctl->n_ew = (max_depth > 0 && !narrow) ? 1 : 0;
+    ctl->n_en = (max_depth > 0 && narrow) ? 1 : 0;
   }
 }
 
@@ -343,6 +350,8 @@ struct EvalArgs {
   int streamed;    // Alg. 6 mode: every node built directly, no parent histograms kept
   const float *cut_values;
   double eta;
+  const int2 *ent;  // per-level work lists of (pair, side): general [0, n_ew), narrow [ent_cap, + n_en)
+  int ent_cap;
 };
 
 __device__ __forceinline__ int warp_excl_scan_i(int v, int lane, int &total) {
@@ -508,20 +517,11 @@ __device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)
 // Loads, the subtraction and the parent store use the coalesced bin order bin = 32 i + lane;
 // a padded per-warp shared tile (conflict-free for both orders) then hands each lane its 8
 // consecutive bins 8 lane .. 8 lane + 7 for the scan and the evaluation.
-constexpr int kEvalWarps = 4;  // 4-warp blocks (x4 per SM): measured best of 1, 2, 4, 8
-__global__ void __launch_bounds__(kEvalWarps * 32, 4) k_eval(EvalArgs A) {
-  __shared__ longlong2 tile[kEvalWarps][256 + 32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int side = (int)(wid & 1);
-  const int64_t pj = wid >> 1;
-  const int p = (int)(pj / A.m), j = (int)(pj % A.m);
-  // sibling pairs per level: 1, 1, 2, 4, ...; the streamed mode lists every node: 2^d
-  const int max_pairs = A.streamed ? (1 << A.d) : (A.d == 0 ? 1 : (1 << (A.d - 1)));
-  if (p >= max_pairs) return;
-  const int n_pairs = A.ctl->n_pairs;  // independent of the pair load below
+constexpr int kEvalWarps = 4;  // 4-warp blocks: measured best of 1, 2, 4, 8
+constexpr int kEvalBlocksWide = 4, kEvalBlocksNarrow = 6;  // resident blocks per SM (registers)
+__device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int side, int j, int lane,
+                                               longlong2 *tl) {
   const Pair P = A.pairs[p];
-  if (p >= n_pairs) return;
   const int node = side ? P.derived : P.built;
   if (node < 0) return;
   if (A.streamed && A.dn[node].feature == -2) return;  // streamed levels list every slot
@@ -598,7 +598,6 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 4) k_eval(EvalArgs A) {
   }
   // transpose through the padded tile: element e lives in slot e + e / 8 (16-B slots), which
   // is conflict-free per quarter-warp both for e = 32 i + lane and for e = 8 lane + i
-  longlong2 *tl = tile[wib];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int e = 32 * i + lane;
@@ -612,6 +611,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 4) k_eval(EvalArgs A) {
     g[i] = v.x;
     h[i] = v.y;
   }
+  __syncwarp();  // the tile is reused by the warp's next item
   const RoundParams rp = *A.rp;
   if (nodeRows <= A.kmax) {  // every partial sum of the node is exact in int32
     int g32[8], h32[8];
@@ -620,6 +620,121 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 4) k_eval(EvalArgs A) {
     eval_node<int>(A, node, j, lane, g32, h32, rp, nodeG, nodeH);
   } else {
     eval_node<long long>(A, node, j, lane, g, h, rp, nodeG, nodeH);
+  }
+}
+
+// Persistent warps over the level's work list: item t = (entry t / m, feature t % m), entry =
+// (pair, side) written by the plan (general list: nodes with > kmax rows, streamed levels).
+__global__ void __launch_bounds__(kEvalWarps * 32, kEvalBlocksWide) k_eval(EvalArgs A) {
+  __shared__ longlong2 tile[kEvalWarps][256 + 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int n_items = A.ctl->n_ew * A.m;
+  const int nw = (int)(gridDim.x * blockDim.x) >> 5;
+  for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < n_items; t += nw) {
+    const int e = t / A.m;
+    const int2 en = A.ent[e];
+    eval_item_wide(A, en.x, en.y, t - e * A.m, lane, tile[wib]);
+  }
+}
+
+// k_eval for nodes with <= kmax rows (most nodes below the first levels): every histogram sum of
+// such a node, and every prefix sum, is exact in int32, so the whole warp works in 32-bit
+// (a wider parent or all-reduced sum is read through its low word: parent - built is exact
+// modulo 2^32 and fits).  Fewer registers than k_eval -> twice the resident warps.
+#ifndef OOCGB_EVAL_NARROW_MINB
+#define OOCGB_EVAL_NARROW_MINB 6  // 80 registers, no spills (= kEvalBlocksNarrow)
+#endif
+__device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int side, int j, int lane, int2 *tl) {
+  const Pair P = A.pairs[p];
+  const int node = side ? P.derived : P.built;
+  if (node < 0) return;
+  if (A.streamed && A.dn[node].feature == -2) return;
+  const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;
+  int g[8], h[8];  // strided: element i is bin 32 i + lane
+  const size_t hsz = (size_t)A.m * kBins * 2;
+  int2 par[8];
+  if (side) {
+    const int ps = P.parent - level_first(A.d - 1);
+    if (P.compact & 1) {
+      const int2 *src = reinterpret_cast<const int2 *>(A.phist_prev + (size_t)ps * hsz) + (size_t)j * kBins;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) par[i] = __ldg(src + 32 * i + lane);
+    } else {  // low words of the int64 pairs
+      const int4 *src = reinterpret_cast<const int4 *>(A.phist_prev + (size_t)ps * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int4 v = __ldg(src + 32 * i + lane);
+        par[i] = make_int2(v.x, v.z);
+      }
+    }
+  }
+  if (A.built64) {
+    const int4 *src = reinterpret_cast<const int4 *>(A.built64 + (size_t)p * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { const int4 v = src[32 * i + lane]; g[i] = v.x; h[i] = v.z; }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { g[i] = 0; h[i] = 0; }
+    const size_t cstride = (size_t)A.n_fg * kFG * kBins;
+    const int2 *src0 = reinterpret_cast<const int2 *>(A.partial) +
+                       (((size_t)P.chunk_base * A.n_fg + j / kFG) * kFG + (j % kFG)) * kBins + lane;
+    for (int c = 0; c < P.n_chunks; ++c) {
+      int2 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __ldg(src0 + c * cstride + 32 * i);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { g[i] += v[i].x; h[i] += v[i].y; }
+    }
+  }
+  if (side) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { g[i] = par[i].x - g[i]; h[i] = par[i].y - h[i]; }
+  }
+  const int f_d = level_first(A.d);
+  if (A.d <= A.D - 2 && !A.streamed) {
+    if (P.compact & (side ? 4 : 2)) {
+      int2 *dst = reinterpret_cast<int2 *>(A.phist_next + (size_t)(node - f_d) * hsz) + (size_t)j * kBins;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_int2(g[i], h[i]);
+    } else {
+      longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
+    }
+  }
+  if (A.dbg) {
+    longlong2 *dst = reinterpret_cast<longlong2 *>(A.dbg + (size_t)node * hsz + (size_t)j * kBins * 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = 32 * i + lane;
+    tl[e + (e >> 3)] = make_int2(g[i], h[i]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = 8 * lane + i;
+    const int2 v = tl[e + (e >> 3)];
+    g[i] = v.x;
+    h[i] = v.y;
+  }
+  __syncwarp();  // the tile is reused by the warp's next item
+  const RoundParams rp = *A.rp;
+  eval_node<int>(A, node, j, lane, g, h, rp, nodeG, nodeH);
+}
+
+// Persistent warps over the level's narrow list (nodes with <= kmax global rows, from the plan).
+__global__ void __launch_bounds__(kEvalWarps * 32, OOCGB_EVAL_NARROW_MINB) k_eval_narrow(EvalArgs A) {
+  __shared__ int2 tile2[kEvalWarps][256 + 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int n_items = A.ctl->n_en * A.m;
+  const int nw = (int)(gridDim.x * blockDim.x) >> 5;
+  for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < n_items; t += nw) {
+    const int e = t / A.m;
+    const int2 en = A.ent[A.ent_cap + e];
+    eval_item_narrow(A, en.x, en.y, t - e * A.m, lane, tile2[wib]);
   }
 }
 
@@ -692,9 +807,11 @@ k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Ca
   }
 }
 
-static void launch_eval(const EvalArgs &A, int max_pairs, cudaStream_t st) {
-  const int64_t warps = (int64_t)max_pairs * A.m * 2;
-  k_eval<<<(unsigned)((warps + kEvalWarps - 1) / kEvalWarps), kEvalWarps * 32, 0, st>>>(A);
+static void launch_eval(const EvalArgs &A, int max_pairs, int num_sms, cudaStream_t st) {
+  const int64_t blocks = ((int64_t)max_pairs * A.m * 2 + kEvalWarps - 1) / kEvalWarps;
+  k_eval<<<(unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * kEvalBlocksWide), kEvalWarps * 32, 0, st>>>(A);
+  k_eval_narrow<<<(unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * OOCGB_EVAL_NARROW_MINB), kEvalWarps * 32, 0,
+                  st>>>(A);
   k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, st>>>(A.d, A.m, A.pairs, A.ctl, A.cand, A.dn, A.cut_values,
                                                          A.cut_ptrs, A.rp, A.lambda, A.eta);
   OOCGB_CK(cudaGetLastError());
@@ -798,6 +915,8 @@ struct PlanArgs {
   int *tile_seg;
   int *chunk_pair;  // histogram chunk -> pair (k_hist's item lookup)
   int n, n_fg, target_items, kmax;
+  int2 *ent;        // eval work lists (EvalArgs::ent)
+  int ent_cap;
 };
 __device__ void plan_level(const PlanArgs &A, int n_segs);
 
@@ -1034,6 +1153,31 @@ __device__ void plan_level_loop(const PlanArgs &A) {
   atomicAdd(&s_rows, (unsigned long long)rows_local);
   __syncthreads();
   const int n_pairs = npair_carry;
+  // eval work lists: (pair, side) of nodes with <= kmax global rows -> narrow, else general
+  {
+    int ew_carry = 0, en_carry = 0;
+    for (int base = 0; base < n_pairs; base += T) {
+      const int p = base + threadIdx.x;
+      int nn = 0;
+      long long rb = 0, rd = 0;
+      if (p < n_pairs) {
+        rb = dn[pairs[p].built].n_rows;
+        rd = dn[pairs[p].derived].n_rows;
+        nn = (rb <= kmax) + (rd <= kmax);
+      }
+      int tw, tn;
+      const int ew = block_excl_scan(p < n_pairs ? 2 - nn : 0, &tw);
+      const int en = block_excl_scan(nn, &tn);
+      if (p < n_pairs) {
+        int iw = ew_carry + ew, in = en_carry + en;
+        if (rb <= kmax) A.ent[A.ent_cap + in++] = make_int2(p, 0); else A.ent[iw++] = make_int2(p, 0);
+        if (rd <= kmax) A.ent[A.ent_cap + in] = make_int2(p, 1); else A.ent[iw] = make_int2(p, 1);
+      }
+      ew_carry += tw;
+      en_carry += tn;
+    }
+    if (threadIdx.x == 0) { ctl->n_ew = ew_carry; ctl->n_en = en_carry; }
+  }
   const long long cr = hist_chunk_rows((long long)s_rows, n_pairs, n_fg, target_items, kmax);
   int chunk_carry = 0;
   for (int base = 0; base < n_pairs; base += T) {
@@ -1111,6 +1255,21 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
     } else {
       emit(ns, S);
     }
+  }
+  // eval work lists: (pair, side) of nodes with <= kmax global rows -> narrow, else general
+  {
+    long long gb = 0, gd = 0;
+    if (split) { gb = pr.built == 2 * S.node + 1 ? gl : gr; gd = pr.built == 2 * S.node + 1 ? gr : gl; }
+    const int nn = split ? (gb <= A.kmax) + (gd <= A.kmax) : 0;
+    int tw, tn;
+    const int ew = block_excl_scan(split ? 2 - nn : 0, &tw);
+    const int en = block_excl_scan(nn, &tn);
+    if (split) {
+      int iw = ew, in = en;
+      if (gb <= A.kmax) A.ent[A.ent_cap + in++] = make_int2(np, 0); else A.ent[iw++] = make_int2(np, 0);
+      if (gd <= A.kmax) A.ent[A.ent_cap + in] = make_int2(np, 1); else A.ent[iw] = make_int2(np, 1);
+    }
+    if (threadIdx.x == 0) { A.ctl->n_ew = tw; A.ctl->n_en = tn; }
   }
   // chunk size from the level's built rows (whole waves of k_hist items), equal chunks per pair;
   // chunks are numbered in decreasing chunk size (longest-processing-time-first order for
@@ -1258,6 +1417,8 @@ static void ensure_work(oocgb_data d, int D) {
   for (int i = 0; i < 2; ++i) w->phist[i] = (long long *)dmalloc(sizeof(long long) * hsz * pslots);
   if (c->world > 1 || d->streamed) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * 2 * max_pairs);
   w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)max_pairs * 2 * m);
+  w->ent_cap = (int)(2 * max_pairs);
+  w->ent = (int2 *)dmalloc(sizeof(int2) * 2 * w->ent_cap);
   w->dnodes = (DNode *)dmalloc(sizeof(DNode) * ((1LL << (D + 1)) - 1));
   w->ctl = (LevelCtl *)dmalloc(sizeof(LevelCtl));
   w->d_rp = (RoundParams *)dmalloc(sizeof(RoundParams));
@@ -1272,7 +1433,7 @@ void free_work(oocgb_data d) {
   if (!w) return;
   for (int i = 0; i < 2; ++i) { dfree(w->ridx[i]); dfree(w->q[i]); dfree(w->segs[i]); dfree(w->phist[i]); }
   dfree(w->seg_cur[0]); dfree(w->seg_cur[1]); dfree(w->tile_seg); dfree(w->chunk_pair); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
-  dfree(w->cand); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg); dfree(w->d_rp);
+  dfree(w->cand); dfree(w->ent); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg); dfree(w->d_rp);
   dfree(w->sw.row_node); dfree(w->sw.b_slot); dfree(w->sw.b_ridx); dfree(w->sw.b_q); dfree(w->sw.slot_cnt);
   dfree(w->sw.slot_cur);
   d->streamed_row_node = nullptr;
@@ -1312,7 +1473,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
       w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta, w->segs[0], w->pairs, w->ctl, n, n_fg, target, kmax,
-      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode, w->chunk_pair);
+      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode, w->chunk_pair, w->ent, w->ent_cap);
   OOCGB_CK(cudaGetLastError());
   int cur = 0;
   const int tiles = (n + kPartTile - 1) / kPartTile;
@@ -1343,7 +1504,8 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 0;
     A.cut_values = d->d_cut_values; A.eta = eta;
-    launch_eval(A, max_pairs, c->stream);
+    A.ent = w->ent; A.ent_cap = w->ent_cap;
+    launch_eval(A, max_pairs, c->num_sms, c->stream);
     mark(1, false);
     mark(2, true);
     PlanArgs PA;
@@ -1352,6 +1514,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     PA.cur_next = w->seg_cur[(lv + 1) & 1]; PA.pairs = w->pairs; PA.tile_seg = w->tile_seg;
     PA.chunk_pair = w->chunk_pair;
     PA.n = n; PA.n_fg = n_fg; PA.target_items = target; PA.kmax = kmax;
+    PA.ent = w->ent; PA.ent_cap = w->ent_cap;
     const bool inline_plan = c->world == 1 && n > 0;
     if (n > 0) {
       k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
@@ -1553,7 +1716,7 @@ __global__ void k_stream_assign(const uint8_t *__restrict__ batch, int stride, i
 __global__ void __launch_bounds__(1024)
 k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *__restrict__ slot_cur,
               Pair *__restrict__ pairs, LevelCtl *ctl, int n_fg, int target_items, int kmax, int64_t batch_rows,
-              int *__restrict__ chunk_pair) {
+              int *__restrict__ chunk_pair, int2 *__restrict__ ent) {
   const long long cr = hist_chunk_rows(batch_rows, n_slots, n_fg, target_items, kmax);
   int carry_rows = 0, carry_chunks = 0;
   for (int base = 0; base < n_slots; base += blockDim.x) {
@@ -1573,6 +1736,7 @@ k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *_
       pr.compact = 0;
       pairs[sl] = pr;
       for (int c = 0; c < nch; ++c) chunk_pair[carry_chunks + ec + c] = sl;
+      ent[sl] = make_int2(sl, 0);  // streamed evaluation: every slot in the general list
     }
     carry_rows += tr;
     carry_chunks += tc;
@@ -1581,6 +1745,8 @@ k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *_
     ctl->n_pairs = n_slots;
     ctl->n_items = carry_chunks * n_fg;
     ctl->hist_next = 0;
+    ctl->n_ew = n_slots;
+    ctl->n_en = 0;
   }
 }
 
@@ -1661,7 +1827,8 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   const int target = w->hist_grid;
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta,
                                                        w->segs[0], w->pairs, w->ctl, 0, n_fg, target, kmax, D,
-                                                       d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], 0, w->chunk_pair);
+                                                       d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], 0, w->chunk_pair, w->ent,
+                                                       w->ent_cap);
   k_stream_init<<<c->num_sms * 4, 256, 0, c->stream>>>(sw.row_node, n);
   OOCGB_CK(cudaGetLastError());
   const int grid = c->num_sms * 8;
@@ -1677,7 +1844,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
       OOCGB_CK(cudaGetLastError());
       if (!hist) return;
       k_stream_plan<<<1, 1024, 0, c->stream>>>(n_slots, first, sw.slot_cnt, sw.slot_cur, w->pairs, w->ctl, n_fg,
-                                               target, kmax, nr, w->chunk_pair);
+                                               target, kmax, nr, w->chunk_pair, w->ent);
       k_stream_scatter<<<grid, 256, 0, c->stream>>>(r0, nr, sw.b_slot, sw.slot_cur, d->d_q, sw.b_ridx, sw.b_q);
       {
         PhaseTimer t(c, 0);
@@ -1692,7 +1859,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     if (!hist) break;
     // every node of the level: pairs[s] = {built = first + s} over the whole data
     k_stream_plan<<<1, 1024, 0, c->stream>>>(n_slots, first, sw.slot_cnt, sw.slot_cur, w->pairs, w->ctl, n_fg,
-                                             target, kmax, 0, w->chunk_pair);
+                                             target, kmax, 0, w->chunk_pair, w->ent);
     PhaseTimer t(c, 1);
     EvalArgs A;
     A.d = lv; A.D = D; A.m = m; A.n_fg = n_fg;
@@ -1704,7 +1871,8 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 1;
     A.cut_values = d->d_cut_values; A.eta = eta;
-    launch_eval(A, n_slots, c->stream);
+    A.ent = w->ent; A.ent_cap = w->ent_cap;
+    launch_eval(A, n_slots, c->num_sms, c->stream);
   }
   // export (same as the in-core path)
   std::vector<DNode> hn(n_nodes);
