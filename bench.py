@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", type=int, default=N_ROWS, help="rows per GPU (config 2: 1M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl1", action="store_true",
+                    help="N=1: run the sharded code path (NCCL exchanges) on a 1-rank communicator")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON line)")
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4],
                     help="2: 1M x 500 in-core f=1 (the driver's bench); 3: 20M x 500 out-of-core, "
@@ -75,6 +77,21 @@ def hbm_peak():
     except Exception:
         pass
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def pipe_roofline(row_features, hist_ms, clocks):
+    """Shared-atomic pipe roofline of k_hist: algorithmic warp-wide ATOMS (2 per symbol / 32 lanes)
+    per second against 1 per clock per SM at the SM clock measured during the timed region."""
+    import torch
+
+    n_sms = torch.cuda.get_device_properties(0).multi_processor_count
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+    atoms = 2.0 * row_features / 32.0
+    achieved = atoms / (hist_ms * 1e-3) / 1e9
+    peak = n_sms * mhz * 1e6 / 1e9
+    return {"bound": "shared-atomic pipe", "kernel": "k_hist", "achieved": achieved, "peak": peak,
+            "unit": "G warp-ATOMS/s", "frac": achieved / peak, "ceiling_frac": 32.0 / 37.0,
+            "sm_mhz": mhz, "sms": n_sms}
 
 
 class ClockSampler:
@@ -437,6 +454,8 @@ def main():
         idl = [ob.nccl_unique_id() if rank == 0 else None]
         tdist.broadcast_object_list(idl, src=0)
         nid = idl[0]
+    elif args.nccl1:  # the multi-GPU code path (every exchange through NCCL) on a 1-rank communicator
+        nid = ob.nccl_unique_id()
     ctx = ob.Context(local, rank, world, nid, stream=stream.cuda_stream)
     rows = args.rows
     X, y = make_data(rows, rank)
@@ -573,7 +592,7 @@ def main():
             "config": {"workload": "config 2: 1M x 500 make_classification, 256 bins, depth 8, in-core, f=1",
                        "rows_per_gpu": rows, "rows_global": rows * world, "n_features": N_FEAT,
                        "max_bin": MAX_BIN, "max_depth": DEPTH, "quant_bits": QBITS,
-                       "parallelism": f"row-sharded dp{world}",
+                       "parallelism": f"row-sharded dp{world}" + (" (NCCL 1-rank exchange path)" if args.nccl1 and world == 1 else ""),
                        "l2": "inputs larger than L2 (512 MB ELLPACK per GPU vs 126 MB L2), no flush"},
             "gpu_launches": launches_per_round(DEPTH) * args.steps,
             "rows_rounds_per_s": rows * world / (ms_step / 1e3),
@@ -585,6 +604,10 @@ def main():
                          "frac": achieved / peak, "traffic": measured_traffic(), "kernel": "k_hist",
                          "algorithmic_bytes_per_launch": hist_bytes / n_hist,
                          "peak_source": peak_src},
+            # k_hist's binding on-chip resource: 2 shared atomics per symbol at <= 1
+            # conflict-free warp-wide ATOMS per clock per SM; the symbol/q loads share the L1 data
+            # pipe (4 + 1 wavefronts per 32 ATOMS at the root), so 32/37 of this peak is the ceiling
+            "pipe_roofline": pipe_roofline(hist_rowfeat, hist_ms, ck),
             "e2e": {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "wall_ms_per_step": e2e_wall_ms, "graph_captures": e2e_diag.get("graph_captures")},
             "graph_captures_timed": tm.get("graph_captures"),

@@ -93,7 +93,8 @@ typedef struct {
  * (e.g. with torch.distributed) and passes them to oocgb_ctx_create on every rank.
  * oocgb_ctx_create: binds `device`; rank/world describe the row sharding (the
  * histograms are "summed across all GPUs using AllReduce").  nccl_id may be NULL iff
- * world == 1.  cuda_stream: a cudaStream_t cast to uint64 to order work on, 0 = library
+ * world == 1; world == 1 WITH an nccl_id runs the multi-GPU code path (every exchange step
+ * through NCCL) on a 1-rank communicator, results identical to the plain context (tests).  cuda_stream: a cudaStream_t cast to uint64 to order work on, 0 = library
  * creates its own non-blocking stream.  ERR_ARG on rank/world mismatch; ERR_DEVICE on
  * CUDA/NCCL init failure.  oocgb_ctx_destroy returns ERR_STATE while data handles are alive. */
 int oocgb_nccl_unique_id(uint8_t out[128]);

@@ -83,6 +83,10 @@ def load_library():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
                           " — there is no CPU fallback")
+    try:  # torch first: the library dlopen()s libnccl.so.2 and must bind to torch's copy (a system
+        import torch  # noqa: F401  NCCL loaded first would shadow torch's bundled one)
+    except ImportError:
+        pass
     L = ctypes.CDLL(LIB_PATH)
     p, i32, i64, u64, d = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
     sig = {

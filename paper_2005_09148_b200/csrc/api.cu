@@ -77,7 +77,7 @@ const NcclApi &nccl_api() {
 }
 
 void allreduce_sum_i64(oocgb_ctx c, long long *d_buf, size_t count) {
-  if (c->world <= 1 || count == 0) return;
+  if (!c->coll || count == 0) return;
   if (c->host_coll) {
     std::vector<long long> h(count);
     OOCGB_CK(cudaMemcpyAsync(h.data(), d_buf, 8 * count, cudaMemcpyDeviceToHost, c->stream));
@@ -91,7 +91,7 @@ void allreduce_sum_i64(oocgb_ctx c, long long *d_buf, size_t count) {
   OOCGB_NCCL(nccl_api().AllReduce(d_buf, d_buf, count, ncclInt64, ncclSum, c->comm, c->stream));
 }
 void allreduce_max_u64(oocgb_ctx c, unsigned long long *d_buf, size_t count) {
-  if (c->world <= 1 || count == 0) return;
+  if (!c->coll || count == 0) return;
   if (c->host_coll) {
     std::vector<unsigned long long> h(count);
     OOCGB_CK(cudaMemcpyAsync(h.data(), d_buf, 8 * count, cudaMemcpyDeviceToHost, c->stream));
@@ -350,10 +350,11 @@ int oocgb_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t 
     OOCGB_CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     OOCGB_CK(cudaMalloc(&c->d_small, 1 << 20));
     OOCGB_CK(cudaMallocHost(&c->h_small, 1 << 20));
-    if (world > 1) {
+    if (world > 1 || nccl_id) {  // world == 1 with an id: the multi-GPU path on a 1-rank communicator
       ncclUniqueId id;
       memcpy(&id, nccl_id, 128);
       OOCGB_NCCL(nccl_api().CommInitRank(&c->comm, world, id, rank));
+      c->coll = true;
     }
   } catch (...) {
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -379,6 +380,7 @@ int oocgb_ctx_create_hostcomm(int32_t device, int32_t rank, int32_t world, oocgb
   c->world = world;
   c->host_coll = fn;
   c->host_coll_user = user;
+  c->coll = world > 1;
   *out = c;
   API_END
 }

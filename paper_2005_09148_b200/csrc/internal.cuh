@@ -169,6 +169,7 @@ struct oocgb_ctx_s {
   bool own_stream = false;
   cudaStream_t copy_stream = nullptr;
   ncclComm_t comm = nullptr;
+  bool coll = false;  // collectives on: world > 1, or a 1-rank NCCL communicator (nccl_id given)
   oocgb_collective_fn host_coll = nullptr;  // test transport (oocgb_ctx_create_hostcomm)
   void *host_coll_user = nullptr;
   int live_data = 0;

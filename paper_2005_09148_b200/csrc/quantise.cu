@@ -209,7 +209,7 @@ void cuts_finalize(oocgb_data d) {
   uint32_t *rowmajor = d->d_sketch;
   int64_t N = (int64_t)n_local_sample;
   uint32_t *gathered = nullptr;
-  if (c->world > 1) {
+  if (c->coll) {
     // allgather the sketch sample: pad every rank to the max count with
     // 0xFFFFFFFF keys (sort after every finite key) and drop them after sorting.
     unsigned long long *d_cnt = (unsigned long long *)c->d_small;

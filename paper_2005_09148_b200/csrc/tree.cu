@@ -1415,7 +1415,7 @@ static void ensure_work(oocgb_data d, int D) {
   const size_t hsz = (size_t)m * kBins * 2;
   const int64_t pslots = D >= 2 ? (1LL << (D - 2)) : 1;
   for (int i = 0; i < 2; ++i) w->phist[i] = (long long *)dmalloc(sizeof(long long) * hsz * pslots);
-  if (c->world > 1 || d->streamed) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * 2 * max_pairs);
+  if (c->coll || d->streamed) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * 2 * max_pairs);
   w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)max_pairs * 2 * m);
   w->ent_cap = (int)(2 * max_pairs);
   w->ent = (int2 *)dmalloc(sizeof(int2) * 2 * w->ent_cap);
@@ -1487,7 +1487,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
                                                                  (lv == 0 && ridx_mode == 0) ? 1 : 0, 32);
     OOCGB_CK(cudaGetLastError());
     mark(0, false);
-    if (c->world > 1) {
+    if (c->coll) {
       int64_t tot = (int64_t)max_pairs * m * kBins;
       k_reduce_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
           w->partial, w->pairs, w->ctl, m, n_fg, w->built64);
@@ -1497,7 +1497,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     EvalArgs A;
     A.d = lv; A.D = D; A.m = m; A.n_fg = n_fg;
     A.pairs = w->pairs; A.ctl = w->ctl; A.partial = w->partial;
-    A.built64 = c->world > 1 ? w->built64 : nullptr;
+    A.built64 = c->coll ? w->built64 : nullptr;
     A.phist_prev = w->phist[(lv + 1) & 1];
     A.phist_next = w->phist[lv & 1];
     A.dbg = keep_debug ? w->dbg : nullptr;
@@ -1510,19 +1510,19 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     mark(2, true);
     PlanArgs PA;
     PA.segs = w->segs[cur]; PA.segs_next = w->segs[cur ^ 1]; PA.ctl = w->ctl; PA.dn = w->dnodes;
-    PA.cur = w->seg_cur[lv & 1]; PA.seg_cnt = c->world > 1 ? w->seg_cnt : nullptr;
+    PA.cur = w->seg_cur[lv & 1]; PA.seg_cnt = c->coll ? w->seg_cnt : nullptr;
     PA.cur_next = w->seg_cur[(lv + 1) & 1]; PA.pairs = w->pairs; PA.tile_seg = w->tile_seg;
     PA.chunk_pair = w->chunk_pair;
     PA.n = n; PA.n_fg = n_fg; PA.target_items = target; PA.kmax = kmax;
     PA.ent = w->ent; PA.ent_cap = w->ent_cap;
-    const bool inline_plan = c->world == 1 && n > 0;
+    const bool inline_plan = !c->coll && n > 0;
     if (n > 0) {
       k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
                                                           w->ridx[cur], w->q[cur], w->ridx[cur ^ 1], w->q[cur ^ 1],
                                                           w->seg_cur[lv & 1], w->tile_seg, inline_plan ? 1 : 0, PA);
       OOCGB_CK(cudaGetLastError());
     }
-    if (c->world > 1) {
+    if (c->coll) {
       const int len = 2 * (1 << lv);
       k_part_counts<<<(len + 255) / 256, 256, 0, c->stream>>>(w->seg_cur[lv & 1], w->ctl, len, w->seg_cnt);
       allreduce_sum_i64(c, w->seg_cnt, (size_t)len);
@@ -1793,7 +1793,7 @@ __global__ void k_stream_leaf_margin(const int32_t *__restrict__ row_node, int64
 oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma, double mcw, double eta,
                                bool keep_debug) {
   oocgb_ctx c = d->ctx;
-  OOCGB_REQUIRE(c->world == 1, OOCGB_ERR_ARG, "streamed build (Alg. 6) runs on one GPU in this version");
+  OOCGB_REQUIRE(!c->coll, OOCGB_ERR_ARG, "streamed build (Alg. 6) runs on one GPU in this version");
   OOCGB_REQUIRE(d->all_selected, OOCGB_ERR_STATE, "streamed build needs sample(NONE) (f = 1)");
   PhaseTimer whole(c, 6);
   ensure_work(d, D);
