@@ -919,6 +919,9 @@ struct PlanArgs {
   int ent_cap;
 };
 __device__ void plan_level(const PlanArgs &A, int n_segs);
+#ifdef OOCGB_PLAN_TRACE
+__device__ unsigned long long g_part_t0 = ~0ull;  // trace build only: first partition block's start
+#endif
 
 // One 2048-position tile per block; thread t handles positions t0 + 256 u + t (u < 8), so every
 // warp-wide load, gather and store touches consecutive positions (coalesced ridx / q, adjacent
@@ -931,6 +934,13 @@ k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
              int2 *__restrict__ q_out, int *__restrict__ cur, const int *__restrict__ tile_seg, int plan_inline,
              PlanArgs PA) {
   static_assert(kPartTile == 8 * kPartThreads, "8 positions per thread");
+#ifdef OOCGB_PLAN_TRACE
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&g_part_t0, t);
+  }
+#endif
   __shared__ TileSegs T;
   __shared__ int s_pre[8][kPartThreads / 32];  // (left | right << 16) per (u, warp), then exclusive prefix
   __shared__ int s_tot;
@@ -1072,8 +1082,21 @@ k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+#ifdef OOCGB_PLAN_TRACE
+  unsigned long long tp0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp0));
+#endif
   plan_level(PA, n_segs);
   if (threadIdx.x == 0) PA.ctl->part_done = 0;
+#ifdef OOCGB_PLAN_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tp1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1));
+    printf("PLANTRACE segs %d plan_ns %llu since_first_block_ns %llu\n", n_segs, tp1 - tp0, tp1 - g_part_t0);
+    g_part_t0 = ~0ull;
+  }
+#endif
 }
 
 // world > 1: the local (left, right) counts of the level's segments, widened for the all-reduce
