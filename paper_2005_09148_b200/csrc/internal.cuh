@@ -61,7 +61,14 @@ const NcclApi &nccl_api();
 // Tuning constants.
 constexpr int kFG = 32;              // features per histogram feature-group (one 32 B sector)
 constexpr int kBins = 256;           // uint8 symbols (R5, R7)
-constexpr int kHistThreads = 512;    // histogram CTA (2 per SM: 32 warps, measured best)
+#ifndef OOCGB_HIST_THREADS
+#define OOCGB_HIST_THREADS 512
+#define OOCGB_HIST_CTAS 2
+#define OOCGB_HIST_DEPTH 3
+#endif
+constexpr int kHistThreads = OOCGB_HIST_THREADS;  // histogram CTA (512 x 2 per SM: 32 warps, measured best)
+constexpr int kHistCtasPerSm = OOCGB_HIST_CTAS;
+constexpr int kHistDepth = OOCGB_HIST_DEPTH;      // k_hist's register pipeline depth (rows in flight per lane)
 constexpr int kHistSmem = 2 * kBins * kFG * 4;  // s32 [bin][g: 32 features | h: 32 features]
 constexpr int kPartTile = 2048;      // positions per partition tile
 constexpr int kPartThreads = 256;

@@ -26,6 +26,10 @@
 #include <climits>
 #include <cmath>
 
+#ifndef OOCGB_HIST_EXPERIMENT
+#define OOCGB_HIST_EXPERIMENT 0  // tools/microbench/hist_levels.cu only
+#endif
+
 // Per-call scalars read by the captured kernels (so one CUDA graph serves every round).
 struct RoundParams {
   long long G, H, n_rows_global;
@@ -189,7 +193,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
 // distinct banks (h picks the bank half, the rotation a bank inside it) -> conflict-free ATOMS.
 // Per symbol: one PRMT (bin * 256 straight from the packed word), one IADD3 (+ the lane's
 // precomputed feature offset and the shared base), two ATOMS.
-__global__ void __launch_bounds__(kHistThreads, 2)
+__global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
 k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
        const int2 *__restrict__ q, const Pair *__restrict__ pairs, LevelCtl *ctl,
        const int *__restrict__ chunk_pair, int *__restrict__ partial, int identity, int row_step) {
@@ -222,7 +226,9 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
     const int c = cg - P.chunk_base;
     const int r0 = P.begin + c * P.chunk_rows;
     const int r1 = min(P.begin + P.count, r0 + P.chunk_rows);
+#if !(OOCGB_HIST_EXPERIMENT & 4)  // microbenchmark: no zero fill
     for (int i = threadIdx.x; i < 2 * kBins * kFG / 4; i += kHistThreads) smem4[i] = make_int4(0, 0, 0, 0);
+#endif
     __syncthreads();
     const uint8_t *base = bins + (size_t)fg * pitch + half * 16;
     auto row_of = [&](int kk) -> int { return identity ? kk : __ldg(ridx + kk); };
@@ -247,15 +253,19 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
         const uint32_t a = __byte_perm(t[s >> 2], 0u, 0x4404u | ((uint32_t)(s & 3) << 4)) + f4[s];
+#if OOCGB_HIST_EXPERIMENT & 1  // microbenchmark: no accumulation (keeps the loads live)
+        if (a == 0xffffffffu) asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(qq.x));
+#else
         asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(qq.x));
         asm volatile("red.shared.add.s32 [%0+128], %1;" ::"r"(a), "r"(qq.y));
+#endif
       }
     };
     // Software pipeline over rows k, k + RT, k + 2RT, ...: kDepth register sets rotate (the loop
     // is unrolled by kDepth); a set is consumed (rotation + reductions) and only then refilled
     // with the row kDepth steps ahead, so no in-flight register is ever copied; the row id for
     // a refill is loaded one round earlier still.
-    constexpr int kDepth = 3;
+    constexpr int kDepth = kHistDepth;
     int k = r0 + (threadIdx.x >> 1);
     uint4 xs[kDepth];
     int2 qs[kDepth];
@@ -297,7 +307,11 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
       for (int i = 0; i < 32; i += 2) {
         const int i0 = (bb * 32 + i) * 64 + lane, i1 = i0 + 64;
         int4 v = make_int4(S[i0], S[i0 + 32], S[i1], S[i1 + 32]);
+#if OOCGB_HIST_EXPERIMENT & 2  // microbenchmark: no partial stores
+        if (f < m && v.x == 0x7fffffff) dst[i >> 1] = v;
+#else
         if (f < m) dst[i >> 1] = v;
+#endif
       }
     }
     __syncthreads();
@@ -1408,7 +1422,7 @@ static void ensure_work(oocgb_data d, int D) {
   const int n_fg = (m + kFG - 1) / kFG;
   const int64_t n = std::max<int64_t>(1, d->n_sel);
   const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
-  const int hist_grid = c->num_sms * 2;
+  const int hist_grid = c->num_sms * kHistCtasPerSm;
   const int target = hist_grid;
   const int64_t max_pairs = D > 0 ? (1LL << (D - 1)) : 1;
   // bound of hist_chunk_rows' item count: C <= n_pairs - 1 + ceil(rows / kmax) + ceil(grid / n_fg)
