@@ -26,6 +26,9 @@
 #include <climits>
 #include <cmath>
 
+#ifndef OOCGB_HIST_LOAD
+#define OOCGB_HIST_LOAD 1  // measured: -4% at the levels below the root (profiles/r01_microbench_hist_levels.txt)
+#endif
 #ifndef OOCGB_HIST_EXPERIMENT
 #define OOCGB_HIST_EXPERIMENT 0  // tools/microbench/hist_levels.cu only
 #endif
@@ -234,13 +237,24 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
     auto row_of = [&](int kk) -> int { return identity ? kk : __ldg(ridx + kk); };
     auto load_row = [&](int kk, int row, uint4 &x, int2 &qv) {
       if (kk < r1) {
+#if OOCGB_HIST_LOAD == 1  // streaming symbols: no L1 allocation
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(base + (size_t)row * row_step));
+#elif OOCGB_HIST_LOAD == 2  // + a 256-B L2 prefetch hint
+        asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "l"(base + (size_t)row * row_step));
+#else
         x = __ldg(reinterpret_cast<const uint4 *>(base + (size_t)row * row_step));
+#endif
         qv = __ldg(q + kk);
       }
     };
     // one row: rotate the lane's 16 symbols right by `rslot` bytes (byte s = feature
     // 16h + ((rslot + s) & 15)), then 16 x 2 conflict-free shared reductions.  PRMT moves byte
     // (s & 3) of a word to bits 8..15 with zeros elsewhere = bin * 256 (the bin's 256-B line).
+#if OOCGB_HIST_EXPERIMENT & 1
+    uint32_t xacc = 0;
+#endif
     auto accumulate = [&](const uint4 &x, const int2 qq) {
       uint32_t w[4] = {x.x, x.y, x.z, x.w};
       uint32_t t[4];
@@ -253,8 +267,8 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
         const uint32_t a = __byte_perm(t[s >> 2], 0u, 0x4404u | ((uint32_t)(s & 3) << 4)) + f4[s];
-#if OOCGB_HIST_EXPERIMENT & 1  // microbenchmark: no accumulation (keeps the loads live)
-        if (a == 0xffffffffu) asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(qq.x));
+#if OOCGB_HIST_EXPERIMENT & 1  // microbenchmark: no shared atomics (one register XOR keeps the data live)
+        xacc ^= a + (uint32_t)qq.x;
 #else
         asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(qq.x));
         asm volatile("red.shared.add.s32 [%0+128], %1;" ::"r"(a), "r"(qq.y));
@@ -297,6 +311,9 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
       }
       k += kDepth * RT;
     }
+#if OOCGB_HIST_EXPERIMENT & 1
+    if (xacc == 0x9e3779b9u) S[threadIdx.x] = (int)xacc;  // keep the experiment's data live
+#endif
     __syncthreads();
     // flush: warp w owns bins [32w, 32w+32); lane l = feature l -> conflict-free reads; each lane
     // writes its feature's 32 (g, h) pairs = 256 contiguous bytes of the [32][256][2] partial.
