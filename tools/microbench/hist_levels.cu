@@ -144,6 +144,7 @@ int main(int argc, char **argv) {
                                                partial, L.identity ? 1 : 0, 32);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
+      if (cudaGetLastError() != cudaSuccess) { printf("launch failed: %s\n", L.name); return 1; }
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       if (it >= 3) best = std::min(best, ms);
