@@ -157,6 +157,17 @@ def hist_algorithmic_bytes(nodes: np.ndarray, m: int) -> float:
     return rows * (m + 8 + 4) + built * m * 256 * 16.0
 
 
+def part_algorithmic_bytes(nodes: np.ndarray) -> float:
+    """DESIGN.md §5 partition: per row of a split node and level, 4 B (row id) + 1 B (the split
+    feature's symbol) + 8 B (q) read and 12 B written."""
+    D = int(np.log2(len(nodes) + 1)) - 1
+    rows = 0
+    for v in range((1 << D) - 1):
+        if nodes["feature"][v] >= 0:
+            rows += int(nodes["n_rows"][v])
+    return rows * 25.0
+
+
 def measured_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per k_hist launch from the committed ncu
     --set full capture (profiles/k_hist_traffic.json), or None."""
@@ -533,6 +544,7 @@ def main():
     tm = ctx.get_timings()
     ctx.set_profiling(False)
     hist_bytes = sum(hist_algorithmic_bytes(nd, N_FEAT) for nd in exported)
+    part_bytes = sum(part_algorithmic_bytes(nd) for nd in exported)
     hist_rowfeat = sum(hist_rows(nd)[0] * N_FEAT for nd in exported)
     hist_ms = tm["hist_ms"]
     n_hist = max(1, int(tm["hist_launches"]))
@@ -599,6 +611,10 @@ def main():
             "histogram": {"row_features_per_s": hist_rowfeat / (hist_ms * 1e-3), "ms_per_round": hist_ms / args.steps,
                           "launches": n_hist, "algorithmic_bytes_per_round": hist_bytes / args.steps},
             "phases_ms_per_round": {k: v / args.steps for k, v in tm.items() if k.endswith("_ms")},
+            "partition": {"ms_per_round": tm["partition_ms"] / args.steps,
+                          "algorithmic_bytes_per_round": part_bytes / args.steps,
+                          "GB_per_s": part_bytes / (tm["partition_ms"] * 1e-3) / 1e9,
+                          "frac_of_hbm": part_bytes / (tm["partition_ms"] * 1e-3) / 1e9 / peak},
             "profiled_ms_per_step": ms_prof / args.steps,  # region B (event nodes in the graph)
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": measured_traffic(), "kernel": "k_hist",
