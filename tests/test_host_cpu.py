@@ -137,3 +137,62 @@ def test_bench_reference_arm_under_torchrun_rank1_exits_clean():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                         "--warmup", "0"], env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+PLANNER_CHECK = r'''
+#include "paper_2005_09148_b200/csrc/internal.cuh"
+#include <cstdio>
+#include <random>
+#include <vector>
+// hist_chunk_rows (the histogram chunk planner of the root level and the streamed batches):
+// chunks never exceed kmax rows (the s32 exactness bound), hold every pair, and fill at most
+// the fewest whole waves of the k_hist grid that can hold the level.
+int main() {
+  std::mt19937_64 g(5);
+  int bad = 0;
+  for (int it = 0; it < 20000; ++it) {
+    const int n_fg = 1 + (int)(g() % 32), grid = 148 * (1 + (int)(g() % 3));
+    const long long kmax = 0x7fffffffLL >> (10 + (int)(g() % 12));
+    const int n_pairs = 1 + (int)(g() % 300);
+    std::vector<long long> c(n_pairs);
+    long long tot = 0;
+    for (auto &x : c) { x = (long long)(g() % (1 + (g() % 2 ? 4000 : 400000))); tot += x; }
+    const long long cr = oocgb::hist_chunk_rows(tot, n_pairs, n_fg, grid, kmax);
+    long long chunks = 0;
+    for (auto x : c) chunks += (x + cr - 1) / cr;
+    const long long lo = kmax < 1024 ? kmax : 1024;
+    // the wave count the planner picked: the smallest w whose budget C admits cr
+    long long C = 0;
+    for (long long w = 1;; ++w) {
+      C = w * grid / n_fg;
+      if (C < n_pairs || C < 1) continue;
+      const long long t = (tot + (C - n_pairs + 1) - 1) / (C - n_pairs + 1);
+      if (t <= kmax) break;
+    }
+    if (cr > kmax || cr < lo || chunks > C) {
+      if (bad++ < 5) printf("bad: tot %lld pairs %d n_fg %d grid %d kmax %lld -> cr %lld chunks %lld C %lld\n", tot,
+                            n_pairs, n_fg, grid, kmax, cr, chunks, C);
+    }
+  }
+  printf("%s\n", bad ? "FAIL" : "OK");
+  return bad ? 1 : 0;
+}
+'''
+
+
+def test_hist_chunk_planner_invariants(tmp_path):
+    """The chunk planner (internal.cuh hist_chunk_rows, DESIGN.md §5 item scheduling), compiled for
+    the host: chunk rows within [min(1024, kmax), kmax] (s32 exactness of the partials, R12) and the
+    chunk count within the chosen number of whole waves, over random levels."""
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc):
+        pytest.skip("nvcc not available")
+    src = tmp_path / "planner.cu"
+    src.write_text(PLANNER_CHECK)
+    exe = tmp_path / "planner"
+    subprocess.check_call([nvcc, "-std=c++17", "-O1", "-I", ROOT, "-o", str(exe), str(src)],
+                          stdout=subprocess.DEVNULL, stderr=subprocess.STDOUT)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip().endswith("OK"), out.stdout
