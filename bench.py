@@ -180,8 +180,9 @@ def measured_traffic():
 
 def launches_per_round(D: int) -> int:
     # update_margin 1 + logistic 1 + sample(NONE): sstate_init, absmax2, sstate_globalise, quantise 4
-    # build_tree: init 1 + per level (k_hist, k_eval, k_finalize, k_part_fused) 4
-    return 6 + 1 + 4 * D
+    # build_tree: init 1 + per level (k_hist, k_eval, k_eval_narrow, k_finalize, k_part_fused) 5
+    # (matches the ncu launch list, profiles/r01_launches_summary.txt: 47 per depth-8 round)
+    return 6 + 1 + 5 * D
 
 
 def make_data(rows, rank):
