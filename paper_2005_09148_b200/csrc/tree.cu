@@ -26,6 +26,9 @@
 #include <climits>
 #include <cmath>
 
+#ifndef OOCGB_EVAL_FOLD
+#define OOCGB_EVAL_FOLD 1
+#endif
 #ifndef OOCGB_HIST_LOAD
 #define OOCGB_HIST_LOAD 1  // measured: -4% at the levels below the root (profiles/r01_microbench_hist_levels.txt)
 #endif
@@ -161,7 +164,9 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
     const long long t1 = clamp_ll(ceil(ldexp(mcw, ss->e_h)));
     const long long t2 = clamp_ll(floor(ldexp(-lambda, ss->e_h))) + 1;
     P.h_min = t1 > t2 ? t1 : t2;
-    P.prefilter = (abs(ss->e_g) <= 60 && abs(ss->e_h) <= 60) ? 1 : 0;
+    // float pre-filter only where every scale is a normal float: 2^-e_g, 2^-e_h, and the folded
+    // c = 2^(e_h - 2 e_g), lambda 2^e_h
+    P.prefilter = (abs(ss->e_g) <= 60 && abs(ss->e_h) <= 60 && abs(ss->e_h - 2 * ss->e_g) <= 100) ? 1 : 0;
     *rp = P;
     DNode r{};
     r.feature = -1;
@@ -465,6 +470,30 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
   unsigned vmask = 0;
   I GL = eg, HL = eh;
   float Lmax = -INFINITY;
+#if OOCGB_EVAL_FOLD
+  // Folded scales, branch-free: with sg = 2^-e_g, sh = 2^-e_h (exact powers of two) the float
+  // terms are tL = c GL^2 / (HL + lq) with c = sg^2 / sh and lq = lambda / sh, the same values up
+  // to rounding order as the unfolded form below; the gain and its bound scale by c exactly
+  // (the pre-filter is on only when c and lq are normal floats, see k_init_build).
+  const float c = rp.sg_inv_f * rp.sg_inv_f / rp.sh_inv_f, lq = lamf / rp.sh_inv_f;
+  const float chalf = 0.5f * c, tolc = 0x1p-18f * c, K = 0.5f * tPf + gamf;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    GL += g[i];
+    HL += h[i];
+    const int b = lane * 8 + i;
+    // an empty bin repeats the previous candidate exactly, which wins the tie (lower bin)
+    const bool v = b <= B - 2 && ((g[i] | h[i]) != 0 || b == 0) && HL >= hmin && HL <= hmax;
+    const float GLf = (float)GL, HLf = (float)HL, GRf = (float)(G - GL), HRf = (float)(H - HL);
+    const float T = __fdividef(GLf * GLf, HLf + lq) + __fdividef(GRf * GRf, HRf + lq);
+    const float gain = chalf * T - K;
+    const float tol = tolc * T + tol0;  // NaN / inf when a term is not finite
+    const bool fin = tol < INFINITY;
+    vmask |= v ? 1u << i : 0u;
+    ub[i] = v ? (fin ? gain + tol : INFINITY) : -INFINITY;
+    Lmax = fmaxf(Lmax, (v && fin) ? gain - tol : -INFINITY);
+  }
+#else
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     GL += g[i];
@@ -490,6 +519,7 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
       }
     }
   }
+#endif
 #pragma unroll
   for (int o = 16; o; o >>= 1) Lmax = fmaxf(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, o));
   // pass 2: exact double gains of the survivors
