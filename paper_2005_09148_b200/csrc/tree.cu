@@ -1,8 +1,9 @@
 // Tree construction (Alg. 1) for sm_100a, depth-wise (R16):
 //   per level d:  k_hist (BuildHistograms, L174-175)      -> s32 partial histograms
 //                 [multi-GPU: k_reduce_partials + ncclAllReduce(int64), P:L188-190]
-//                 k_eval  (EvaluateSplit, L176-178; Eq. 8) -> per-(node, feature) best split,
-//                          sibling = parent - built (R17), parents kept for the next level
+//                 k_eval, k_eval_narrow (EvaluateSplit, L176-178; Eq. 8) -> per-(node, feature)
+//                          best split over the plan's int64 / int32 work lists, sibling =
+//                          parent - built (R17), parents kept for the next level
 //                 k_finalize (node decision: argmax over features,
 //                          Eq. 6 leaf values, R13-R15)
 //                 k_part_fused / k_part_plan (RepartitionInstances, L172-173):
