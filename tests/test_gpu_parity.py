@@ -174,13 +174,18 @@ TREE_CASES = [
     (20000, 70, 256, 5, 2, 0.1, False),
     (4096, 8, 256, 0, 0, 1.0, False),
     (5000, 10, 256, 10, 0, 1.0, False),
+    # > 256 segments at the deepest levels (the block-strided plan) with int64 (> kmax rows) nodes
+    # at the top and int32 ones below: both evaluation lists and the general plan path
+    (60000, 12, 256, 10, 0, 1.0, False),
+    (40000, 16, 256, 11, 2, 0.5, True),
+    (70000, 8, 256, 11, 0, 1.0, "noise"),   # > 256 segments: the block-strided plan
 ]
 
 
 @pytest.mark.parametrize("n,m,max_bin,depth,mode,ratio,stress", TREE_CASES)
 def test_tree_bit_exact(ctx, n, m, max_bin, depth, mode, ratio, stress):
     if n >= 50:
-        X, y = synth.make_classification(n, max(m, 2), seed=7 + n, stress=stress and m >= 4)
+        X, y = synth.make_classification(n, max(m, 2), seed=7 + n, stress=stress is True and m >= 4)
         X = np.ascontiguousarray(X[:, :m])
     else:
         rng = np.random.default_rng(n)
@@ -189,6 +194,10 @@ def test_tree_bit_exact(ctx, n, m, max_bin, depth, mode, ratio, stress):
     cv, cp, B = _oracle_cuts_bins(X, max_bin)
     margin = np.random.default_rng(n).normal(scale=0.5, size=n).astype(np.float32)
     g, h = oracle.logistic_grad(margin, y)
+    if stress == "noise":  # random gradient pairs: noise splits everywhere, hundreds of segments
+        rng = np.random.default_rng(n + 1)
+        g = rng.uniform(-1.0, 1.0, n).astype(np.float32)
+        h = rng.uniform(0.05, 1.0, n).astype(np.float32)
     on, olor, ohist, sel = _oracle_tree(B, m, cv, cp, g, h, mode, ratio, depth)
     d = ctx.quantise(X, max_bin)
     d.set_gradients(g, h)
