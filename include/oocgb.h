@@ -155,7 +155,7 @@ int oocgb_set_logistic_gradients(oocgb_data data, const float *margin, const flo
  * MVS (Eq. 9, capped PPS with an exact integer threshold, g' = g/p, h' = h/p).  Random draws
  * are Philox4x64-10 keyed (seed, round) with counter (global_row, 0, 0, 0) (R24), so the
  * sample is independent of world size and page size.  Then fixed point (R12):
- * q = rint(x 2^e), e = quant_bits - k with frexp(max|x|) = (., k); quant_bits in [8, 25].
+ * q = rint(x 2^e), e = quant_bits - k with frexp(max|x|) = (., k); quant_bits in [8, 20] (R12: non-returning s32 shared atomics need chunk_rows * 2^quant_bits < 2^31).
  * For PINNED_HOST data this also compacts the selected rows of every page into one device
  * page (Alg. 7).  ERR_ARG: ratio not in (0, 1], bad mode/quant_bits; ERR_STATE:
  * no gradients; ERR_NOMEM: sampled page does not fit (lower ratio).  info may be NULL: then

@@ -348,6 +348,10 @@ int oocgb_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t 
       c->own_stream = true;
     }
     OOCGB_CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 3; ++i) {
+      OOCGB_CK(cudaEventCreateWithFlags(&c->pipe_copy_done[i], cudaEventDisableTiming));
+      OOCGB_CK(cudaEventCreateWithFlags(&c->pipe_consumed[i], cudaEventDisableTiming));
+    }
     OOCGB_CK(cudaMalloc(&c->d_small, 1 << 20));
     OOCGB_CK(cudaMallocHost(&c->h_small, 1 << 20));
     if (world > 1 || nccl_id) {  // world == 1 with an id: the multi-GPU path on a 1-rank communicator
@@ -359,6 +363,10 @@ int oocgb_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t 
   } catch (...) {
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (int i = 0; i < 3; ++i) {
+      if (c->pipe_copy_done[i]) cudaEventDestroy(c->pipe_copy_done[i]);
+      if (c->pipe_consumed[i]) cudaEventDestroy(c->pipe_consumed[i]);
+    }
     if (c->d_small) cudaFree(c->d_small);
     if (c->h_small) cudaFreeHost(c->h_small);
     delete c;
@@ -389,7 +397,12 @@ int oocgb_ctx_destroy(oocgb_ctx c) {
   API_BEGIN
   OOCGB_REQUIRE(c, OOCGB_ERR_ARG, "ctx is NULL");
   OOCGB_REQUIRE(c->live_data == 0, OOCGB_ERR_STATE, "ctx_destroy: data handles are still alive");
+  OOCGB_REQUIRE(c->live_trees == 0, OOCGB_ERR_STATE, "ctx_destroy: tree handles are still alive");
   bind(c);
+  for (int i = 0; i < 3; ++i) {
+    if (c->pipe_copy_done[i]) cudaEventDestroy(c->pipe_copy_done[i]);
+    if (c->pipe_consumed[i]) cudaEventDestroy(c->pipe_consumed[i]);
+  }
   cudaStreamSynchronize(c->stream);
   if (c->comm) nccl_api().CommDestroy(c->comm);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -588,6 +601,7 @@ int oocgb_sample(oocgb_data d, int32_t mode, double ratio, double mvs_lambda, ui
   OOCGB_REQUIRE(d->cuts_ready && d->rows_written == d->n_local, OOCGB_ERR_STATE, "sample: pages not complete");
   OOCGB_REQUIRE(d->has_grad, OOCGB_ERR_STATE, "sample before set_gradients");
   bind(d->ctx);
+  d->sample_serial++;
   sample_rows(d, mode, ratio, mvs_lambda, seed, round, quant_bits, info);
   API_END
 }
@@ -603,6 +617,7 @@ int oocgb_sample_goss(oocgb_data d, double a, double b, uint64_t seed, uint64_t 
   OOCGB_REQUIRE(d->cuts_ready && d->rows_written == d->n_local, OOCGB_ERR_STATE, "sample: pages not complete");
   OOCGB_REQUIRE(d->has_grad, OOCGB_ERR_STATE, "sample before set_gradients");
   bind(d->ctx);
+  d->sample_serial++;
   sample_rows(d, OOCGB_SAMPLE_GOSS, a, 0.0, seed, round, quant_bits, info, b);
   API_END
 }
@@ -614,6 +629,7 @@ int oocgb_set_streaming(oocgb_data d, int32_t enable) {
                 "streamed build needs PINNED_HOST pages");
   d->streamed = enable != 0;
   d->has_sample = false;
+  d->sample_serial++;
   API_END
 }
 
@@ -650,6 +666,7 @@ int oocgb_tree_destroy(oocgb_tree t) {
   OOCGB_REQUIRE(t, OOCGB_ERR_ARG, "tree is NULL");
   // stream-ordered reuse: later users of the buffer run after every kernel already enqueued
   pool_put(t->ctx, t->pnodes_bytes, t->d_pnodes);
+  t->ctx->live_trees--;
   delete t;
   API_END
 }

@@ -180,6 +180,9 @@ struct oocgb_ctx_s {
   oocgb_collective_fn host_coll = nullptr;  // test transport (oocgb_ctx_create_hostcomm)
   void *host_coll_user = nullptr;
   int live_data = 0;
+  int live_trees = 0;
+  // page-pipeline events (stream.cuh), created with the ctx on its device
+  cudaEvent_t pipe_copy_done[3] = {}, pipe_consumed[3] = {};
   int num_sms = 148;
   bool profiling = false;
   double timings[16] = {0};
@@ -242,6 +245,7 @@ struct oocgb_data_s {
   // tree workspace (lazy, sized for (n_sel cap, depth))
   struct Work *work = nullptr;
   uint64_t tree_serial = 0;
+  uint64_t sample_serial = 0;   // bumped by every sample / set_streaming: trees remember theirs
   // Alg. 6 streamed build (f = 1, PINNED_HOST): trees are built by level-batched passes over the
   // pinned pages instead of copying every page into HBM
   bool streamed = false;
@@ -262,6 +266,7 @@ struct oocgb_tree_s {
   oocgb_ctx ctx = nullptr;
   size_t pnodes_bytes = 0;
   uint64_t serial = 0;
+  uint64_t sample_serial = 0;        // the data's sample this tree was built from
   int32_t max_depth = 0;
   std::vector<oocgb_node> nodes;
   oocgb::PNode *d_pnodes = nullptr;  // device copy for predict

@@ -198,6 +198,31 @@ void sketch_append(oocgb_data d, const float *dX, int64_t row0_global, int64_t n
   OOCGB_REQUIRE(herr != 3, OOCGB_ERR_NOMEM, "quantise: sketch sample exceeded its capacity");
 }
 
+// Per-feature sort of column-major keys [m][N] (CUB segmented radix sort).  CUB takes 32-bit
+// item counts and segment offsets, so the features go in batches of at most (2^31 - 1) / N
+// columns (offsets relative to the batch), which keeps N * m >= 2^31 inputs exact.
+static void sort_columns(oocgb_ctx c, const uint32_t *colmajor, uint32_t *sorted, int64_t N, int m) {
+  if (N <= 0 || m <= 0) return;
+  OOCGB_REQUIRE(N <= 0x7fffffffLL, OOCGB_ERR_ARG, "cuts: sketch sample above 2^31 rows");
+  const int fb = (int)std::max<int64_t>(1, std::min<int64_t>(m, 0x7fffffffLL / N));
+  std::vector<int> offs(fb + 1);
+  for (int j = 0; j <= fb; ++j) offs[j] = (int)(j * N);
+  int *d_offs = (int *)dmalloc(sizeof(int) * (fb + 1));
+  OOCGB_CK(cudaMemcpyAsync(d_offs, offs.data(), sizeof(int) * (fb + 1), cudaMemcpyHostToDevice, c->stream));
+  size_t tmp = 0;
+  OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, colmajor, sorted, (int)(N * fb), fb, d_offs,
+                                                   d_offs + 1, 0, 32, c->stream));
+  void *d_tmp = dmalloc(std::max<size_t>(tmp, 16));
+  for (int j0 = 0; j0 < m; j0 += fb) {
+    const int nf = std::min(fb, m - j0);
+    OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tmp, colmajor + (size_t)j0 * N, sorted + (size_t)j0 * N,
+                                                     (int)(N * nf), nf, d_offs, d_offs + 1, 0, 32, c->stream));
+  }
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  dfree(d_tmp);
+  dfree(d_offs);
+}
+
 void cuts_finalize(oocgb_data d) {
   oocgb_ctx c = d->ctx;
   if (!d->d_sketch) sketch_append(d, nullptr, 0, 0);
@@ -243,17 +268,7 @@ void cuts_finalize(oocgb_data d) {
     dfree(gathered);
     // sort per feature, then extract with the true count (padding keys sit at the end)
     uint32_t *sorted = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, N) * m);
-    std::vector<int> offs(m + 1);
-    for (int j = 0; j <= m; ++j) offs[j] = (int)(j * N);
-    int *d_offs = (int *)dmalloc(sizeof(int) * (m + 1));
-    OOCGB_CK(cudaMemcpyAsync(d_offs, offs.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice, c->stream));
-    size_t tmp = 0;
-    OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, colmajor, sorted, (int)(N * m), m,
-                                                     d_offs, d_offs + 1, 0, 32, c->stream));
-    void *d_tmp = dmalloc(std::max<size_t>(tmp, 16));
-    OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tmp, colmajor, sorted, (int)(N * m), m,
-                                                     d_offs, d_offs + 1, 0, 32, c->stream));
-    dfree(d_tmp);
+    sort_columns(c, colmajor, sorted, N, m);
     dfree(colmajor);
     // compact each feature's first Ntrue keys into [m][Ntrue]
     uint32_t *trimmed = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, Ntrue) * m);
@@ -261,7 +276,6 @@ void cuts_finalize(oocgb_data d) {
       OOCGB_CK(cudaMemcpyAsync(trimmed + (int64_t)j * Ntrue, sorted + (int64_t)j * N,
                                sizeof(uint32_t) * (size_t)Ntrue, cudaMemcpyDeviceToDevice, c->stream));
     dfree(sorted);
-    dfree(d_offs);
     rowmajor = nullptr;
     N = Ntrue;
     // fall through to extraction with `trimmed` as the sorted column-major keys
@@ -287,22 +301,8 @@ void cuts_finalize(oocgb_data d) {
     if (N > 0) k_transpose_keys<<<tg, tb, 0, c->stream>>>(rowmajor, N, m, colmajor);
     OOCGB_CK(cudaGetLastError());
     uint32_t *sorted = (uint32_t *)dmalloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(1, N) * m);
-    std::vector<int> offs(m + 1);
-    for (int j = 0; j <= m; ++j) offs[j] = (int)(j * N);
-    int *d_offs = (int *)dmalloc(sizeof(int) * (m + 1));
-    OOCGB_CK(cudaMemcpyAsync(d_offs, offs.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice, c->stream));
-    if (N > 0) {
-      size_t tmp = 0;
-      OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, colmajor, sorted, (int)(N * m), m,
-                                                       d_offs, d_offs + 1, 0, 32, c->stream));
-      void *d_tmp = dmalloc(std::max<size_t>(tmp, 16));
-      OOCGB_CK(cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tmp, colmajor, sorted, (int)(N * m), m,
-                                                       d_offs, d_offs + 1, 0, 32, c->stream));
-      OOCGB_CK(cudaStreamSynchronize(c->stream));
-      dfree(d_tmp);
-    }
+    sort_columns(c, colmajor, sorted, N, m);
     dfree(colmajor);
-    dfree(d_offs);
     float *d_cuts = (float *)dmalloc(sizeof(float) * (size_t)m * 256);
     int *d_cnt2 = (int *)dmalloc(sizeof(int) * m);
     k_extract_cuts<<<m, 256, 0, c->stream>>>(sorted, N, d->max_bin, d_cuts, d_cnt2);

@@ -19,15 +19,7 @@ template <class F>
 void for_each_page(oocgb_data d, F fn) {
   oocgb_ctx c = d->ctx;
   ensure_staging(d);
-  static thread_local cudaEvent_t copy_done[kStages] = {}, consumed[kStages] = {};
-  static thread_local int inited = 0;
-  if (!inited) {
-    for (int i = 0; i < kStages; ++i) {
-      OOCGB_CK(cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming));
-      OOCGB_CK(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
-    }
-    inited = 1;
-  }
+  cudaEvent_t *copy_done = c->pipe_copy_done, *consumed = c->pipe_consumed;  // per ctx (its device)
   // the copy stream must not overwrite staging still used by earlier work on the ctx stream
   OOCGB_CK(cudaEventRecord(consumed[0], c->stream));
   for (int i = 0; i < kStages; ++i) OOCGB_CK(cudaStreamWaitEvent(c->copy_stream, consumed[0], 0));
@@ -63,15 +55,7 @@ void for_each_batch(oocgb_data d, int64_t rows, F fn) {
     }
     d->stream_batch_rows = rows;
   }
-  static thread_local cudaEvent_t copy_done[kStages] = {}, consumed[kStages] = {};
-  static thread_local int inited = 0;
-  if (!inited) {
-    for (int i = 0; i < kStages; ++i) {
-      OOCGB_CK(cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming));
-      OOCGB_CK(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
-    }
-    inited = 1;
-  }
+  cudaEvent_t *copy_done = c->pipe_copy_done, *consumed = c->pipe_consumed;  // per ctx (its device)
   for (int i = 0; i < kStages; ++i) OOCGB_CK(cudaEventRecord(consumed[i], c->stream));
   const int64_t nb = (d->n_local + rows - 1) / rows;
   for (int64_t b = 0; b < nb; ++b) {

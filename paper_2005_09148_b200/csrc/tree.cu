@@ -1475,7 +1475,9 @@ static void ensure_work(oocgb_data d, int D) {
   const int64_t max_pairs = D > 0 ? (1LL << (D - 1)) : 1;
   // bound of hist_chunk_rows' item count: C <= n_pairs - 1 + ceil(rows / kmax) + ceil(grid / n_fg)
   int64_t items = target + (int64_t)n_fg * (((n + kmax - 1) / kmax) + max_pairs + 2) + n_fg;
-  if (w && w->cap_rows >= n && w->max_depth >= D && w->m == m && w->items_cap >= items) return;
+  const bool need64 = c->coll || d->streamed;  // all-reduced / streamed int64 node histograms
+  if (w && w->cap_rows >= n && w->max_depth >= D && w->m == m && w->items_cap >= items && (!need64 || w->built64))
+    return;
   free_work(d);
   w = new Work();
   w->cap_rows = n;
@@ -1500,7 +1502,7 @@ static void ensure_work(oocgb_data d, int D) {
   const size_t hsz = (size_t)m * kBins * 2;
   const int64_t pslots = D >= 2 ? (1LL << (D - 2)) : 1;
   for (int i = 0; i < 2; ++i) w->phist[i] = (long long *)dmalloc(sizeof(long long) * hsz * pslots);
-  if (c->coll || d->streamed) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * 2 * max_pairs);
+  if (need64) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * 2 * max_pairs);
   w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)max_pairs * 2 * m);
   w->ent_cap = (int)(2 * max_pairs);
   w->ent = (int2 *)dmalloc(sizeof(int2) * 2 * w->ent_cap);
@@ -1700,6 +1702,8 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   oocgb_tree t = new oocgb_tree_s();
   t->owner = d;
   t->serial = ++d->tree_serial;
+  t->sample_serial = d->sample_serial;
+  c->live_trees++;
   t->max_depth = D;
   t->nodes.resize(n_nodes);
   std::vector<PNode> pn(n_nodes);
@@ -1969,6 +1973,8 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   oocgb_tree t = new oocgb_tree_s();
   t->owner = d;
   t->serial = ++d->tree_serial;
+  t->sample_serial = d->sample_serial;
+  c->live_trees++;
   t->max_depth = D;
   t->nodes.resize(n_nodes);
   std::vector<PNode> pn(n_nodes);
@@ -2016,13 +2022,16 @@ void update_margin(oocgb_data d, oocgb_tree t, float *d_margin) {
   oocgb_ctx c = d->ctx;
   Work *w = d->work;
   if (d->streamed && d->placement == OOCGB_PLACE_PINNED_HOST) {
-    OOCGB_REQUIRE(w && t->serial == d->tree_serial && d->all_selected && d->streamed_row_node, OOCGB_ERR_STATE,
+    OOCGB_REQUIRE(w && t->serial == d->tree_serial && t->sample_serial == d->sample_serial && d->all_selected &&
+                      d->streamed_row_node,
+                  OOCGB_ERR_STATE,
                   "update_margin: needs the latest tree of an f = 1 sample");
     k_stream_leaf_margin<<<c->num_sms * 8, 256, 0, c->stream>>>(d->streamed_row_node, d->n_local, w->dnodes, d_margin);
     OOCGB_CK(cudaGetLastError());
     return;
   }
-  OOCGB_REQUIRE(w && t->serial == d->tree_serial && d->all_selected && d->placement == OOCGB_PLACE_DEVICE,
+  OOCGB_REQUIRE(w && t->serial == d->tree_serial && t->sample_serial == d->sample_serial && d->all_selected &&
+                    !d->streamed && d->placement == OOCGB_PLACE_DEVICE,
                 OOCGB_ERR_STATE, "update_margin: needs the latest tree of an in-core, f = 1 sample");
   const int n = (int)d->n_sel;
   if (n > 0)

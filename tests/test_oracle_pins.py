@@ -85,6 +85,33 @@ def test_cuts_rank_accuracy(B):
         assert c[-1] == col[-1]
 
 
+@pytest.mark.parametrize("N,B,tie_frac", [(1003, 16, 0.5), (777, 256, 0.5), (5000, 7, 0.7), (4099, 256, 0.6)])
+def test_cuts_ceil_rank_with_ties_equals_np_sort(N, B, tie_frac):
+    """O1 step 4 / R1 exactly, from np.sort: with more than B distinct values the cuts are
+    v[ceil(b N / B)] (1-based, b = 1..B) of the sorted column with repeats dropped, and the last
+    cut is the column max.  N is not a multiple of B and a large share of the values are tied, so a
+    floor-rank, an off-by-one index or kept repeats all change the result (checked below)."""
+    rng = np.random.default_rng(N + B)
+    n_tie = int(N * tie_frac)
+    ties = rng.choice(np.array([-1.5, 0.25, 3.0, 7.75], np.float32), size=n_tie)
+    cont = rng.normal(size=N - n_tie).astype(np.float32) * 4 + 1.0
+    col = np.concatenate([ties, cont])
+    rng.shuffle(col)
+    X = col[:, None]
+    assert len(np.unique(col)) > B
+    cv, cp = oracle.cuts(X, B)
+    v = np.sort(col)
+    b = np.arange(1, B + 1)
+    ceil_idx = (b * N + B - 1) // B          # 1-based ceil(b N / B)
+    expect = np.unique(v[ceil_idx - 1])      # sorted -> unique = drop repeats, keep increasing
+    np.testing.assert_array_equal(cv[cp[0]:cp[1]], expect)
+    assert cv[cp[1] - 1] == v[-1]
+    # the fixture discriminates the plausible mistakes
+    floor_idx = np.maximum(1, (b * N) // B)
+    assert not np.array_equal(np.unique(v[floor_idx - 1]), expect) or not np.array_equal(v[ceil_idx - 1], expect)
+    assert len(v[ceil_idx - 1]) != len(expect)  # repeats really were dropped
+
+
 def test_cuts_negative_zero_canonical():
     X = np.array([[-0.0], [0.0], [1.0]], np.float32)
     cv, cp = oracle.cuts(X, 256)
@@ -409,19 +436,25 @@ def test_leaf_weight_worked_example():
     assert nodes["sum_g"][0] == -4.0 and nodes["sum_h"][0] == 2.0
 
 
-def test_objective_identity():
-    """Eq.7(parent) - Eq.7(children) = gain + gamma, for the chosen split."""
-    rng = np.random.default_rng(4)
-    g = rng.normal(size=64)
+@pytest.mark.parametrize("seed", [4, 5, 6])
+def test_objective_identity(seed):
+    """Eq. 7 -> Eq. 8: Eq. 7 of the one-leaf tree minus Eq. 7 of the split
+    tree (gamma T included) equals the chosen split's gain.  The fixture
+    always splits: bin 0 carries g ~ -2, bin 1 carries g ~ +1.5, so the only candidate has a gain
+    far above gamma (a skipped draw would pin nothing)."""
+    rng = np.random.default_rng(seed)
+    bins_ = np.arange(64) % 2
+    g = np.where(bins_ == 0, -2.0, 1.5) + rng.normal(scale=0.1, size=64)
     h = rng.uniform(0.1, 1, size=64)
-    bins_ = rng.integers(0, 2, size=64)
     nodes, _, _ = _two_bin_tree(g, h, bins_, lam=1.0, gamma=0.3, mcw=0.0)
-    if nodes["feature"][0] < 0:
-        pytest.skip("no split on this draw")
-    obj = lambda G, H: -0.5 * G * G / (H + 1.0)
-    lhs = obj(nodes["sum_g"][0], nodes["sum_h"][0]) - obj(nodes["sum_g"][1], nodes["sum_h"][1]) - obj(
-        nodes["sum_g"][2], nodes["sum_h"][2])
-    assert abs(-lhs - (nodes["gain"][0] + 0.3)) < 1e-12
+    assert nodes["feature"][0] == 0 and nodes["split_bin"][0] == 0
+    # Eq. 7 (P:L136-139) of a whole tree: -1/2 sum_leaves G^2 / (H + lambda) + gamma T
+    eq7 = lambda leaves: sum(-0.5 * G * G / (H + 1.0) for G, H in leaves) + 0.3 * len(leaves)
+    before = eq7([(nodes["sum_g"][0], nodes["sum_h"][0])])
+    after = eq7([(nodes["sum_g"][1], nodes["sum_h"][1]), (nodes["sum_g"][2], nodes["sum_h"][2])])
+    assert nodes["gain"][0] > 1.0
+    # the loss reduction of the split is Eq. 8's gain (gamma included once, for the extra leaf)
+    assert abs((before - after) - nodes["gain"][0]) < 1e-12 * max(1.0, abs(nodes["gain"][0]))
 
 
 def _greedy_raw(X, qg, qh, e_g, e_h, rows, depth, D, lam, gamma, mcw, out, v):
