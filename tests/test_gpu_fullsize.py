@@ -19,7 +19,15 @@ def config2():
     return X, y
 
 
-def test_config2_cuts_bins_root_histogram_split(ctx, config2):
+@pytest.fixture(scope="module")
+def config2_oracle(config2):
+    """Oracle cuts (500 sorts of 1M values, ~1 min single thread) and bins of config 2."""
+    X, _ = config2
+    cv, cp = oracle.cuts(X, 256)
+    return cv, cp, oracle.bins(X, cv, cp)
+
+
+def test_config2_cuts_bins_root_histogram_split(ctx, config2, config2_oracle):
     X, y = config2
     n, m = X.shape
     d = ctx.quantise(X, 256)
@@ -30,8 +38,7 @@ def test_config2_cuts_bins_root_histogram_split(ctx, config2):
     cv, cp = oracle.cuts(np.ascontiguousarray(X[:, feats]), 256)
     for k, j in enumerate(feats):
         np.testing.assert_array_equal(gv[gp[j]:gp[j + 1]], cv[cp[k]:cp[k + 1]], err_msg=f"feature {j}")
-    # full cuts from the oracle are needed for bins / trees: 500 x sort(1M) ~ 1 min single thread
-    cv_all, cp_all = oracle.cuts(X, 256)
+    cv_all, cp_all, B = config2_oracle
     assert gv.tobytes() == cv_all.tobytes() and np.array_equal(gp, cp_all)
     rows = np.sort(rng.choice(n, size=10_000, replace=False))
     B_s = oracle.bins(X[rows], cv_all, cp_all)
@@ -42,7 +49,6 @@ def test_config2_cuts_bins_root_histogram_split(ctx, config2):
     d.set_gradients(g, h)
     d.sample(ob.SAMPLE_NONE, 1.0, quant_bits=16)
     t = d.build_tree(1, 1.0, 0.0, 1.0, 0.1, keep_debug=True)
-    B = oracle.bins(X, cv_all, cp_all)
     qg, e_g = oracle.quantise(g.astype(np.float64), 16)
     qh, e_h = oracle.quantise(h.astype(np.float64), 16)
     on, lor, hist = oracle.build_tree(B, m, cv_all, cp_all, qg, qh, e_g, e_h, 1, want_hist=True)
@@ -61,6 +67,46 @@ def test_config2_cuts_bins_root_histogram_split(ctx, config2):
             assert n8["gain"][v] > 0
     assert n8["n_rows"][0] == n
     t8.close()
+    d.close()
+
+
+@pytest.mark.parametrize("quant_bits", [16])
+def test_config2_depth8_two_rounds_vs_oracle(ctx, config2, config2_oracle, quant_bits):
+    """The benchmarked configuration itself (bench.py: 1M x 500, 256 bins, depth 8, f = 1,
+    lambda 1, gamma 0, mcw 1, eta 0.1, the same CUDA graph and kernels), two consecutive boosting
+    rounds with the margin updated in between (Eq. 1 via the partition, update_margin): every
+    tree field, the histogram of every node of depth < 8 (built and derived), the leaf of every
+    row and the updated margins are bit-exact against the oracle (Alg. 1; Eq. 8
+    P:L144-151; Eq. 6)."""
+    X, y = config2
+    cv, cp, B = config2_oracle
+    n, m = X.shape
+    d = ctx.quantise(X, 256)
+    gm = np.zeros(n, np.float32)
+    om = np.zeros(n, np.float32)
+    for r in range(2):
+        np.testing.assert_array_equal(gm, om, err_msg=f"margins before round {r}")
+        g, h = oracle.logistic_grad(om, y)  # identical gradients on both sides
+        d.set_gradients(g, h)
+        d.sample(ob.SAMPLE_NONE, 1.0, round=r, quant_bits=quant_bits)
+        t = d.build_tree(8, 1.0, 0.0, 1.0, 0.1, keep_debug=True)
+        qg, e_g = oracle.quantise(g.astype(np.float64), quant_bits)
+        qh, e_h = oracle.quantise(h.astype(np.float64), quant_bits)
+        on, lor, hist = oracle.build_tree(B, m, cv, cp, qg, qh, e_g, e_h, 8, 1.0, 0.0, 1.0, 0.1, want_hist=True)
+        gn = t.export()
+        for f in on.dtype.names:
+            np.testing.assert_array_equal(gn[f], on[f], err_msg=f"round {r}: {f}")
+        assert int((on["feature"] >= 0).sum()) > 100, "the tree should be deep and bushy"
+        for v in range(255):
+            if on["feature"][v] == -2:
+                continue
+            np.testing.assert_array_equal(t.get_histogram(v), hist[v], err_msg=f"round {r}: node {v}")
+        np.testing.assert_array_equal(t.get_partition(n), lor, err_msg=f"round {r}: leaf of row")
+        gm = d.update_margin(t, gm)
+        om = oracle.predict(B, on, om)
+        np.testing.assert_array_equal(gm, om, err_msg=f"round {r}: margins after the update")
+        t.close()
+        del hist
     d.close()
 
 

@@ -19,7 +19,7 @@ WORKER = r'''
 import os, sys, json
 sys.path.insert(0, os.environ["OOCGB_ROOT"])
 import numpy as np, torch, torch.distributed as dist
-import paper_2005_09148_b200 as ob, synth
+import paper_2005_09148_b200 as ob, synth, oracle
 from paper_2005_09148_b200.dist import shard_rows, gloo_collective
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 dist.init_process_group("gloo")
@@ -30,7 +30,8 @@ margin = rng.normal(scale=0.5, size=n).astype(np.float32)
 row0, nl = shard_rows(n, rank, world)
 ctx = ob.Context(0, rank, world, host_collective=gloo_collective())
 d = ctx.quantise(X[row0:row0 + nl], 256, row0_global=row0, n_rows_global=n)
-d.set_logistic_gradients(margin[row0:row0 + nl], y[row0:row0 + nl])
+g_all, h_all = oracle.logistic_grad(margin, y)  # host gradients: identical inputs for the oracle
+d.set_gradients(g_all[row0:row0 + nl], h_all[row0:row0 + nl])
 info = d.sample(mode, ratio, 1.0, seed=7, round=2, quant_bits=16)
 gid, qg, qh = d.get_sample(info["n_selected_local"])
 t = d.build_tree(depth)
@@ -45,7 +46,7 @@ res = dict(rank=rank, cuts=cv.tobytes().hex()[:4000], ncuts=int(cp[-1]), cuts_ha
 if rank == 0:
     c1 = ob.Context(0)
     d1 = c1.quantise(X, 256)
-    d1.set_logistic_gradients(margin, y)
+    d1.set_gradients(g_all, h_all)
     i1 = d1.sample(mode, ratio, 1.0, seed=7, round=2, quant_bits=16)
     g1, _, _ = d1.get_sample(i1["n_selected_local"])
     t1 = d1.build_tree(depth)
@@ -59,6 +60,22 @@ if rank == 0:
         assert np.array_equal(n1[f], nodes[f]), f"tree field {f} differs (2 ranks vs 1)"
     p1 = d1.predict([t1], np.zeros(n, np.float32))
     assert np.array_equal(p1[row0:row0 + nl], pm), "predict differs"
+    # the oracle on the full data (Alg. 1 + Eq. 8, R9 sampling, R12 fixed point): the 2-rank tree
+    # is compared with it directly, field by field
+    ocv, ocp = oracle.cuts(X, 256, seed=2)
+    assert ocv.tobytes() == cv.tobytes() and np.array_equal(ocp, cp), "cuts differ from the oracle"
+    OB = oracle.bins(X, ocv, ocp)
+    s_ = oracle.sample(g_all, h_all, mode, ratio, 1.0, 7, 2)
+    sel_ = s_["selected"].astype(bool)
+    assert int(sel_.sum()) == info["n_selected_global"], "sample size differs from the oracle"
+    oqg, oe_g = oracle.quantise(s_["gs"][sel_], 16)
+    oqh, oe_h = oracle.quantise(s_["hs"][sel_], 16)
+    assert (oe_g, oe_h) == (info["e_g"], info["e_h"]), "fixed-point exponents differ from the oracle"
+    on_, _, _ = oracle.build_tree(OB[sel_], m, ocv, ocp, oqg, oqh, oe_g, oe_h, depth)
+    for f in on_.dtype.names:
+        assert np.array_equal(on_[f], nodes[f]), f"tree field {f} differs (2 ranks vs oracle)"
+    op = oracle.predict(OB, on_, np.zeros(n, np.float32))
+    assert np.array_equal(op[row0:row0 + nl], pm), "predict differs from the oracle"
     print("RANK0-REFERENCE-OK", info["n_selected_global"], int((n1["feature"] >= 0).sum()))
 all_g = [None] * world
 dist.all_gather_object(all_g, gid.tolist())

@@ -55,6 +55,27 @@ def test_cuts_negative_zero_and_ties(ctx):
     d.close()
 
 
+@pytest.mark.parametrize("n,max_bin,tie_frac", [(1003, 16, 0.5), (40001, 256, 0.5), (5000, 7, 0.7), (4099, 256, 0.6)])
+def test_cuts_heavy_ties_more_than_B_distinct(ctx, n, max_bin, tie_frac):
+    """R1 step 4 (ceil rank, repeats dropped) on the GPU: more than B distinct values, a large
+    share of them tied on a few values, n not a multiple of B; cuts and bins bit-exact."""
+    rng = np.random.default_rng(n)
+    X = rng.normal(size=(n, 5)).astype(np.float32) * 4
+    for j in range(5):
+        k = int(n * tie_frac)
+        idx = rng.choice(n, size=k, replace=False)
+        X[idx, j] = rng.choice(np.array([-1.5, 0.25, 3.0, 7.75], np.float32) + j, size=k)
+        assert len(np.unique(X[:, j])) > max_bin
+    cv, cp, B = _oracle_cuts_bins(X, max_bin)
+    assert any(cp[j + 1] - cp[j] < max_bin for j in range(5))  # some repeats were dropped
+    d = ctx.quantise(X, max_bin)
+    gv, gp = d.get_cuts()
+    np.testing.assert_array_equal(gp, cp)
+    assert gv.tobytes() == cv.tobytes()
+    np.testing.assert_array_equal(d.get_bins(), B)
+    d.close()
+
+
 def test_nonfinite_rejected(ctx):
     X = np.ones((10, 3), np.float32)
     X[4, 1] = np.nan
@@ -198,10 +219,15 @@ def test_tree_bit_exact(ctx, n, m, max_bin, depth, mode, ratio, stress):
         rng = np.random.default_rng(n + 1)
         g = rng.uniform(-1.0, 1.0, n).astype(np.float32)
         h = rng.uniform(0.05, 1.0, n).astype(np.float32)
-    on, olor, ohist, sel = _oracle_tree(B, m, cv, cp, g, h, mode, ratio, depth)
+    _check_tree(ctx, X, max_bin, cv, cp, B, g, h, mode, ratio, depth, 16)
+
+
+def _check_tree(ctx, X, max_bin, cv, cp, B, g, h, mode, ratio, depth, quant_bits):
+    n, m = X.shape
+    on, olor, ohist, sel = _oracle_tree(B, m, cv, cp, g, h, mode, ratio, depth, quant_bits=quant_bits)
     d = ctx.quantise(X, max_bin)
     d.set_gradients(g, h)
-    info = d.sample(mode, ratio, 1.0, 1, 0, 16)
+    info = d.sample(mode, ratio, 1.0, 1, 0, quant_bits)
     t = d.build_tree(depth, 1.0, 0.0, 1.0, 0.1, keep_debug=True)
     gn = t.export()
     _compare_trees(gn, on)
@@ -222,6 +248,33 @@ def test_tree_bit_exact(ctx, n, m, max_bin, depth, mode, ratio, stress):
         np.testing.assert_array_equal(um, om)
     t.close()
     d.close()
+    return on
+
+
+# quant_bits decides kmax = (2^31 - 1) >> P, i.e. the histogram chunking, which nodes go to the
+# int64 (general) or int32 (narrow) evaluation list and which parents are kept as compact s32
+# pairs: each case has nodes above and below kmax and multi-chunk pairs (R12)
+QB_CASES = [
+    # n, m, depth, mode, ratio, quant_bits
+    (20000, 24, 6, 0, 1.0, 20),      # kmax 2047: every node of the top levels is multi-chunk int64
+    (30000, 16, 7, 2, 0.5, 20),
+    (20000, 24, 6, 0, 1.0, 8),       # kmax 8.4M: everything narrow
+    (600000, 8, 5, 0, 1.0, 12),      # kmax 524287: root int64, children int32
+    (9000000, 3, 3, 0, 1.0, 8),      # kmax 8388607: root int64 at P = 8
+]
+
+
+@pytest.mark.parametrize("n,m,depth,mode,ratio,quant_bits", QB_CASES)
+def test_tree_bit_exact_quant_bits(ctx, n, m, depth, mode, ratio, quant_bits):
+    X, y = synth.fast_classification(n, m, seed=31 + n) if n > 100000 else synth.make_classification(n, m, seed=31 + n)
+    cv, cp, B = _oracle_cuts_bins(X, 256)
+    margin = np.random.default_rng(n).normal(scale=0.5, size=n).astype(np.float32)
+    g, h = oracle.logistic_grad(margin, y)
+    kmax = (2**31 - 1) >> quant_bits
+    on = _check_tree(ctx, X, 256, cv, cp, B, g, h, mode, ratio, depth, quant_bits)
+    rows = on["n_rows"][on["feature"] != -2]
+    if quant_bits != 8 or n > kmax:
+        assert rows.max() > kmax and rows.min() <= kmax  # both evaluation lists are exercised
 
 
 def test_logistic_gradients_close(ctx):
@@ -335,6 +388,66 @@ def test_training_auc_config1(ctx):
     assert abs(a_gpu - a_orc) / a_orc <= 1e-3
     assert a_gpu > 0.8
     d.close()
+
+
+def test_streaming_after_in_core_build(ctx):
+    """an in-core build of PINNED_HOST f = 1 data, then set_streaming(1) on the same
+    data: the streamed build needs its int64 node buffers (allocated on demand) and gives the
+    same tree."""
+    n, m = 20000, 24
+    X, y = synth.make_classification(n, m, seed=12)
+    g, h = oracle.logistic_grad(np.zeros(n, np.float32), y)
+    d = ctx.quantise(X, 256, page_bytes=4096 * 32, placement=ob.PLACE_PINNED_HOST)
+    d.set_gradients(g, h)
+    d.sample(0, 1.0)
+    t0 = d.build_tree(6)
+    d.set_streaming(True)
+    d.sample(0, 1.0)
+    t1 = d.build_tree(6)
+    _compare_trees(t1.export(), t0.export())
+    t0.close()
+    t1.close()
+    d.close()
+
+
+def test_update_margin_refuses_tree_of_older_sample(ctx):
+    """MVS sample -> tree -> sample(NONE) -> update_margin(tree) must be ERR_STATE
+    (the tree's partition covers another sample), not out-of-bounds work."""
+    n, m = 5000, 8
+    X, y = synth.make_classification(n, m, seed=13)
+    g, h = oracle.logistic_grad(np.zeros(n, np.float32), y)
+    d = ctx.quantise(X, 256)
+    d.set_gradients(g, h)
+    d.sample(2, 0.3)
+    t = d.build_tree(4)
+    d.sample(0, 1.0)
+    with pytest.raises(ob.OocgbError) as e:
+        d.update_margin(t, np.zeros(n, np.float32))
+    assert e.value.status == ob.ERR_STATE
+    t2 = d.build_tree(4)
+    with pytest.raises(ob.OocgbError) as e:  # not the latest tree either
+        d.update_margin(t, np.zeros(n, np.float32))
+    assert e.value.status == ob.ERR_STATE
+    d.update_margin(t2, np.zeros(n, np.float32))
+    t.close()
+    t2.close()
+    d.close()
+
+
+def test_ctx_destroy_with_live_tree_is_state_error():
+    c = ob.Context(0)
+    n, m = 500, 4
+    X, y = synth.make_classification(n, m, seed=14)
+    d = c.quantise(X, 256)
+    d.set_gradients(*oracle.logistic_grad(np.zeros(n, np.float32), y))
+    d.sample(0, 1.0)
+    t = d.build_tree(3)
+    d.close()
+    with pytest.raises(ob.OocgbError) as e:
+        c.close()
+    assert e.value.status == ob.ERR_STATE
+    t.close()
+    c.close()
 
 
 def test_state_errors(ctx):
