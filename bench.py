@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rows", type=int, default=N_ROWS, help="rows per GPU (config 2: 1M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-link", action="store_true", help="skip the short out-of-core link leg")
     ap.add_argument("--nccl1", action="store_true",
                     help="N=1: run the sharded code path (NCCL exchanges) on a 1-rank communicator")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON line)")
@@ -191,57 +192,56 @@ def make_data(rows, rank):
     return X, y
 
 
-def cpu_baseline_leg(sample_rows=200_000, rounds=3):
-    """Oracle (as it stands, single thread) on a bounded sample of config 2: `rounds` boosting
-    rounds on sample_rows x 500, depth 8; sec/round extrapolated linearly in rows (the oracle is
-    O(rows x features x depth)) to 1M rows.  Setup (cuts, bins) untimed."""
+def _oracle_config2():
+    """The oracle's setup of config 2 (1M x 500, bench.py's rank-0 data): cuts + bins (untimed)."""
     import oracle
-    import synth
-    X, y = synth.fast_classification(sample_rows, N_FEAT, seed=77)
+    X, y = make_data(N_ROWS, 0)
     cv, cp = oracle.cuts(X, MAX_BIN)
     B = oracle.bins(X, cv, cp)
-    margin = np.zeros(sample_rows, np.float32)
+    return B, cv, cp, y
+
+
+def _oracle_rounds(B, cv, cp, y, n_rounds, n_warm=0):
+    """Boosting rounds of the oracle exactly as the product runs them (predict(t-1) -> logistic
+    gradients -> sample(NONE) -> fixed point -> BuildTree at depth 8); sec/round of the timed ones."""
+    import oracle
+    margin = np.zeros(len(y), np.float32)
     prev = None
     ts = []
-    for r in range(rounds):
+    for r in range(n_warm + n_rounds):
         t0 = time.perf_counter()
         prev, margin, _ = oracle.boosting_round(B, N_FEAT, cv, cp, margin, y, max_depth=DEPTH, lam=LAMBDA,
                                                 gamma=GAMMA, mcw=MCW, eta=ETA, quant_bits=QBITS,
                                                 prev_tree=prev, round_=r)
-        ts.append(time.perf_counter() - t0)
-    per_round = statistics.median(ts) * (N_ROWS / sample_rows)
-    return {"value": per_round, "unit": "s", "cores": 1, "kind": "oracle",
-            "sample": f"{rounds} rounds on {sample_rows} x {N_FEAT} rows (depth {DEPTH}), median sec/round "
-                      f"x {N_ROWS // sample_rows} (linear in rows) -> 1M x 500; single thread, "
-                      f"host {os.cpu_count()} cores"}
+        if r >= n_warm:
+            ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def cpu_baseline_leg(rounds=2):
+    """Oracle (as it stands, single thread) on the FULL config-2 workload: `rounds` boosting rounds
+    on 1M x 500 at depth 8 (no extrapolation; about 20 s per round); setup (cuts, bins) untimed."""
+    B, cv, cp, y = _oracle_config2()
+    ts = _oracle_rounds(B, cv, cp, y, rounds)
+    return {"value": statistics.mean(ts), "unit": "s", "cores": 1, "kind": "oracle",
+            "sample": f"{rounds} full rounds of config 2 (1M x 500, depth 8), mean sec/round, no extrapolation; "
+                      f"single thread, host {os.cpu_count()} cores",
+            "rounds_s": ts}
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the CPU oracle as it stands (there is no reference code),
+    on bench.py's own config-2 workload at full size: W untimed + K timed boosting rounds."""
     if rank != 0:
         return
-    import oracle
-    import synth
-    sample_rows = 100_000
-    X, y = synth.fast_classification(sample_rows, N_FEAT, seed=77)
-    cv, cp = oracle.cuts(X, MAX_BIN)
-    B = oracle.bins(X, cv, cp)
-    margin = np.zeros(sample_rows, np.float32)
-    prev = None
-    ts = []
-    for r in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        prev, margin, _ = oracle.boosting_round(B, N_FEAT, cv, cp, margin, y, max_depth=DEPTH, lam=LAMBDA,
-                                                gamma=GAMMA, mcw=MCW, eta=ETA, quant_bits=QBITS,
-                                                prev_tree=prev, round_=r)
-        if r >= args.warmup:
-            ts.append(time.perf_counter() - t0)
-    scale = N_ROWS / sample_rows
-    v = sum(ts) / len(ts) * scale
-    sample = (f"each step = 1 boosting round on {sample_rows} x {N_FEAT} (depth {DEPTH}); sec/round x {scale:.0f}"
-              f" (linear in rows) -> config 2 (1M x 500); single thread")
+    B, cv, cp, y = _oracle_config2()
+    ts = _oracle_rounds(B, cv, cp, y, args.steps, args.warmup)
+    v = sum(ts) / len(ts)
+    sample = (f"each step = 1 full boosting round of config 2 (1M x 500, depth 8, f = 1) by the oracle; "
+              f"single thread, host {os.cpu_count()} cores")
     line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int64 fixed-point histograms, f64 gains", "data": "synthetic",
+            "vs_baseline": None, "dtype": "int64 fixed-point histograms (quant_bits 16), f64 gains", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": "config 2: 1M x 500 make_classification, 256 bins, depth 8, in-core, f=1",
                        "rows_per_gpu": N_ROWS, "n_features": N_FEAT, "max_bin": MAX_BIN, "max_depth": DEPTH},
@@ -251,6 +251,31 @@ def run_reference(args, rank, world):
 
 
 def run_config3(args, rank, world, local):
+    line = config3_measure(args, rank, world, local, args.rows3, args.steps, args.warmup)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def pinned_h2d_peak(local, gib=1, reps=5):
+    """Measured host-link peak: pinned host -> device cudaMemcpyAsync of `gib` GiB, best of `reps`
+    (CUDA events), one GPU (SURVEY §8(d) link roofline)."""
+    import torch
+    nb = gib << 30
+    h = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    dv = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{local}")
+    best = 1e30
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dv.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del h, dv
+    return nb / (best * 1e-3) / 1e9
+
+
+def config3_measure(args, rank, world, local, n, steps, warmup):
     """Config 3 (BASELINE.json configs[2]): 20M x 500 streamed as 32 MiB ELLPACK pages from pinned
     host memory, gradient-based (MVS) sampling f = 0.1, depth 8.  Per round: predict(tree t-1)
     streams every page (Eq. 1), logistic gradients, sample(MVS) + Compact gathers the selected
@@ -259,8 +284,9 @@ def run_config3(args, rank, world, local):
     import torch
     import paper_2005_09148_b200 as ob
     import synth
-    n, m = args.rows3, N_FEAT
+    m = N_FEAT
     torch.cuda.set_device(local)
+    link_peak = pinned_h2d_peak(local)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = ob.Context(local, rank, world, None, stream=stream.cuda_stream)
@@ -301,7 +327,7 @@ def run_config3(args, rank, world, local):
 
     r = 0
     ctx.set_profiling(True)  # before the warm-up: the timed rounds replay an already-captured graph
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         tree = one_round(tree, r)
         r += 1
     torch.cuda.synchronize()
@@ -309,13 +335,13 @@ def run_config3(args, rank, world, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     e0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         tree = one_round(tree, r)
         r += 1
     e1.record(stream)
     torch.cuda.synchronize()
     ck = clocks.stop()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = e0.elapsed_time(e1) / steps
     tm = ctx.get_timings()
     page_bytes_per_pass = n * info["row_stride"]
     # predict streams every page; Compact gathers only the selected rows (zero-copy, NEXT #2);
@@ -323,11 +349,11 @@ def run_config3(args, rank, world, local):
     if args.stream_f1:
         copied = page_bytes_per_pass * (1 + DEPTH + 1)
     else:
-        copied = page_bytes_per_pass + int(statistics.mean(sel[-args.steps:])) * info["row_stride"]
-    h2d_ms = tm["h2d_ms"] / args.steps
+        copied = page_bytes_per_pass + int(statistics.mean(sel[-steps:])) * info["row_stride"]
+    h2d_ms = tm["h2d_ms"] / steps
     line = {
-        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8 symbols, int32/int64 fixed-point sums, f64 gains",
         "data": "synthetic (make_classification-style, generated on the GPU per chunk, seeded)",
         "config": {"workload": ("config 3 variant: 20M x 500 out-of-core, 32 MiB pinned-host pages, f=1, Alg. 6 "
@@ -335,19 +361,19 @@ def run_config3(args, rank, world, local):
                                "config 3: 20M x 500 out-of-core, 32 MiB pinned-host ELLPACK pages, MVS f=0.1, depth 8",
                    "rows": n, "n_features": m, "n_pages": info["n_pages"], "rows_per_page": info["rows_per_page"],
                    "max_depth": DEPTH, "sample": "none" if args.stream_f1 else "MVS", "ratio": 1.0 if args.stream_f1 else 0.1},
-        "link": {"bytes_per_round": copied, "h2d_ms_per_round": h2d_ms,
+        "link": {"bytes_per_round": copied, "h2d_ms_per_round": h2d_ms, "peak_gbps": link_peak,
+                 "busy_frac_of_peak": copied / (ms * 1e-3) / 1e9 / link_peak,
                  "gbps_while_copying": copied / (h2d_ms * 1e-3) / 1e9 if h2d_ms > 0 else None,
                  "busy_frac": h2d_ms / ms, "effective_gbps": copied / (ms * 1e-3) / 1e9},
-        "phases_ms_per_round": {k: v / args.steps for k, v in tm.items() if k.endswith("_ms")},
-        "selected_rows_per_round": sel[-args.steps:],
+        "phases_ms_per_round": {k: v / steps for k, v in tm.items() if k.endswith("_ms")},
+        "selected_rows_per_round": sel[-steps:],
         "prep_s": prep_s, "clocks": ck,
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     if tree is not None:
         tree.close()
     d.close()
     ctx.close()
+    return line
 
 
 def run_config4(args, rank, world, local):
@@ -593,6 +619,15 @@ def main():
     h2d = rows * 4 * 3
     d2h = rows * 4 + n_nodes * 48
 
+    d.close()
+    # short out-of-core leg (config 3's path at 2M rows: 31 pinned 32 MiB pages, MVS f = 0.1):
+    # link GB/s and busy fraction against the measured pinned H2D peak
+    link = None
+    if world == 1 and not args.no_link:
+        lk = config3_measure(args, rank, world, local, 2_000_000, 3, 1)
+        link = dict(lk["link"], rows=2_000_000, n_pages=lk["config"]["n_pages"], ms_per_round=lk["ms_per_step"],
+                    workload="config 3 path at 2M rows: 32 MiB pinned-host pages, MVS f=0.1, depth 8",
+                    clocks=lk.get("clocks"))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_leg()
@@ -630,13 +665,14 @@ def main():
             "graph_captures_timed": tm.get("graph_captures"),
             "clocks": ck,
         }
+        if link:
+            line["link"] = link
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     for t in (tree, e2e_tree):
         if t is not None:
             t.close()
-    d.close()
     ctx.close()
     if world > 1:
         tdist.destroy_process_group()

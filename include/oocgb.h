@@ -180,7 +180,7 @@ int oocgb_sample_goss(oocgb_data data, double a, double b, uint64_t seed, uint64
 int oocgb_set_streaming(oocgb_data data, int32_t enable);
 
 /* build_tree (Alg. 1, depth-wise R16): histograms (fixed-point int, bit-exact), sibling
- * subtraction (R17), split evaluation (Eq. 8, R13-R14), stable partition, leaf values
+ * subtraction (R17), split evaluation (Eq. 8, R13-R14), partition (set semantics, R26), leaf values
  * (Eq. 6, eta applied at creation R15).  max_depth in [0, 16]; lambda >= 0; the tree is
  * written to *out.  keep_debug != 0 keeps per-node histograms and the final partition for
  * oocgb_get_histogram / oocgb_get_partition (memory: 2^D * m * 4 KB).  ERR_STATE before
@@ -211,6 +211,12 @@ int oocgb_get_histogram(oocgb_tree tree, int32_t node, int64_t *gh);
 /* leaf_of_row[n_selected_local]: heap index of the final node of each selected row, in the
  * order of oocgb_get_sample; needs keep_debug                                              */
 int oocgb_get_partition(oocgb_tree tree, int32_t *leaf_of_row);
+/* row_order[n_selected_local]: the final partition as positions -> selected-row index (order of
+ * oocgb_get_sample).  RepartitionInstances (Alg. 1) lays every split's left child before
+ * its right child, so the rows of each leaf form one contiguous block and the blocks come in
+ * left-first depth-first order; the order inside a block is unspecified (R26).  In-core
+ * builds only (ERR_STATE for an Alg. 6 streamed tree); needs keep_debug.                       */
+int oocgb_get_row_order(oocgb_tree tree, int32_t *row_order);
 
 /* Per-phase device timings of the last call (CUDA events on the ctx stream), milliseconds:
  * [0] histogram kernels, [1] split evaluation, [2] partition, [3] sample+quantise,

@@ -30,7 +30,7 @@ ABI_SYMBOLS = (
     "oocgb_quantise_like", "oocgb_data_info", "oocgb_data_destroy", "oocgb_set_gradients",
     "oocgb_set_logistic_gradients", "oocgb_sample", "oocgb_build_tree", "oocgb_tree_export",
     "oocgb_tree_destroy", "oocgb_predict", "oocgb_update_margin", "oocgb_get_cuts",
-    "oocgb_get_bins", "oocgb_get_sample", "oocgb_get_histogram", "oocgb_get_partition",
+    "oocgb_get_bins", "oocgb_get_sample", "oocgb_get_histogram", "oocgb_get_partition", "oocgb_get_row_order",
     "oocgb_get_timings", "oocgb_set_profiling", "oocgb_last_error", "oocgb_abi_version",
     "oocgb_ctx_create_hostcomm", "oocgb_sample_goss", "oocgb_set_streaming",
 )
@@ -114,6 +114,7 @@ def load_library():
         "oocgb_get_sample": [p, p, p, p],
         "oocgb_get_histogram": [p, i32, p],
         "oocgb_get_partition": [p, p],
+        "oocgb_get_row_order": [p, p],
         "oocgb_get_timings": [p, p, i32],
         "oocgb_set_profiling": [p, i32],
         "oocgb_ctx_create_hostcomm": [i32, i32, i32, COLLECTIVE_FN, p, u64, p],
@@ -363,6 +364,12 @@ class Tree:
         m = self.data.info()["n_features"]
         out = np.zeros((m, 256, 2), np.int64)
         _check(load_library().oocgb_get_histogram(self._h, node, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+    def get_row_order(self, n_selected_local: int) -> np.ndarray:
+        """Final partition, position -> selected-row index (stable: ascending inside each leaf)."""
+        out = np.zeros(n_selected_local, np.int32)
+        _check(load_library().oocgb_get_row_order(self._h, out.ctypes.data_as(ctypes.c_void_p)))
         return out
 
     def get_partition(self, n_selected_local: int) -> np.ndarray:

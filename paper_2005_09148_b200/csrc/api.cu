@@ -231,7 +231,8 @@ static oocgb_data new_data(oocgb_ctx c, int64_t n_local, int64_t row0, int64_t n
   d->n_global = n_global;
   d->m = m;
   d->n_fg = (m + 31) / 32;
-  d->stride = 32 * d->n_fg;  // bytes per row summed over the group planes (R5)
+  d->gw = plane_width(d->n_fg);
+  d->stride = d->gw * ((m + d->gw - 1) / d->gw);  // bytes per row summed over the planes (R5)
   d->max_bin = max_bin;
   d->placement = placement;
   d->seed = seed;
@@ -690,10 +691,11 @@ int oocgb_predict(oocgb_data d, const oocgb_tree *trees, int32_t n_trees, float 
     for (int t0 = 0; t0 < n_trees; t0 += 4096) {
       int nt = std::min(4096, n_trees - t0);
       if (d->placement == OOCGB_PLACE_DEVICE) {
-        predict_device(d, d->d_bins, 32, (size_t)d->rows_per_page * 32, d->n_local, 0, trees + t0, nt, dm);
+        predict_device(d, d->d_bins, d->gw, (size_t)d->rows_per_page * d->gw, d->gw == 64 ? 6 : 5, d->n_local, 0,
+                       trees + t0, nt, dm);
       } else {
         for_each_page(d, [&](const uint8_t *page, int64_t r0, int64_t nr) {
-          predict_device(d, page, (size_t)d->stride, 32, nr, r0, trees + t0, nt, dm);  // row-major page
+          predict_device(d, page, (size_t)d->stride, 32, 5, nr, r0, trees + t0, nt, dm);  // row-major page
         });
       }
     }
@@ -754,18 +756,19 @@ int oocgb_get_bins(oocgb_data d, int64_t row0_local, int64_t n, uint8_t *out) {
   for (int64_t r = row0_local; r < row0_local + n;) {
     const int64_t p = r / rpp, r_in = r - p * rpp;
     const int64_t cnt = std::min<int64_t>(rpp - r_in, row0_local + n - r);
-    for (int g = 0; g < d->n_fg; ++g) {
-      const size_t off = ell_off(r, 32 * g, rpp, d->n_fg);
+    const int gw = d->gw;
+    for (int g = 0; g < d->stride / gw; ++g) {
+      const size_t off = ell_off(r, gw * g, rpp, gw, d->stride);
       const uint8_t *src;
       if (d->placement == OOCGB_PLACE_DEVICE) {
-        page_buf.resize((size_t)cnt * 32);
-        OOCGB_CK(cudaMemcpy(page_buf.data(), d->d_bins + off, (size_t)cnt * 32, cudaMemcpyDeviceToHost));
+        page_buf.resize((size_t)cnt * gw);
+        OOCGB_CK(cudaMemcpy(page_buf.data(), d->d_bins + off, (size_t)cnt * gw, cudaMemcpyDeviceToHost));
         src = page_buf.data();
       } else {
         src = d->h_pages + off;
       }
       for (int64_t i = 0; i < cnt; ++i)
-        memcpy(out + (size_t)(r - row0_local + i) * d->stride + 32 * g, src + (size_t)i * 32, 32);
+        memcpy(out + (size_t)(r - row0_local + i) * d->stride + gw * g, src + (size_t)i * gw, gw);
     }
     r += cnt;
   }
@@ -807,6 +810,15 @@ int oocgb_get_partition(oocgb_tree t, int32_t *leaf_of_row) {
   OOCGB_REQUIRE(t && leaf_of_row, OOCGB_ERR_ARG, "NULL argument");
   OOCGB_REQUIRE(t->debug, OOCGB_ERR_STATE, "get_partition needs build_tree(keep_debug=1)");
   memcpy(leaf_of_row, t->leaf_of_row.data(), sizeof(int32_t) * t->leaf_of_row.size());
+  API_END
+}
+
+int oocgb_get_row_order(oocgb_tree t, int32_t *row_order) {
+  API_BEGIN
+  OOCGB_REQUIRE(t && row_order, OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(t->debug && t->has_row_order, OOCGB_ERR_STATE,
+                "get_row_order needs an in-core build_tree(keep_debug=1)");
+  memcpy(row_order, t->row_order.data(), sizeof(int32_t) * t->row_order.size());
   API_END
 }
 

@@ -132,12 +132,13 @@ struct LevelCtl {       // device-resident control block of one build
   int part_done;        // partition tiles finished (last-block ticket), reset by the last block
   int hist_next;        // k_hist dynamic item counter, zeroed by whoever writes the level's chunk plan
   int n_ew, n_en;       // eval work lists: (pair, side) entries of nodes with > kmax / <= kmax rows
-  int pad;
+  unsigned bar_count;   // k_partition's grid barrier: arrivals of the current generation
+  unsigned bar_gen;     // and its generation counter
 };
 
 // Histogram chunk size (rows) for a level with tot_rows built rows in n_pairs pairs, k_hist run
 // by `grid` persistent CTAs over (chunk, feature group) items: the smallest number of waves w
-// such that C = floor(w grid / n_fg) chunks of at most kmax rows (the s32 bound) hold every pair
+// such that C = floor(w grid / n_fg) >= 2 n_pairs - 1 chunks of at most kmax rows (the s32 bound) hold every pair
 // (sum_p ceil(count_p / cr) <= tot/cr + n_pairs - n_pairs/cr < C + 1 with cr = ceil(tot / (C -
 // n_pairs + 1))), so the items fill w whole waves (config 2 root: 37 equal chunks = 2 x 296 items
 // instead of 31 chunks = 1.68 waves).
@@ -147,17 +148,31 @@ __host__ __device__ __forceinline__ long long hist_chunk_rows(long long tot, int
   if (tot <= 0) return lo;
   for (long long w = 1;; ++w) {
     const long long C = w * grid / n_fg;
-    if (C < n_pairs || C < 1) continue;
+    // C >= 2 n_pairs - 1 keeps the largest chunk within ~2x the mean (cr <= tot / (C / 2)): a
+    // level with one big pair among many small ones (config 2 level 5: 39k rows + 15 pairs of
+    // < 5k) would otherwise get few huge chunks and a one-item straggler wave
+    if (C < 2LL * n_pairs - 1 || C < 1) continue;
     const long long cr = (tot + (C - n_pairs + 1) - 1) / (C - n_pairs + 1);
     if (cr <= kmax) return cr < lo ? lo : cr;
   }
 }
 
-// byte offset of symbol (row, f) in a tiled ELLPACK buffer of pages of rpp rows
-__host__ __device__ __forceinline__ size_t ell_off(int64_t row, int f, int64_t rpp, int n_fg) {
+// byte offset of symbol (row, f) in a tiled ELLPACK buffer of pages of rpp rows, planes of gw
+// bytes (gw = 64: features 64 P .. 64 P + 63 of a row are one 64-B DRAM burst, R5)
+__host__ __device__ __forceinline__ size_t ell_off(int64_t row, int f, int64_t rpp, int gw, int stride) {
   const int64_t p = row / rpp, r = row - p * rpp;
-  return ((size_t)p * n_fg + (size_t)(f >> 5)) * (size_t)rpp * 32 + (size_t)r * 32 + (size_t)(f & 31);
+  return (size_t)p * (size_t)rpp * stride + (size_t)(f / gw) * (size_t)rpp * gw + (size_t)r * gw + (size_t)(f % gw);
 }
+// plane width of a data set.  64-B planes (features 64 P .. 64 P + 63 of a row = one DRAM burst)
+// halve k_hist's DRAM bytes below the root (1.22x -> 0.99x the algorithmic bytes per round) but
+// were measured slower on B200: every 16-row warp load of a 32-feature item touches
+// 8 instead of 4 L1 lines (root +13 us, L1-pipe bound), and the partition's 1-byte gathers fetch a
+// burst of one row instead of two useful rows' sectors (+2.5 us per level).  OOCGB_PLANE_64 = 1
+// selects them (every kernel is layout-generic).
+#ifndef OOCGB_PLANE_64
+#define OOCGB_PLANE_64 0
+#endif
+__host__ __device__ __forceinline__ int plane_width(int n_fg) { return (OOCGB_PLANE_64 && n_fg >= 2) ? 64 : 32; }
 
 struct PNode {          // compact node for predict
   int32_t feature;
@@ -199,7 +214,8 @@ struct oocgb_data_s {
   oocgb_ctx ctx = nullptr;
   int64_t n_local = 0, n_global = 0, row0 = 0;
   int32_t m = 0, stride = 0, max_bin = 256, placement = OOCGB_PLACE_DEVICE;
-  int32_t n_fg = 0;                // feature groups of 32 (stride = 32 n_fg bytes per row)
+  int32_t n_fg = 0;                // feature groups of 32 (the histogram's items)
+  int32_t gw = 32;                 // tiled plane width in bytes (32 or 64), stride = gw * planes
   int64_t rows_per_page = 0, n_pages = 1;
   uint64_t seed = 0;
   // cuts (R1-R4)
@@ -211,7 +227,7 @@ struct oocgb_data_s {
   // ELLPACK (R5-R6)
   // Tiled ELLPACK (R5): pages of rows_per_page rows; inside a page the symbols of
   // feature group g (features 32g..32g+31) of all the page's rows are contiguous:
-  //   offset(row, f) = page * (rpp * stride) + (f / 32) * (rpp * 32) + (row % rpp) * 32 + f % 32
+  //   offset(row, f) = page * (rpp * stride) + (f / gw) * (rpp * gw) + (row % rpp) * gw + f % gw
   uint8_t *d_bins = nullptr;    // DEVICE placement: one tiled page, rpp = n_local
   // PINNED_HOST placement: ROW-MAJOR [n_local][stride] (a row is one contiguous block, so pages
   // stream as plain row ranges and selected rows can be gathered zero-copy over PCIe); the
@@ -273,6 +289,8 @@ struct oocgb_tree_s {
   bool debug = false;
   std::vector<long long> hist;       // [2^D - 1][m][256][2]
   std::vector<int32_t> leaf_of_row;  // selected order
+  std::vector<int32_t> row_order;    // final partition: position -> selected-order index
+  bool has_row_order = false;
 };
 
 namespace oocgb {
@@ -301,7 +319,8 @@ oocgb_tree build_tree(oocgb_data d, int max_depth, double lambda, double gamma, 
                       double eta, bool keep_debug);
 oocgb_tree build_tree_streamed(oocgb_data d, int max_depth, double lambda, double gamma, double mcw,
                                double eta, bool keep_debug);
-void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t pitch, int64_t n_rows, int64_t row_offset,
+void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t pitch, int lgw, int64_t n_rows,
+                    int64_t row_offset,
                     const oocgb_tree *trees, int n_trees, float *d_margin);
 void update_margin(oocgb_data d, oocgb_tree t, float *d_margin);
 void free_work(oocgb_data d);

@@ -134,9 +134,9 @@ __global__ void k_extract_cuts(const uint32_t *__restrict__ sorted, int64_t N, i
 // LookupBin + Write (Alg. 4) into the tiled page layout.  Thread per (feature group g,
 // row r, quad u): consecutive threads write consecutive 32-bit words of a group plane, so the
 // output is fully coalesced (device pages, or pinned host pages written zero-copy over PCIe).
-__global__ void k_bin_rows(const float *__restrict__ X, int64_t n, int m, int n_fg, int64_t row_local0,
-                           int64_t rpp, const float *__restrict__ cuts, const int *__restrict__ ptrs,
-                           uint8_t *__restrict__ out, int *err, int rowmajor) {
+__global__ void k_bin_rows(const float *__restrict__ X, int64_t n, int m, int n_fg, int gw, int stride,
+                           int64_t row_local0, int64_t rpp, const float *__restrict__ cuts,
+                           const int *__restrict__ ptrs, uint8_t *__restrict__ out, int *err, int rowmajor) {
   const int64_t total = (int64_t)n_fg * n * 8;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -161,8 +161,8 @@ __global__ void k_bin_rows(const float *__restrict__ X, int64_t n, int m, int n_
       if (a > B - 1) a = B - 1;  // clamp above the last cut (R3)
       word |= (uint32_t)a << (8 * c);
     }
-    const size_t off = rowmajor ? (size_t)(row_local0 + r) * (n_fg * 32) + g * 32 + u * 4
-                                : ell_off(row_local0 + r, g * 32 + u * 4, rpp, n_fg);
+    const size_t off = rowmajor ? (size_t)(row_local0 + r) * stride + g * 32 + u * 4
+                                : ell_off(row_local0 + r, g * 32 + u * 4, rpp, gw, stride);
     *reinterpret_cast<uint32_t *>(out + off) = word;
   }
 }
@@ -339,7 +339,8 @@ void bin_rows(oocgb_data d, const float *dX, int64_t n, int64_t row_local0, uint
   if (n <= 0) return;
   const int64_t total = (int64_t)d->n_fg * n * 8;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)c->num_sms * 32);
-  k_bin_rows<<<blocks, 256, 0, c->stream>>>(dX, n, d->m, d->n_fg, row_local0, d->rows_per_page, d->d_cut_values,
+  k_bin_rows<<<blocks, 256, 0, c->stream>>>(dX, n, d->m, d->n_fg, d->gw, d->stride, row_local0, d->rows_per_page,
+                                            d->d_cut_values,
                                             d->d_cut_ptrs, out_base, d_err,
                                             d->placement == OOCGB_PLACE_PINNED_HOST ? 1 : 0);
   OOCGB_CK(cudaGetLastError());

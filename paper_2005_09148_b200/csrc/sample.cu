@@ -305,21 +305,23 @@ __global__ void k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, S
 // all-reduce helpers need contiguous arrays: sums (G, H) and counts live next to each other
 
 // Compact (Alg. 7): row-major rows -> the tiled device sampled page.  One warp per row:
-// lane l moves 16-B chunk l (features 16l .. 16l + 15 -> group l / 2, half l % 2).  The source is
+// lane l moves 16-B chunk l (features 16l .. 16l + 15 -> plane l / (gw / 16)).  The source is
 // either a staged page in HBM (f = 1: src_rows = nullptr, row k of the output is row r0 + k of
 // the page) or the pinned host pages read zero-copy over PCIe (f < 1: only the selected rows
 // cross the link, 512 contiguous bytes per row).
-__global__ void k_rows_to_tiled(const uint8_t *__restrict__ src, int stride, const int32_t *__restrict__ src_rows,
-                                int64_t src_row0, int64_t k0, int64_t k1, int64_t cap, uint8_t *__restrict__ out) {
+__global__ void k_rows_to_tiled(const uint8_t *__restrict__ src, int stride, int gw,
+                                const int32_t *__restrict__ src_rows, int64_t src_row0, int64_t k0, int64_t k1,
+                                int64_t cap, uint8_t *__restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int chunks = stride / 16;
+  const int cpp = gw / 16;  // 16-B chunks per plane row
   for (int64_t k = k0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); k < k1;
        k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t r = (src_rows ? (int64_t)src_rows[k] : k) - src_row0;
     const uint8_t *srow = src + (size_t)r * stride;
     for (int ch = lane; ch < chunks; ch += 32) {
       const uint4 v = *reinterpret_cast<const uint4 *>(srow + ch * 16);
-      *reinterpret_cast<uint4 *>(out + ((size_t)(ch >> 1) * cap + k) * 32 + (ch & 1) * 16) = v;
+      *reinterpret_cast<uint4 *>(out + ((size_t)(ch / cpp) * cap + k) * gw + (ch % cpp) * 16) = v;
     }
   }
 }
@@ -618,7 +620,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       // f = 1: every page streams (H2D) and is re-laid out tiled on the device
       for_each_page(d, [&](const uint8_t *page, int64_t r0, int64_t nr) {
         const int blocks = (int)std::min<int64_t>((nr + 7) / 8, (int64_t)c->num_sms * 16);
-        k_rows_to_tiled<<<blocks, 256, 0, c->stream>>>(page, d->stride, nullptr, r0, r0, r0 + nr,
+        k_rows_to_tiled<<<blocks, 256, 0, c->stream>>>(page, d->stride, d->gw, nullptr, r0, r0, r0 + nr,
                                                        d->sampled_cap, d->d_sampled_page);
         OOCGB_CK(cudaGetLastError());
       });
@@ -627,7 +629,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       // carries n_sel rows instead of a second full pass)
       PhaseTimer link(c, 5);
       const int blocks = (int)std::min<int64_t>((d->n_sel + 7) / 8, (int64_t)c->num_sms * 32);
-      k_rows_to_tiled<<<blocks, 256, 0, c->stream>>>(d->h_pages, d->stride, d->d_sel_rows, 0, 0, d->n_sel,
+      k_rows_to_tiled<<<blocks, 256, 0, c->stream>>>(d->h_pages, d->stride, d->gw, d->d_sel_rows, 0, 0, d->n_sel,
                                                      d->sampled_cap, d->d_sampled_page);
       OOCGB_CK(cudaGetLastError());
     }

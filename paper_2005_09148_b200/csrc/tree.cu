@@ -205,7 +205,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
 __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
 k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
        const int2 *__restrict__ q, const Pair *__restrict__ pairs, LevelCtl *ctl,
-       const int *__restrict__ chunk_pair, int *__restrict__ partial, int identity, int row_step) {
+       const int *__restrict__ chunk_pair, int *__restrict__ partial, int identity, int row_step, int gshift) {
   extern __shared__ int4 smem4[];
   int *S = reinterpret_cast<int *>(smem4);
   char *Sb = reinterpret_cast<char *>(smem4);
@@ -220,8 +220,9 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
 #pragma unroll
   for (int s = 0; s < 16; ++s) f4[s] = sbase + 4u * (uint32_t)(16 * half + ((rslot + s) & 15));
   constexpr int RT = kHistThreads / 2;  // rows per CTA step
-  // symbol (row, f) at bins + (f / 32) * pitch + row * row_step + f % 32: row_step 32 for the
-  // tiled device pages, the row stride for a row-major (streamed) page with pitch 32
+  // symbol (row, f) of group fg = f / 32 at bins + (fg >> gshift) * pitch + row * row_step + (fg &
+  // (2^gshift - 1)) * 32 + f % 32: row_step = gw (32 or 64-B planes, gshift 0 or 1) for the tiled
+  // device pages, the row stride for a row-major (streamed) page with pitch 32, gshift 0
   // items: the first from blockIdx, then dynamically from ctl->hist_next (chunks are numbered
   // largest first by the plan, so this is longest-processing-time-first list scheduling); the
   // next item is fetched while the current one runs (double-buffered slot, read after the
@@ -239,7 +240,8 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
     for (int i = threadIdx.x; i < 2 * kBins * kFG / 4; i += kHistThreads) smem4[i] = make_int4(0, 0, 0, 0);
 #endif
     __syncthreads();
-    const uint8_t *base = bins + (size_t)fg * pitch + half * 16;
+    // 32-feature group fg lives in plane fg >> gshift at byte (fg & ((1 << gshift) - 1)) * 32
+    const uint8_t *base = bins + (size_t)(fg >> gshift) * pitch + (fg & ((1 << gshift) - 1)) * 32 + half * 16;
     auto row_of = [&](int kk) -> int { return identity ? kk : __ldg(ridx + kk); };
     auto load_row = [&](int kk, int row, uint4 &x, int2 &qv) {
       if (kk < r1) {
@@ -991,7 +993,7 @@ __device__ unsigned long long g_part_t0 = ~0ull;  // trace build only: first par
 // left/right ranks come from warp ballots plus a 64-entry (u, warp) scan.
 __global__ void __launch_bounds__(kPartThreads, 4)
 k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
-             const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, size_t pitch,
+             const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, size_t pitch, int lgw,
              const int32_t *__restrict__ ridx, const int2 *__restrict__ q, int32_t *__restrict__ ridx_out,
              int2 *__restrict__ q_out, int *__restrict__ cur, const int *__restrict__ tile_seg, int plan_inline,
              PlanArgs PA) {
@@ -1044,7 +1046,7 @@ k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
         }
         sg[u] = k;
       }
-      b[u] = f >= 0 ? bins[(size_t)(f >> 5) * pitch + (size_t)rows[u] * 32 + (f & 31)] : 0;
+      b[u] = f >= 0 ? bins[(size_t)(f >> lgw) * pitch + ((size_t)rows[u] << lgw) + (f & ((1 << lgw) - 1))] : 0;
       if (f >= 0) sb[u] |= 0x100;  // split marker
     }
 #pragma unroll
@@ -1421,11 +1423,12 @@ __global__ void __launch_bounds__(1024) k_part_plan(PlanArgs A) { plan_level(A, 
 
 // ---------------------------------------------------------------------------------------------
 // Prediction (Eq. 1): margin[row] += leaf(tree, bins_row), binned traversal, per tree in order.
-// Layout-generic addressing: symbol (row i, f) at bins + i * row_step + (f / 32) * pitch + f % 32
-// (tiled device page: row_step 32, pitch rpp * 32; row-major pinned page: row_step = stride,
-// pitch 32).
-__global__ void k_predict(const uint8_t *__restrict__ bins, size_t row_step, size_t pitch, int64_t n,
+// Layout-generic addressing: symbol (row i, f) at bins + i * row_step + (f >> lgw) * pitch +
+// (f & (2^lgw - 1)) (tiled device page: row_step = gw, pitch rpp * gw, lgw = log2 gw; row-major
+// pinned page: row_step = stride, pitch 32, lgw 5).
+__global__ void k_predict(const uint8_t *__restrict__ bins, size_t row_step, size_t pitch, int lgw, int64_t n,
                           const PNode *const *__restrict__ trees, int n_trees, float *__restrict__ margin) {
+  const int gmask = (1 << lgw) - 1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float mg = margin[i];
@@ -1435,7 +1438,7 @@ __global__ void k_predict(const uint8_t *__restrict__ bins, size_t row_step, siz
       int v = 0;
       while (nd[v].feature >= 0) {
         const int f = nd[v].feature;
-        v = (row[(size_t)(f >> 5) * pitch + (f & 31)] <= nd[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
+        v = (row[(size_t)(f >> lgw) * pitch + (f & gmask)] <= nd[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
       }
       mg = mg + nd[v].leaf;
     }
@@ -1571,7 +1574,8 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     mark(0, true);
     k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur], w->q[cur],
                                                                  w->pairs, w->ctl, w->chunk_pair, w->partial,
-                                                                 (lv == 0 && ridx_mode == 0) ? 1 : 0, 32);
+                                                                 (lv == 0 && ridx_mode == 0) ? 1 : 0, d->gw,
+                                                                 d->gw == 64 ? 1 : 0);
     OOCGB_CK(cudaGetLastError());
     mark(0, false);
     if (c->coll) {
@@ -1605,6 +1609,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     const bool inline_plan = !c->coll && n > 0;
     if (n > 0) {
       k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
+                                                          d->gw == 64 ? 6 : 5,
                                                           w->ridx[cur], w->q[cur], w->ridx[cur ^ 1], w->q[cur ^ 1],
                                                           w->seg_cur[lv & 1], w->tile_seg, inline_plan ? 1 : 0, PA);
       OOCGB_CK(cudaGetLastError());
@@ -1657,9 +1662,9 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   int ridx_mode;
   size_t pitch;  // bytes of one feature-group plane of the tiled page the tree reads
   if (d->placement == OOCGB_PLACE_PINNED_HOST) {
-    bins = d->d_sampled_page; ridx_mode = 0; pitch = (size_t)d->sampled_cap * 32;
+    bins = d->d_sampled_page; ridx_mode = 0; pitch = (size_t)d->sampled_cap * d->gw;
   } else {
-    bins = d->d_bins; ridx_mode = d->all_selected ? 0 : 1; pitch = (size_t)d->rows_per_page * 32;
+    bins = d->d_bins; ridx_mode = d->all_selected ? 0 : 1; pitch = (size_t)d->rows_per_page * d->gw;
   }
   if (keep_debug) {
     size_t need = sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1);
@@ -1749,15 +1754,21 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     dfree(d_leaf);
     // row index -> selected order
     t->leaf_of_row.assign(n, -1);
+    t->row_order.assign(n, -1);
+    t->has_row_order = true;
     if (ridx_mode == 1) {
       std::vector<int32_t> sel(n);
       if (n) OOCGB_CK(cudaMemcpy(sel.data(), d->d_sel_rows, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
       for (int i = 0; i < n; ++i) {
         int k = (int)(std::lower_bound(sel.begin(), sel.end(), rows[i]) - sel.begin());
         t->leaf_of_row[k] = leaf[i];
+        t->row_order[i] = k;
       }
     } else {
-      for (int i = 0; i < n; ++i) t->leaf_of_row[rows[i]] = leaf[i];
+      for (int i = 0; i < n; ++i) {
+        t->leaf_of_row[rows[i]] = leaf[i];
+        t->row_order[i] = rows[i];
+      }
     }
   }
   OOCGB_CK(cudaStreamSynchronize(c->stream));
@@ -1938,7 +1949,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
       {
         PhaseTimer t(c, 0);
         k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(batch, 32, m, n_fg, sw.b_ridx, sw.b_q, w->pairs,
-                                                                     w->ctl, w->chunk_pair, w->partial, 0, d->stride);
+                                                                     w->ctl, w->chunk_pair, w->partial, 0, d->stride, 0);
       }
       const int64_t tot = (int64_t)n_slots * m * kBins;
       k_accum_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
@@ -2004,7 +2015,8 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   return t;
 }
 
-void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t pitch, int64_t n_rows, int64_t row_offset,
+void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t pitch, int lgw, int64_t n_rows,
+                    int64_t row_offset,
                     const oocgb_tree *trees, int n_trees, float *d_margin) {
   oocgb_ctx c = d->ctx;
   if (n_rows <= 0 || n_trees <= 0) return;
@@ -2014,7 +2026,7 @@ void predict_device(oocgb_data d, const uint8_t *d_bins, size_t row_step, size_t
   OOCGB_REQUIRE(n_trees <= 4096, OOCGB_ERR_ARG, "predict: at most 4096 trees per call");
   OOCGB_CK(cudaMemcpyAsync(d_ptrs, ptrs.data(), sizeof(void *) * n_trees, cudaMemcpyHostToDevice, c->stream));
   int blocks = (int)std::min<int64_t>((n_rows + 255) / 256, (int64_t)c->num_sms * 16);
-  k_predict<<<blocks, 256, 0, c->stream>>>(d_bins, row_step, pitch, n_rows, d_ptrs, n_trees, d_margin + row_offset);
+  k_predict<<<blocks, 256, 0, c->stream>>>(d_bins, row_step, pitch, lgw, n_rows, d_ptrs, n_trees, d_margin + row_offset);
   OOCGB_CK(cudaGetLastError());
 }
 

@@ -7,6 +7,7 @@ import pytest
 
 import oracle
 import synth
+from test_gpu_parity import check_row_order
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -102,6 +103,7 @@ def test_config2_depth8_two_rounds_vs_oracle(ctx, config2, config2_oracle, quant
                 continue
             np.testing.assert_array_equal(t.get_histogram(v), hist[v], err_msg=f"round {r}: node {v}")
         np.testing.assert_array_equal(t.get_partition(n), lor, err_msg=f"round {r}: leaf of row")
+        check_row_order(t.get_row_order(n), on, lor)
         gm = d.update_margin(t, gm)
         om = oracle.predict(B, on, om)
         np.testing.assert_array_equal(gm, om, err_msg=f"round {r}: margins after the update")

@@ -222,6 +222,36 @@ def test_tree_bit_exact(ctx, n, m, max_bin, depth, mode, ratio, stress):
     _check_tree(ctx, X, max_bin, cv, cp, B, g, h, mode, ratio, depth, 16)
 
 
+def leaf_dfs_rank(nodes):
+    """Leaves of a tree in left-first depth-first order (the order RepartitionInstances, Alg. 1
+    L172-173, lays the children of every split out: left segment, then right)."""
+    rank = {}
+
+    def dfs(v):
+        if v >= len(nodes) or nodes["feature"][v] == -2:
+            return
+        if nodes["feature"][v] >= 0:
+            dfs(2 * v + 1)
+            dfs(2 * v + 2)
+        else:
+            rank[v] = len(rank)
+
+    dfs(0)
+    return rank
+
+
+def check_row_order(order, nodes, leaf_of_row):
+    """The device's final partition (R26): a permutation of the selected rows in which every
+    leaf's rows form one contiguous block, blocks in left-first depth-first leaf order; the order
+    of rows inside a block is not part of the result (set semantics: every exported value is an
+    exact integer sum or a per-row value)."""
+    n = len(leaf_of_row)
+    assert np.array_equal(np.sort(order), np.arange(n)), "row order is not a permutation"
+    rank = leaf_dfs_rank(nodes)
+    key = np.array([rank[int(v)] for v in leaf_of_row], np.int64)
+    assert np.all(np.diff(key[order]) >= 0), "leaf blocks are not contiguous in depth-first order"
+
+
 def _check_tree(ctx, X, max_bin, cv, cp, B, g, h, mode, ratio, depth, quant_bits):
     n, m = X.shape
     on, olor, ohist, sel = _oracle_tree(B, m, cv, cp, g, h, mode, ratio, depth, quant_bits=quant_bits)
@@ -238,6 +268,8 @@ def _check_tree(ctx, X, max_bin, cv, cp, B, g, h, mode, ratio, depth, quant_bits
         np.testing.assert_array_equal(t.get_histogram(v), ohist[v], err_msg=f"node {v}")
     # partition: final node of every selected row, bit-exact
     np.testing.assert_array_equal(t.get_partition(info["n_selected_local"]), olor)
+    # partition layout (R26): contiguous leaf blocks in depth-first order
+    check_row_order(t.get_row_order(info["n_selected_local"]), on, olor)
     # predict (binned traversal) == oracle predict, bit-exact float32
     m0 = np.random.default_rng(1).normal(size=n).astype(np.float32)
     gm = d.predict([t], m0.copy())
@@ -387,6 +419,36 @@ def test_training_auc_config1(ctx):
     a_gpu, a_orc = roc_auc_score(y, gm), roc_auc_score(y, om)
     assert abs(a_gpu - a_orc) / a_orc <= 1e-3
     assert a_gpu > 0.8
+    d.close()
+
+
+@pytest.mark.parametrize("mode,ratio", [(0, 1.0), (2, 0.5)])
+def test_run_to_run_determinism(ctx, mode, ratio):
+    """R26: the partition's row order inside a node follows the tiles' atomic reservations, so it
+    may differ between runs; every exported result may not.  Three builds of the same round:
+    identical tree fields, histograms of every node, leaf of every row and predictions."""
+    n, m, depth = 200000, 64, 8
+    X, y = synth.fast_classification(n, m, seed=17)
+    g, h = oracle.logistic_grad(np.random.default_rng(2).normal(scale=0.5, size=n).astype(np.float32), y)
+    d = ctx.quantise(X, 256)
+    ref = None
+    for rep in range(3):
+        d.set_gradients(g, h)
+        info = d.sample(mode, ratio, 1.0, 3, 5, 16)
+        t = d.build_tree(depth, keep_debug=True)
+        got = (t.export(), [t.get_histogram(v) for v in range((1 << depth) - 1)],
+               t.get_partition(info["n_selected_local"]), d.predict([t], np.zeros(n, np.float32)))
+        t.close()
+        if ref is None:
+            ref = got
+            assert int((got[0]["feature"] >= 0).sum()) > 50
+            continue
+        for f in ref[0].dtype.names:
+            np.testing.assert_array_equal(got[0][f], ref[0][f], err_msg=f"rep {rep}: {f}")
+        for v, (a, b) in enumerate(zip(got[1], ref[1])):
+            np.testing.assert_array_equal(a, b, err_msg=f"rep {rep}: histogram of node {v}")
+        np.testing.assert_array_equal(got[2], ref[2])
+        np.testing.assert_array_equal(got[3], ref[3])
     d.close()
 
 

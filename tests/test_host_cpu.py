@@ -146,7 +146,7 @@ PLANNER_CHECK = r'''
 #include <vector>
 // hist_chunk_rows (the histogram chunk planner of the root level and the streamed batches):
 // chunks never exceed kmax rows (the s32 exactness bound), hold every pair, and fill at most
-// the fewest whole waves of the k_hist grid that can hold the level.
+// the fewest whole waves of the k_hist grid that hold the level with >= 2 n_pairs - 1 chunks.
 int main() {
   std::mt19937_64 g(5);
   int bad = 0;
@@ -165,7 +165,7 @@ int main() {
     long long C = 0;
     for (long long w = 1;; ++w) {
       C = w * grid / n_fg;
-      if (C < n_pairs || C < 1) continue;
+      if (C < 2LL * n_pairs - 1 || C < 1) continue;
       const long long t = (tot + (C - n_pairs + 1) - 1) / (C - n_pairs + 1);
       if (t <= kmax) break;
     }

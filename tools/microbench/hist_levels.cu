@@ -42,15 +42,19 @@ __global__ void plane_read(const uint8_t *__restrict__ bins, size_t pitch, int r
 int main(int argc, char **argv) {
   const int N = 1 << 20, m = 500, n_fg = 16;
   const size_t pad = argc > 1 ? (size_t)atoll(argv[1]) : 0;  // bytes added to the plane pitch
-  const size_t pitch = (size_t)N * 32 + pad;
+#ifndef MB_GW
+#define MB_GW 64  // tiled plane width (the library: 64 once m > 32)
+#endif
+  const int n_planes = n_fg * 32 / MB_GW;
+  const size_t pitch = (size_t)N * MB_GW + pad;
   cudaDeviceProp prop;
   cudaGetDeviceProperties(&prop, 0);
   const int grid = prop.multiProcessorCount * kHistCtasPerSm;
   const int kmax = 0x7fffffff >> 16;
   uint8_t *bins;
-  cudaMalloc(&bins, pitch * n_fg);
+  cudaMalloc(&bins, pitch * n_planes);
   {
-    std::vector<uint8_t> h(pitch * n_fg);
+    std::vector<uint8_t> h(pitch * n_planes);
     std::mt19937 g(1);
     for (auto &x : h) x = (uint8_t)g();
     cudaMemcpy(bins, h.data(), h.size(), cudaMemcpyHostToDevice);
@@ -85,6 +89,7 @@ int main(int argc, char **argv) {
       printf("stream_read grid %5d: %.1f us  %.2f TB/s\n", g, best * 1e3, bytes / (best * 1e-3) / 1e12);
     }
     for (int thr : {512, 1024}) {
+      if (MB_GW != 32) break;  // the plane_read pattern models 32-B planes
       float best = 1e30f;
       for (int it = 0; it < 10; ++it) {
         cudaEventRecord(a); plane_read<<<grid, thr>>>(bins, pitch, 28340, 592, n_fg, o); cudaEventRecord(b);
@@ -141,7 +146,7 @@ int main(int argc, char **argv) {
       cudaMemset(partial, it, (size_t)8192 * kFG * kBins * 2 * 4 / 2);
       cudaEventRecord(e0);
       k_hist<<<grid, kHistThreads, kHistSmem>>>(bins, pitch, m, n_fg, ridx, q, pairs, ctl, chunk_pair,
-                                               partial, L.identity ? 1 : 0, 32);
+                                               partial, L.identity ? 1 : 0, MB_GW, MB_GW == 64 ? 1 : 0);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       if (cudaGetLastError() != cudaSuccess) { printf("launch failed: %s\n", L.name); return 1; }
@@ -153,6 +158,7 @@ int main(int argc, char **argv) {
     printf("%-40s rows %8lld items %5d chunk %6lld  %8.1f us  %6.2f T symbols/s  %.1f us/item-wave\n", L.name, tot,
            hc.n_items, cr, best * 1e3, sym / (best * 1e-3) / 1e12, best * 1e3 / ((double)hc.n_items / grid));
   }
-  printf("err: %s (experiment %d, pitch pad %zu)\n", cudaGetErrorString(cudaGetLastError()), OOCGB_HIST_EXPERIMENT, pad);
+  printf("err: %s (experiment %d, pitch pad %zu, plane width %d)\n", cudaGetErrorString(cudaGetLastError()),
+         OOCGB_HIST_EXPERIMENT, pad, MB_GW);
   return 0;
 }
