@@ -49,13 +49,16 @@ def parse():
     ap.add_argument("--nccl1", action="store_true",
                     help="N=1: run the sharded code path (NCCL exchanges) on a 1-rank communicator")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON line)")
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4],
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                     help="2: 1M x 500 in-core f=1 (the driver's bench); 3: 20M x 500 out-of-core, "
                          "32 MiB pinned pages, MVS f=0.1")
     ap.add_argument("--rows3", type=int, default=20_000_000, help="config 3 rows")
     ap.add_argument("--stream-f1", action="store_true",
                     help="config 3 without sampling: Alg. 6 streamed build (one page pass per level)")
     ap.add_argument("--rows4", type=int, default=100_000_000, help="config 4 training rows")
+    ap.add_argument("--rows5", type=int, default=400_000_000, help="config 5 global rows (sharded)")
+    ap.add_argument("--strong-rows", type=int, default=0,
+                    help="strong scaling: a fixed global row count sharded over the ranks (e.g. 100M)")
     ap.add_argument("--rounds4", type=int, default=50, help="config 4 boosting rounds per setting")
     return ap.parse_args()
 
@@ -190,6 +193,50 @@ def make_data(rows, rank):
     import synth
     X, y = synth.fast_classification(rows, N_FEAT, seed=1000 + rank)
     return X, y
+
+
+GEN_CHUNK = 1 << 21  # rows per generated chunk (global chunk grid: the data set is the same for every W)
+
+
+def shard_chunks(n_global, rank, world, chunk=GEN_CHUNK):
+    """This rank's rows [row0, row0 + n) (dist.shard_rows) as pieces of the GLOBAL generation grid:
+    (global chunk start, chunk rows, slice begin, slice end) -- a chunk is generated whole and
+    sliced, so the union of the ranks' rows is one data set whatever the world size."""
+    from paper_2005_09148_b200.dist import shard_rows
+    row0, n = shard_rows(n_global, rank, world)
+    out = []
+    r = row0
+    while r < row0 + n:
+        c0 = (r // chunk) * chunk
+        cn = min(chunk, n_global - c0)
+        b, e = r - c0, min(cn, row0 + n - c0)
+        out.append((c0, cn, b, e))
+        r = c0 + e
+    return row0, n, out
+
+
+def load_shard(ctx, n_global, rank, world, seed=5, device="cuda"):
+    """Multi-GPU data path (config 2 weak scaling, config 5, strong scaling): every rank generates
+    its own rows on its GPU (synth.torch_classification_chunk, never on the host) and streams
+    them through the library's two-pass quantise (oocgb_sketch_push, the sketch all-gather in
+    oocgb_cuts_finalize, oocgb_pages_push).  Returns (data, labels on the device, row0, n)."""
+    import torch
+    import synth
+    row0, n, pieces = shard_chunks(n_global, rank, world)
+    d = ctx.sketch_begin(N_FEAT, MAX_BIN, n_global, seed=2)
+    for c0, cn, b, e in pieces:
+        X, _ = synth.torch_classification_chunk(c0, cn, N_FEAT, seed=seed, device=device)
+        d.sketch_push(X[b:e].contiguous(), c0 + b)
+        del X
+    d.cuts_finalize()
+    ys = []
+    for c0, cn, b, e in pieces:
+        X, y = synth.torch_classification_chunk(c0, cn, N_FEAT, seed=seed, device=device)
+        d.pages_push(X[b:e].contiguous(), c0 + b)
+        ys.append(y[b:e])
+        del X
+    labels = torch.cat(ys) if ys else torch.zeros(0, device=device)
+    return d, labels.contiguous(), row0, n
 
 
 def _oracle_config2():
@@ -495,12 +542,32 @@ def main():
     elif args.nccl1:  # the multi-GPU code path (every exchange through NCCL) on a 1-rank communicator
         nid = ob.nccl_unique_id()
     ctx = ob.Context(local, rank, world, nid, stream=stream.cuda_stream)
-    rows = args.rows
-    X, y = make_data(rows, rank)
-    Xd = torch.from_numpy(X).cuda()
-    yd = torch.from_numpy(y).cuda()
-    d = ctx.quantise(Xd, MAX_BIN, row0_global=rank * rows, n_rows_global=world * rows)
-    del Xd
+    if args.config == 5 or args.strong_rows:
+        # config 5 (400M x 500 sharded) or strong scaling (a fixed global row count)
+        n_global = args.strong_rows or args.rows5
+        d, yd, _, rows = load_shard(ctx, n_global, rank, world)
+        y = yd.cpu().numpy()
+        workload = (f"config 5: {n_global} x {N_FEAT} row-sharded over {world} GPU(s)" if args.config == 5 else
+                    f"strong scaling: {n_global} x {N_FEAT} row-sharded over {world} GPU(s)")
+        scaling = "strong"
+        rows_global = n_global
+    elif world > 1:
+        # config 2 weak scaling: 1M rows per GPU, generated on each rank's GPU
+        d, yd, _, rows = load_shard(ctx, args.rows * world, rank, world)
+        y = yd.cpu().numpy()
+        workload = "config 2 weak scaling: 1M x 500 per GPU, 256 bins, depth 8, in-core, f=1"
+        scaling = "weak"
+        rows_global = args.rows * world
+    else:
+        rows = args.rows
+        X, y = make_data(rows, rank)
+        Xd = torch.from_numpy(X).cuda()
+        yd = torch.from_numpy(y).cuda()
+        d = ctx.quantise(Xd, MAX_BIN, row0_global=rank * rows, n_rows_global=world * rows)
+        del Xd
+        workload = "config 2: 1M x 500 make_classification, 256 bins, depth 8, in-core, f=1"
+        scaling = "weak"
+        rows_global = rows
     torch.cuda.synchronize()
     margin = torch.zeros(rows, dtype=torch.float32, device="cuda")
 
@@ -570,9 +637,10 @@ def main():
     tree_shape_state[2].close()
     tm = ctx.get_timings()
     ctx.set_profiling(False)
-    hist_bytes = sum(hist_algorithmic_bytes(nd, N_FEAT) for nd in exported)
-    part_bytes = sum(part_algorithmic_bytes(nd) for nd in exported)
-    hist_rowfeat = sum(hist_rows(nd)[0] * N_FEAT for nd in exported)
+    # per GPU: the exported tree counts global rows; each rank built 1/W of them (row-sharded)
+    hist_bytes = sum(hist_algorithmic_bytes(nd, N_FEAT) for nd in exported) / world
+    part_bytes = sum(part_algorithmic_bytes(nd) for nd in exported) / world
+    hist_rowfeat = sum(hist_rows(nd)[0] * N_FEAT for nd in exported) / world
     hist_ms = tm["hist_ms"]
     n_hist = max(1, int(tm["hist_launches"]))
     achieved = (hist_bytes / n_hist) / (hist_ms / n_hist * 1e-3) / 1e9  # GB/s per launch average
@@ -626,6 +694,7 @@ def main():
     if world == 1 and not args.no_link:
         lk = config3_measure(args, rank, world, local, 2_000_000, 3, 1)
         link = dict(lk["link"], rows=2_000_000, n_pages=lk["config"]["n_pages"], ms_per_round=lk["ms_per_step"],
+                    phases_ms_per_round=lk["phases_ms_per_round"],
                     workload="config 3 path at 2M rows: 32 MiB pinned-host pages, MVS f=0.1, depth 8",
                     clocks=lk.get("clocks"))
     cpu = None
@@ -634,16 +703,16 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": scaling,
             "vs_baseline": None, "dtype": "u8 symbols, int32/int64 fixed-point sums, f64 gains",
-            "data": "synthetic (make_classification-style, seeded)",
-            "config": {"workload": "config 2: 1M x 500 make_classification, 256 bins, depth 8, in-core, f=1",
-                       "rows_per_gpu": rows, "rows_global": rows * world, "n_features": N_FEAT,
+            "data": "synthetic (make_classification-style, seeded; W > 1: generated on each rank's GPU)",
+            "config": {"workload": workload,
+                       "rows_per_gpu": rows, "rows_global": rows_global, "n_features": N_FEAT,
                        "max_bin": MAX_BIN, "max_depth": DEPTH, "quant_bits": QBITS,
                        "parallelism": f"row-sharded dp{world}" + (" (NCCL 1-rank exchange path)" if args.nccl1 and world == 1 else ""),
                        "l2": "inputs larger than L2 (512 MB ELLPACK per GPU vs 126 MB L2), no flush"},
             "gpu_launches": launches_per_round(DEPTH) * args.steps,
-            "rows_rounds_per_s": rows * world / (ms_step / 1e3),
+            "rows_rounds_per_s": rows_global / (ms_step / 1e3),
             "histogram": {"row_features_per_s": hist_rowfeat / (hist_ms * 1e-3), "ms_per_round": hist_ms / args.steps,
                           "launches": n_hist, "algorithmic_bytes_per_round": hist_bytes / args.steps},
             "phases_ms_per_round": {k: v / args.steps for k, v in tm.items() if k.endswith("_ms")},

@@ -32,7 +32,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     tmp = OUT + f".tmp{os.getpid()}"
     extra = os.environ.get("OOCGB_EXTRA_NVCC", "").split()  # tuning experiments (-D...)
-    cmd = [NVCC, *FLAGS, *extra, "-o", tmp, *SRC, "-ldl"]
+    flags = [f for f in FLAGS if not (f == "-fmad=false" and os.environ.get("OOCGB_FMAD") == "1")]
+    cmd = [NVCC, *flags, *extra, "-o", tmp, *SRC, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

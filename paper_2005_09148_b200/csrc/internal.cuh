@@ -196,6 +196,7 @@ struct oocgb_ctx_s {
   void *host_coll_user = nullptr;
   int live_data = 0;
   int live_trees = 0;
+  bool mvs_attr = false;  // k_mvs_decide's dynamic shared memory attribute set on this device
   // page-pipeline events (stream.cuh), created with the ctx on its device
   cudaEvent_t pipe_copy_done[3] = {}, pipe_consumed[3] = {};
   int num_sms = 148;
@@ -257,6 +258,8 @@ struct oocgb_data_s {
   int64_t sel_cap = 0;
   double *d_gs = nullptr, *d_hs = nullptr;  // scaled g', h' of the selected rows
   long long *d_tmp64 = nullptr;             // MVS g_hat / q64 [n_local]
+  void *d_mvs = nullptr;                    // MVS device threshold state (sample.cu MvsDev)
+  unsigned long long *d_mvs_stats = nullptr;  // its per-bucket (count, sum, max) [3][2048]
   int64_t tmp_cap = 0;
   // tree workspace (lazy, sized for (n_sel cap, depth))
   struct Work *work = nullptr;

@@ -9,6 +9,8 @@
 //          on the distinct values, so instead of a sort we run a radix descent over the value
 //          space with per-bucket (count, sum, max) — exactly what multi-GPU needs (the stats
 //          are all-reduced).  p = 1 above the threshold, g_hat_q / mu below.
+//          The descent runs entirely on the device (k_mvs_*: no host round trip); GOSS's
+//          k-th-largest select reuses its passes (k_goss_decide).
 //  Selection u < p with u from Philox(seed, round; global_row, stream 0) (R24); g' = g/p.
 //  Fixed point: q = rint(x 2^e), e = quant_bits - k, frexp(max|x|) = (., k) (R12).
 #include "internal.cuh"
@@ -23,7 +25,6 @@ namespace oocgb {
 constexpr int kSelThreads = 256;
 constexpr int kSelPerThread = 8;
 constexpr int kSelTile = kSelThreads * kSelPerThread;
-constexpr int kRadixBuckets = 2048;
 
 __device__ __forceinline__ void atomic_max_abs(unsigned long long *dst, double x) {
   atomicMax(dst, (unsigned long long)__double_as_longlong(fabs(x)));
@@ -40,73 +41,316 @@ __global__ void k_logistic(const float *__restrict__ margin, const float *__rest
   }
 }
 
-// Eq. 9: g_hat = sqrt(g*g + lambda*(h*h)), no contraction (explicit _rn intrinsics).
-__global__ void k_ghat(const float *__restrict__ g, const float *__restrict__ h, int64_t n,
-                       double lam, double *__restrict__ ghat, unsigned long long *maxbits) {
+// ---------------------------------------------------------------------------------------------
+// MVS threshold on the device (R9): the radix descent of the exact integer
+// threshold runs as a fixed sequence of kernels on the ctx stream -- no host round trip.
+//   k_mvs_ghat_max   max g_hat (all ranks: all-reduce max)
+//   k_mvs_init       e', the bit width of the largest g_hat_q, the first pass's buckets
+//   k_mvs_pass<1>    g_hat_q = rint(g_hat 2^e') stored + (count, sum, max) per bucket of the
+//                    top <= 11 bits (one pass over g, h)
+//   k_mvs_decide     D(k) at every bucket edge in exact int128 (the host loop it replaces,
+//                    DESIGN.md §5): found / descend into one bucket
+//   k_mvs_pass<2+>   statistics of the next <= 11 bits over the values still in range; pass 2 reads
+//                    every g_hat_q and compacts the in-range ones, later passes read only those
+//   k_mvs_totals     k* = #{q > t*}, R = sum{q <= t*}; k_mvs_finish: mu (R9)
+// Per-bucket counts use native 32-bit shared atomics; the 64-bit sums are two 32-bit words with
+// an explicit carry (returning ATOMS on the low word); the bucket maximum takes a 64-bit CAS
+// only when a value exceeds the current maximum (a plain read filters the rest).
+struct MvsDev {
+  unsigned long long maxbits;            // max g_hat, double bits (all ranks)
+  int e, fallback_uniform, qbits, npass_used;
+  unsigned long long lo, above, below_sum;
+  long long below_max, fallback, tstar;
+  int have_fb, found, bits_left, sh, nb, pass;
+  unsigned long long compact_n[2];       // compacted in-range values per ping-pong buffer
+  unsigned long long tot[2];             // k_mvs_totals: count(q > t*), sum(q <= t*)
+  long long kstar;
+  double mu;
+  int has_t, pad;
+};
+constexpr int kMvsBuckets = 2048;
+constexpr int kMvsDecideSmem = 3 * (kMvsBuckets + 1) * 8;
+
+__global__ void k_mvs_ghat_max(const float *__restrict__ g, const float *__restrict__ h, int64_t n, double lam,
+                               unsigned long long *maxbits) {
   double mx = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double gi = (double)g[i], hi = (double)h[i];
-    double v = __dsqrt_rn(__dadd_rn(__dmul_rn(gi, gi), __dmul_rn(lam, __dmul_rn(hi, hi))));
-    ghat[i] = v;
-    mx = fmax(mx, v);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double gi = (double)g[i], hi = (double)h[i];
+    mx = fmax(mx, __dsqrt_rn(__dadd_rn(__dmul_rn(gi, gi), __dmul_rn(lam, __dmul_rn(hi, hi)))));
   }
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(mx));
 }
 
-// g_hat_q = rint(g_hat 2^e'), in place (double -> int64).
-__global__ void k_ghat_q(long long *__restrict__ buf, int64_t n, double scale) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double v = __longlong_as_double(buf[i]);
-    buf[i] = __double2ll_rn(__dmul_rn(v, scale));
-  }
+__device__ __forceinline__ void mvs_geometry(MvsDev *mv) {
+  const int wdt = mv->bits_left < 11 ? mv->bits_left : 11;
+  mv->sh = mv->bits_left - wdt;
+  mv->bits_left -= wdt;
+  mv->nb = 1 << wdt;
 }
 
-// Per-bucket (count, sum, max) of the values in [lo, lo + NB << shift).
-__global__ void k_radix_stats(const long long *__restrict__ q, int64_t n, unsigned long long lo,
-                              int shift, int nb, unsigned long long *cnt, unsigned long long *sum,
-                              unsigned long long *mx) {
-  __shared__ unsigned int s_cnt[kRadixBuckets];
-  __shared__ unsigned long long s_sum[kRadixBuckets];
-  __shared__ unsigned long long s_max[kRadixBuckets];
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) { s_cnt[b] = 0; s_sum[b] = 0; s_max[b] = 0; }
+__global__ void k_mvs_init(MvsDev *mv, int log2n, unsigned long long *stats) {
+  const double gmax = __longlong_as_double((long long)mv->maxbits);
+  MvsDev m = *mv;
+  m.found = 0; m.have_fb = 0; m.lo = 0; m.above = 0; m.below_sum = 0; m.below_max = -1; m.fallback = -1;
+  m.tstar = -1; m.pass = 0; m.compact_n[0] = m.compact_n[1] = 0; m.tot[0] = m.tot[1] = 0; m.has_t = 0;
+  m.kstar = -1; m.mu = 0.0; m.fallback_uniform = 0; m.e = 0; m.npass_used = 0;
+  if (!(gmax > 0.0)) {
+    m.fallback_uniform = 1;  // every g_hat is 0 -> uniform sampling
+    m.found = 1;
+  } else {
+    int kM;
+    frexp(gmax, &kM);
+    m.e = (62 - log2n) - kM;
+    const unsigned long long qmax = (unsigned long long)__double2ll_rn(ldexp(gmax, m.e));
+    m.qbits = qmax ? 64 - __clzll((long long)qmax) : 1;
+    m.bits_left = m.qbits;
+    mvs_geometry(&m);
+  }
+  *mv = m;
+  for (int i = threadIdx.x; i < 3 * kMvsBuckets; i += blockDim.x) stats[i] = 0;
+}
+
+// statistics of one pass: values v in [lo, lo + nb << sh) -> bucket (v - lo) >> sh
+struct MvsSmem {
+  unsigned cnt[kMvsBuckets];
+  unsigned slo[kMvsBuckets], shi[kMvsBuckets];
+  unsigned long long mx[kMvsBuckets];
+};
+// Warp-aggregated update: lanes whose values fall in the same bucket (__match_any) combine their
+// count, sum and maximum with shuffles first, and one leader per bucket issues the shared atomics
+// (early rounds put nearly every g_hat in one bucket: p ~ 0.5 gives g_hat ~ 0.559 on every row, a
+// 32-way conflict per warp without the aggregation).  A group's sum cannot overflow: every
+// g_hat_q <= 2^(62 - ceil_log2 n) and a group holds at most min(32, n) of them.
+__device__ __forceinline__ void mvs_add(MvsSmem &S, bool in, int b, unsigned long long v) {
+  const unsigned inmask = __ballot_sync(__activemask(), in);
+  if (!in) return;
+  const unsigned peers = __match_any_sync(inmask, b);
+  unsigned long long sum = 0, mx = 0;
+  for (unsigned m = peers; m; m &= m - 1) {
+    const unsigned long long x = __shfl_sync(peers, v, __ffs(m) - 1);
+    sum += x;
+    mx = x > mx ? x : mx;
+  }
+  if ((int)(threadIdx.x & 31) != __ffs(peers) - 1) return;
+  atomicAdd(&S.cnt[b], (unsigned)__popc(peers));
+  const unsigned vl = (unsigned)sum, vh = (unsigned)(sum >> 32);
+  const unsigned old = atomicAdd(&S.slo[b], vl);
+  const unsigned carry = (old + vl < old) ? 1u : 0u;
+  if (vh + carry) atomicAdd(&S.shi[b], vh + carry);
+  if (mx > *(volatile unsigned long long *)&S.mx[b]) atomicMax(&S.mx[b], mx);
+}
+
+// PASS == 1: g_hat_q from (g, h) (stored to q64); PASS == 2: every q64, in-range values compacted
+// to dst; PASS == 3: the compacted values of the previous pass (src, count compact_n[src_slot])
+template <int PASS>
+__global__ void __launch_bounds__(256) k_mvs_pass(const float *__restrict__ g, const float *__restrict__ h,
+                                                  double lam, long long *__restrict__ q64, int64_t n,
+                                                  long long *buf0, long long *buf1, MvsDev *mv,
+                                                  unsigned long long *stats) {
+  __shared__ MvsSmem S;
+  if (mv->found) return;
+  const unsigned long long lo = mv->lo;
+  const int sh = mv->sh, nb = mv->nb;
+  const unsigned long long span = (unsigned long long)nb << sh;
+  const int slot = mv->pass & 1;
+  long long *dst = slot ? buf1 : buf0;
+  const long long *src = slot ? buf0 : buf1;
+  int64_t cnt_n = n;
+  if (PASS == 3) cnt_n = (int64_t)mv->compact_n[slot ^ 1];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) { S.cnt[b] = 0; S.slo[b] = 0; S.shi[b] = 0; S.mx[b] = 0; }
   __syncthreads();
-  const unsigned long long span = (unsigned long long)nb << shift;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    unsigned long long v = (unsigned long long)q[i];
-    if (v < lo || v - lo >= span) continue;
-    int b = (int)((v - lo) >> shift);
-    atomicAdd(&s_cnt[b], 1u);
-    atomicAdd(&s_sum[b], v);
-    atomicMax(&s_max[b], v);
+  const double scale = PASS == 1 ? ldexp(1.0, mv->e) : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt_n; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long v;
+    if (PASS == 1) {
+      const double gi = (double)g[i], hi = (double)h[i];
+      const double gh = __dsqrt_rn(__dadd_rn(__dmul_rn(gi, gi), __dmul_rn(lam, __dmul_rn(hi, hi))));
+      const long long q = __double2ll_rn(__dmul_rn(gh, scale));
+      q64[i] = q;
+      v = (unsigned long long)q;
+    } else {
+      v = (unsigned long long)(PASS == 2 ? q64[i] : src[i]);
+    }
+    const bool in = v >= lo && v - lo < span;
+    mvs_add(S, in, in ? (int)((v - lo) >> sh) : -1, v);
+    if (PASS >= 2) {  // compaction for the next pass (order irrelevant: statistics only)
+      const unsigned m = __ballot_sync(__activemask(), in);
+      if (in) {
+        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&mv->compact_n[slot], (unsigned long long)__popc(m));
+        base = __shfl_sync(m, base, leader);
+        dst[base + __popc(m & ((1u << lane) - 1u))] = (long long)v;
+      }
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    if (s_cnt[b]) {
-      atomicAdd(&cnt[b], (unsigned long long)s_cnt[b]);
-      atomicAdd(&sum[b], s_sum[b]);
-      atomicMax(&mx[b], s_max[b]);
+    if (S.cnt[b]) {
+      atomicAdd(&stats[b], (unsigned long long)S.cnt[b]);
+      atomicAdd(&stats[kMvsBuckets + b], ((unsigned long long)S.shi[b] << 32) | S.slo[b]);
+      atomicMax(&stats[2 * kMvsBuckets + b], S.mx[b]);
     }
   }
 }
 
-// count(q > t), sum(q <= t)
-__global__ void k_threshold_totals(const long long *__restrict__ q, int64_t n, long long t,
-                                   unsigned long long *out /*[2]*/) {
+// One descent step (the former host loop, same operation order): D at every edge j = 0..nb,
+// j* = the largest j with P_j; then found / descend.  Single block of 1024 threads.
+__global__ void __launch_bounds__(1024) k_mvs_decide(MvsDev *mv, unsigned long long *stats, unsigned long long f_q,
+                                                      long long n_global) {
+  if (mv->found) return;
+  extern __shared__ unsigned long long s_dyn[];  // 3 x (kMvsBuckets + 1) words (> 48 KB: dynamic)
+  unsigned long long *s_cnt = s_dyn, *s_sum = s_dyn + (kMvsBuckets + 1);
+  long long *s_max = reinterpret_cast<long long *>(s_dyn + 2 * (kMvsBuckets + 1));
+  __shared__ int s_jstar;
+  const int nb = mv->nb;
+  const unsigned long long *cnt = stats, *sum = stats + kMvsBuckets, *mx = stats + 2 * kMvsBuckets;
+  // suffix counts suf[j] = sum_{b >= j} cnt[b]; prefix sums pre[j] = sum_{b < j} sum[b];
+  // prefix maxima A[j] = max over non-empty b < j of mx[b] (-1 if none)
+  for (int j = threadIdx.x; j <= nb; j += blockDim.x) {
+    s_cnt[j] = j < nb ? cnt[j] : 0;
+    s_sum[j] = j > 0 ? sum[j - 1] : 0;
+    s_max[j] = (j > 0 && cnt[j - 1]) ? (long long)mx[j - 1] : -1;
+  }
+  if (threadIdx.x == 0) s_jstar = -1;
+  __syncthreads();
+  for (int o = 1; o <= nb; o <<= 1) {  // Hillis-Steele scans (suffix for counts)
+    unsigned long long c[3], su[3];
+    long long m[3];
+    int k = 0;
+    for (int j = threadIdx.x; j <= nb; j += blockDim.x, ++k) {
+      c[k] = (j + o <= nb) ? s_cnt[j + o] : 0;
+      su[k] = j >= o ? s_sum[j - o] : 0;
+      m[k] = j >= o ? s_max[j - o] : -1;
+    }
+    __syncthreads();
+    k = 0;
+    for (int j = threadIdx.x; j <= nb; j += blockDim.x, ++k) {
+      s_cnt[j] += c[k];
+      s_sum[j] += su[k];
+      if (m[k] > s_max[j]) s_max[j] = m[k];
+    }
+    __syncthreads();
+  }
+  const __int128 two32 = (__int128)1 << 32;
+  const __int128 F = (__int128)f_q * (__int128)n_global;
+  for (int j = threadIdx.x; j <= nb; j += blockDim.x) {
+    const unsigned long long Rj = mv->below_sum + s_sum[j];
+    const long long Aj = s_max[j] > mv->below_max ? s_max[j] : mv->below_max;
+    const unsigned long long kj = mv->above + s_cnt[j];
+    if (Aj >= 0 && Rj > 0) {
+      const __int128 lhs = (__int128)Aj * (F - (__int128)kj * two32);
+      const __int128 rhs = two32 * (__int128)Rj;
+      if (lhs < rhs) atomicMax(&s_jstar, j);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int jstar = s_jstar;
+    const int sh = mv->sh;
+    mv->npass_used = mv->pass + 1;
+    if (jstar < 0) {
+      if (mv->have_fb) { mv->tstar = mv->fallback; mv->found = 1; }
+      else if (sh == 0) { mv->found = 1; }                 // no threshold: every non-zero row p = 1
+      else { mv->above += nb >= 1 ? s_cnt[1] : 0; }        // descend into bucket 0
+    } else {
+      const long long A_at = s_max[jstar] > mv->below_max ? s_max[jstar] : mv->below_max;
+      if (sh == 0 || jstar == nb) { mv->tstar = A_at; mv->found = 1; }
+      else {
+        mv->fallback = A_at;
+        mv->have_fb = 1;
+        mv->below_sum += s_sum[jstar];
+        const long long bm = s_max[jstar];
+        if (bm > mv->below_max) mv->below_max = bm;
+        mv->above += s_cnt[jstar + 1];
+        mv->lo += (unsigned long long)jstar << sh;
+      }
+    }
+    if (!mv->found) {
+      mv->pass += 1;
+      if (mv->bits_left <= 0) mv->found = 1;  // defensive: no bits left (cannot happen for sh > 0)
+      else mvs_geometry(mv);
+      mv->compact_n[mv->pass & 1] = 0;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * kMvsBuckets; i += blockDim.x) stats[i] = 0;
+}
+
+// k* = #{q > t*}, R = sum{q <= t*}
+__global__ void k_mvs_totals(const long long *__restrict__ q, int64_t n, MvsDev *mv) {
+  if (mv->tstar < 0) return;
+  const long long t = mv->tstar;
   unsigned long long c = 0, s = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    long long v = q[i];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long v = q[i];
     if (v > t) ++c; else s += (unsigned long long)v;
   }
   for (int o = 16; o; o >>= 1) {
     c += __shfl_down_sync(0xffffffffu, c, o);
     s += __shfl_down_sync(0xffffffffu, s, o);
   }
-  if ((threadIdx.x & 31) == 0) { atomicAdd(&out[0], c); atomicAdd(&out[1], s); }
+  if ((threadIdx.x & 31) == 0) { atomicAdd(&mv->tot[0], c); atomicAdd(&mv->tot[1], s); }
+}
+
+__global__ void k_mvs_finish(MvsDev *mv, unsigned long long f_q, long long n_global) {
+  if (mv->tstar >= 0) {
+    const __int128 two32 = (__int128)1 << 32;
+    const __int128 F = (__int128)f_q * (__int128)n_global;
+    const unsigned long long kstar = mv->tot[0], R = mv->tot[1];
+    mv->kstar = (long long)kstar;
+    mv->mu = ((double)(long long)R * 4294967296.0) / (double)(F - (__int128)kstar * two32);
+    mv->has_t = 1;
+  } else {
+    mv->kstar = -1;
+    mv->has_t = 0;
+  }
+}
+
+// GOSS (R25): one step of the radix select of the k_a-th largest value: the largest bucket j whose
+// count from the top (above + suffix count) reaches k_a (the host loop it replaces)
+__global__ void __launch_bounds__(1024) k_goss_decide(MvsDev *mv, unsigned long long *stats, unsigned long long k_a) {
+  if (mv->found) return;
+  extern __shared__ unsigned long long s_dyn[];
+  unsigned long long *s_cnt = s_dyn;
+  __shared__ int s_j;
+  const int nb = mv->nb;
+  for (int j = threadIdx.x; j <= nb; j += blockDim.x) s_cnt[j] = j < nb ? stats[j] : 0;
+  if (threadIdx.x == 0) s_j = 0;
+  __syncthreads();
+  for (int o = 1; o <= nb; o <<= 1) {  // suffix sums
+    unsigned long long c[3];
+    int k = 0;
+    for (int j = threadIdx.x; j <= nb; j += blockDim.x, ++k) c[k] = (j + o <= nb) ? s_cnt[j + o] : 0;
+    __syncthreads();
+    k = 0;
+    for (int j = threadIdx.x; j <= nb; j += blockDim.x, ++k) s_cnt[j] += c[k];
+    __syncthreads();
+  }
+  for (int j = threadIdx.x + 1; j < nb; j += blockDim.x)
+    if (mv->above + s_cnt[j] >= k_a) atomicMax(&s_j, j);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int j = s_j;
+    mv->npass_used = mv->pass + 1;
+    mv->above += s_cnt[j + 1];
+    mv->lo += (unsigned long long)j << mv->sh;
+    if (mv->sh == 0 || mv->bits_left <= 0) {
+      mv->found = 1;
+    } else {
+      mv->pass += 1;
+      mvs_geometry(mv);
+      mv->compact_n[mv->pass & 1] = 0;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * kMvsBuckets; i += blockDim.x) stats[i] = 0;
+}
+
+__global__ void k_goss_finish(MvsDev *mv, long long k_a) {
+  mv->tstar = (long long)mv->lo;
+  mv->has_t = (k_a > 0 && !mv->fallback_uniform && mv->lo > 0) ? 1 : 0;
 }
 
 struct SelParams {
@@ -130,8 +374,27 @@ __device__ __forceinline__ double sel_prob(const SelParams &P, const long long *
 }
 
 // pass 1: selection flags (bytes) + per-tile counts
-__global__ void k_select_flags(SelParams P, const long long *__restrict__ q64, int64_t n,
+// MVS (mode 2): the threshold, mu and the all-zero fallback come from the device state
+__device__ __forceinline__ SelParams sel_params(const SelParams &P0, const MvsDev *mv) {
+  SelParams P = P0;
+  if (mv && P.mode == 2) {
+    if (mv->fallback_uniform) {
+      P.mode = 1;
+    } else {
+      P.has_t = mv->has_t;
+      P.t = mv->tstar;
+      P.mu = mv->mu;
+    }
+  } else if (mv && P.mode == 3) {  // GOSS: the top set threshold (p_rest stays the host's)
+    P.has_t = mv->has_t;
+    P.t = mv->tstar;
+  }
+  return P;
+}
+
+__global__ void k_select_flags(SelParams P0, const MvsDev *mv, const long long *__restrict__ q64, int64_t n,
                                uint8_t *__restrict__ flags, int *__restrict__ tile_cnt) {
+  const SelParams P = sel_params(P0, mv);
   int64_t base = (int64_t)blockIdx.x * kSelTile;
   int c = 0;
 #pragma unroll
@@ -177,11 +440,12 @@ __global__ void k_scan_exclusive(const int *__restrict__ in, int64_t n, long lon
 }
 
 // pass 2: ordered scatter of the selected rows; g' = g/p (MVS) in double; max |g'|, |h'|.
-__global__ void k_select_scatter(SelParams P, const long long *__restrict__ q64,
+__global__ void k_select_scatter(SelParams P0, const MvsDev *mv, const long long *__restrict__ q64,
                                  const uint8_t *__restrict__ flags, const long long *__restrict__ tile_off,
                                  const float *__restrict__ g, const float *__restrict__ h, int64_t n,
                                  int32_t *__restrict__ sel_rows, double *__restrict__ gs,
                                  double *__restrict__ hs, unsigned long long *maxbits /*[2]*/) {
+  const SelParams P = sel_params(P0, mv);
   __shared__ int s_flags[kSelTile];
   __shared__ int s_warp[kSelThreads / 32];
   int64_t base = (int64_t)blockIdx.x * kSelTile;
@@ -357,6 +621,40 @@ static void ensure_sample_buffers(oocgb_data d) {
   }
 }
 
+static MvsDev *mvs_state(oocgb_data d) {
+  oocgb_ctx c = d->ctx;
+  if (!d->d_mvs) {
+    d->d_mvs = dmalloc(sizeof(MvsDev));
+    d->d_mvs_stats = (unsigned long long *)dmalloc(sizeof(unsigned long long) * 3 * kMvsBuckets);
+  }
+  if (!c->mvs_attr) {  // per ctx (= per device)
+    OOCGB_CK(cudaFuncSetAttribute(k_mvs_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, kMvsDecideSmem));
+    OOCGB_CK(cudaFuncSetAttribute(k_goss_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, kMvsDecideSmem));
+    c->mvs_attr = true;
+  }
+  return (MvsDev *)d->d_mvs;
+}
+
+// the radix passes over g_hat_q (<= ceil((63 - ceil_log2 n) / 11), each followed by `decide`)
+template <class Decide>
+static void mvs_passes(oocgb_data d, MvsDev *mv, unsigned long long *stats, double lam, int log2n, Decide decide) {
+  oocgb_ctx c = d->ctx;
+  const int64_t n = d->n_local;
+  long long *buf0 = reinterpret_cast<long long *>(d->d_gs), *buf1 = reinterpret_cast<long long *>(d->d_hs);
+  const int npass = std::max(1, (63 - log2n + 10) / 11);
+  for (int p = 0; p < npass; ++p) {
+    if (p == 0)
+      k_mvs_pass<1><<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, lam, d->d_tmp64, n, buf0, buf1, mv, stats);
+    else if (p == 1)
+      k_mvs_pass<2><<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, lam, d->d_tmp64, n, buf0, buf1, mv, stats);
+    else
+      k_mvs_pass<3><<<c->num_sms * 8, 256, 0, c->stream>>>(d->d_g, d->d_h, lam, d->d_tmp64, n, buf0, buf1, mv,
+                                                            stats);
+    OOCGB_CK(cudaGetLastError());
+    decide();
+  }
+}
+
 void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64_t seed,
                  uint64_t round, int quant_bits, oocgb_sample_info *info, double goss_b) {
   oocgb_ctx c = d->ctx;
@@ -366,8 +664,6 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
   d->has_sample = false;
   oocgb_sample_info si{};
   si.k_star = -1;
-  unsigned long long *d_u = (unsigned long long *)c->d_small;  // small scratch
-  unsigned long long *h_u = (unsigned long long *)c->h_small;
   const uint64_t f_q = (uint64_t)nearbyint(ratio * 4294967296.0);
   const __int128 two32 = (__int128)1 << 32;
   const __int128 F = (__int128)f_q * (__int128)d->n_global;
@@ -379,110 +675,28 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
   P.p_uniform = (double)f_q * 0x1.0p-32;
   int eff_mode = mode;
 
+  const MvsDev *mvp = nullptr;
   if (mode == OOCGB_SAMPLE_MVS) {
-    // Eq. 9 + global max
-    OOCGB_CK(cudaMemsetAsync(d_u, 0, 8, c->stream));
+    // R9 on the device (no host round trip): max g_hat, then the radix descent of the exact
+    // threshold over g_hat_q (<= ceil((63 - ceil_log2 n) / 11) passes), then k*, R, mu
+    MvsDev *mv = mvs_state(d);
+    unsigned long long *stats = d->d_mvs_stats;
+    const int log2n = ceil_log2(d->n_global);
+    OOCGB_CK(cudaMemsetAsync(&mv->maxbits, 0, 8, c->stream));
     if (n > 0)
-      k_ghat<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, n, mvs_lambda,
-                                                    (double *)d->d_tmp64, d_u);
-    allreduce_max_u64(c, d_u, 1);
-    OOCGB_CK(cudaMemcpyAsync(h_u, d_u, 8, cudaMemcpyDeviceToHost, c->stream));
-    OOCGB_CK(cudaStreamSynchronize(c->stream));
-    double gmax;
-    memcpy(&gmax, h_u, 8);
-    if (gmax == 0.0) {
-      eff_mode = OOCGB_SAMPLE_UNIFORM;  // S:L320 fallback
-      si.fallback_uniform = 1;
-    } else {
-      int kM;
-      frexp(gmax, &kM);
-      int e = (62 - ceil_log2(d->n_global)) - kM;
-      si.e_prime = e;
-      if (n > 0) k_ghat_q<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, ldexp(1.0, e));
-      // radix descent over [0, 2^qbits), qbits = bit width of the largest g_hat_q (known from
-      // the global max), in passes of <= 11 bits: starting at the top set bit keeps the first
-      // pass's buckets spread (no all-in-bucket-0 contention at large n)
-      const unsigned long long qmax = (unsigned long long)nearbyint(ldexp(gmax, e));
-      const int qbits = qmax ? 64 - __builtin_clzll(qmax) : 1;
-      unsigned long long lo = 0, above = 0, below_sum = 0;
-      long long below_max = -1, fallback = -1;
-      bool have_fb = false, found = false;
-      long long tstar = -1;
-      unsigned long long *d_stats = d_u + 16;
-      unsigned long long *h_stats = h_u + 16;
-      for (int bits_left = qbits; bits_left > 0 && !found;) {
-        const int wdt = std::min(11, bits_left);
-        const int sh = bits_left - wdt;
-        bits_left -= wdt;
-        int nb = 1 << wdt;
-        OOCGB_CK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 3 * nb, c->stream));
-        if (n > 0)
-          k_radix_stats<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, lo, sh, nb, d_stats,
-                                                               d_stats + nb, d_stats + 2 * nb);
-        OOCGB_CK(cudaGetLastError());
-        allreduce_sum_i64(c, (long long *)d_stats, 2 * (size_t)nb);
-        allreduce_max_u64(c, d_stats + 2 * nb, nb);
-        OOCGB_CK(cudaMemcpyAsync(h_stats, d_stats, sizeof(unsigned long long) * 3 * nb,
-                                 cudaMemcpyDeviceToHost, c->stream));
-        OOCGB_CK(cudaStreamSynchronize(c->stream));
-        const unsigned long long *cnt = h_stats, *sum = h_stats + nb, *mx = h_stats + 2 * nb;
-        // evaluate P at every edge j = 0..nb (edge value lo + j << sh)
-        std::vector<unsigned long long> suf_cnt(nb + 1, 0);
-        for (int j = nb - 1; j >= 0; --j) suf_cnt[j] = suf_cnt[j + 1] + cnt[j];
-        int jstar = -1;
-        long long A_at_jstar = -1;
-        unsigned long long Rj = below_sum;
-        long long Aj = below_max;
-        for (int j = 0; j <= nb; ++j) {
-          if (j > 0) {
-            Rj += sum[j - 1];
-            if (cnt[j - 1]) Aj = std::max<long long>(Aj, (long long)mx[j - 1]);
-          }
-          unsigned long long kj = above + suf_cnt[j];
-          bool Pj = false;
-          if (Aj >= 0 && Rj > 0) {
-            __int128 lhs = (__int128)Aj * (F - (__int128)kj * two32);
-            __int128 rhs = two32 * (__int128)Rj;
-            Pj = lhs < rhs;
-          }
-          if (Pj) { jstar = j; A_at_jstar = Aj; }
-        }
-        if (jstar < 0) {
-          if (have_fb) { tstar = fallback; found = true; break; }
-          // No edge is true and nothing lies below lo: the bottom edge is degenerate (no
-          // A below it), so t* — if it exists — is inside bucket 0.  Descend without a fallback.
-          if (sh == 0) { found = true; break; }  // no threshold: every non-zero row gets p = 1
-          above += suf_cnt[1];
-          continue;
-        }
-        if (sh == 0 || jstar == nb) { tstar = A_at_jstar; found = true; break; }
-        fallback = A_at_jstar;
-        have_fb = true;
-        for (int j = 0; j < jstar; ++j) {
-          below_sum += sum[j];
-          if (cnt[j]) below_max = std::max<long long>(below_max, (long long)mx[j]);
-        }
-        above += suf_cnt[jstar + 1];
-        lo += (unsigned long long)jstar << sh;
-      }
-      if (tstar >= 0) {
-        OOCGB_CK(cudaMemsetAsync(d_u, 0, 16, c->stream));
-        if (n > 0) k_threshold_totals<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, tstar, d_u);
-        allreduce_sum_i64(c, (long long *)d_u, 2);
-        OOCGB_CK(cudaMemcpyAsync(h_u, d_u, 16, cudaMemcpyDeviceToHost, c->stream));
-        OOCGB_CK(cudaStreamSynchronize(c->stream));
-        unsigned long long kstar = h_u[0], R = h_u[1];
-        double mu = ((double)(long long)R * 4294967296.0) / (double)(F - (__int128)kstar * two32);
-        P.has_t = 1;
-        P.t = tstar;
-        P.mu = mu;
-        si.k_star = (int64_t)kstar;
-        si.mu = mu;
-      } else {
-        P.has_t = 0;
-        si.k_star = -1;
-      }
-    }
+      k_mvs_ghat_max<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, n, mvs_lambda, &mv->maxbits);
+    allreduce_max_u64(c, &mv->maxbits, 1);
+    k_mvs_init<<<1, 256, 0, c->stream>>>(mv, log2n, stats);
+    mvs_passes(d, mv, stats, mvs_lambda, log2n, [&]() {
+      allreduce_sum_i64(c, (long long *)stats, 2 * (size_t)kMvsBuckets);
+      allreduce_max_u64(c, stats + 2 * kMvsBuckets, kMvsBuckets);
+      k_mvs_decide<<<1, 1024, kMvsDecideSmem, c->stream>>>(mv, stats, f_q, d->n_global);
+    });
+    if (n > 0) k_mvs_totals<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, mv);
+    allreduce_sum_i64(c, (long long *)mv->tot, 2);
+    k_mvs_finish<<<1, 1, 0, c->stream>>>(mv, f_q, d->n_global);
+    OOCGB_CK(cudaGetLastError());
+    mvp = mv;
   }
   if (mode == OOCGB_SAMPLE_GOSS) {
     // R25: |g| quantised like g_hat (lambda = 0: sqrt(g^2) = |g| exactly), the k_a-th largest
@@ -494,51 +708,22 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
     const long long k_a = (long long)(((unsigned __int128)a_q * (unsigned __int128)d->n_global + (1ULL << 31)) >> 32);
     P.p_uniform = p_rest;
     P.has_t = 0;
-    OOCGB_CK(cudaMemsetAsync(d_u, 0, 8, c->stream));
-    if (n > 0)
-      k_ghat<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, n, 0.0, (double *)d->d_tmp64, d_u);
-    allreduce_max_u64(c, d_u, 1);
-    OOCGB_CK(cudaMemcpyAsync(h_u, d_u, 8, cudaMemcpyDeviceToHost, c->stream));
-    OOCGB_CK(cudaStreamSynchronize(c->stream));
-    double gmax;
-    memcpy(&gmax, h_u, 8);
-    int e = 0;
-    if (gmax > 0.0) {
-      int kM;
-      frexp(gmax, &kM);
-      e = (62 - ceil_log2(d->n_global)) - kM;
-    }
-    si.e_prime = e;
-    if (n > 0) k_ghat_q<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, ldexp(1.0, e));
-    if (k_a > 0 && gmax > 0.0) {
-      // radix select of the k_a-th largest value over [0, 2^qbits), passes of <= 11 bits
-      const unsigned long long qmax = (unsigned long long)nearbyint(ldexp(gmax, e));
-      const int qbits = qmax ? 64 - __builtin_clzll(qmax) : 1;
-      unsigned long long lo = 0, above = 0;
-      unsigned long long *d_stats = d_u + 16;
-      unsigned long long *h_stats = h_u + 16;
-      for (int bits_left = qbits; bits_left > 0;) {
-        const int wdt = std::min(11, bits_left);
-        const int sh = bits_left - wdt;
-        bits_left -= wdt;
-        const int nb = 1 << wdt;
-        OOCGB_CK(cudaMemsetAsync(d_stats, 0, sizeof(unsigned long long) * 3 * nb, c->stream));
-        if (n > 0)
-          k_radix_stats<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_tmp64, n, lo, sh, nb, d_stats,
-                                                               d_stats + nb, d_stats + 2 * nb);
-        OOCGB_CK(cudaGetLastError());
-        allreduce_sum_i64(c, (long long *)d_stats, (size_t)nb);
-        OOCGB_CK(cudaMemcpyAsync(h_stats, d_stats, sizeof(unsigned long long) * nb, cudaMemcpyDeviceToHost, c->stream));
-        OOCGB_CK(cudaStreamSynchronize(c->stream));
-        int j = nb - 1;
-        for (; j > 0; --j) {
-          if (above + h_stats[j] >= (unsigned long long)k_a) break;
-          above += h_stats[j];
-        }
-        lo += (unsigned long long)j << sh;
-      }
-      if (lo > 0) { P.has_t = 1; P.t = (long long)lo; }
-    }
+    // the k_a-th largest |g|_q by the device radix select (the MVS passes with lambda = 0:
+    // sqrt(g^2) = |g| exactly), no host round trip
+    MvsDev *mv = mvs_state(d);
+    unsigned long long *stats = d->d_mvs_stats;
+    const int log2n = ceil_log2(d->n_global);
+    OOCGB_CK(cudaMemsetAsync(&mv->maxbits, 0, 8, c->stream));
+    if (n > 0) k_mvs_ghat_max<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, n, 0.0, &mv->maxbits);
+    allreduce_max_u64(c, &mv->maxbits, 1);
+    k_mvs_init<<<1, 256, 0, c->stream>>>(mv, log2n, stats);
+    if (k_a > 0) mvs_passes(d, mv, stats, 0.0, log2n, [&]() {
+      allreduce_sum_i64(c, (long long *)stats, (size_t)kMvsBuckets);
+      k_goss_decide<<<1, 1024, kMvsDecideSmem, c->stream>>>(mv, stats, (unsigned long long)k_a);
+    });
+    k_goss_finish<<<1, 1, 0, c->stream>>>(mv, k_a);
+    OOCGB_CK(cudaGetLastError());
+    mvp = mv;
     si.k_star = k_a;
     si.mu = p_rest;
     eff_mode = OOCGB_SAMPLE_GOSS;
@@ -547,6 +732,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
 
   if (!d->d_ss) {
     d->d_ss = (SampleState *)dmalloc(sizeof(SampleState));
+    OOCGB_CK(cudaMemsetAsync(d->d_ss, 0, sizeof(SampleState), c->stream));  // every field defined
     OOCGB_CK(cudaMallocHost(&d->h_ss, sizeof(SampleState)));
   }
   SampleState *ss = d->d_ss;
@@ -575,16 +761,26 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       tmp_alloc.push_back(toff);
     }
     if (n > 0) {
-      k_select_flags<<<(unsigned)tiles, kSelThreads, 0, c->stream>>>(P, d->d_tmp64, n, flags, tcnt);
+      k_select_flags<<<(unsigned)tiles, kSelThreads, 0, c->stream>>>(P, mvp, d->d_tmp64, n, flags, tcnt);
       k_scan_exclusive<<<1, 1024, 0, c->stream>>>(tcnt, tiles, toff, &ss->n_sel_local);
       k_select_scatter<<<(unsigned)tiles, kSelThreads, 0, c->stream>>>(
-          P, d->d_tmp64, flags, toff, d->d_g, d->d_h, n, d->d_sel_rows, d->d_gs, d->d_hs, ss->maxbits);
+          P, mvp, d->d_tmp64, flags, toff, d->d_g, d->d_h, n, d->d_sel_rows, d->d_gs, d->d_hs, ss->maxbits);
       OOCGB_CK(cudaGetLastError());
     }
     OOCGB_CK(cudaMemcpyAsync(d->h_ss, ss, sizeof(SampleState), cudaMemcpyDeviceToHost, c->stream));
+    MvsDev *hmv = reinterpret_cast<MvsDev *>((char *)c->h_small + (900 << 10));
+    if (mvp) OOCGB_CK(cudaMemcpyAsync(hmv, mvp, sizeof(MvsDev), cudaMemcpyDeviceToHost, c->stream));
     OOCGB_CK(cudaStreamSynchronize(c->stream));
     for (void *p : tmp_alloc) dfree(p);
     d->n_sel = d->h_ss->n_sel_local;
+    if (mvp && mode == OOCGB_SAMPLE_MVS) {  // R9 results for the info record
+      si.e_prime = hmv->e;
+      si.fallback_uniform = hmv->fallback_uniform;
+      si.k_star = hmv->has_t ? hmv->kstar : -1;
+      si.mu = hmv->has_t ? hmv->mu : 0.0;
+    } else if (mvp) {
+      si.e_prime = hmv->e;
+    }
   }
   allreduce_max_u64(c, ss->maxbits, 2);
   k_sstate_globalise<<<1, 1, 0, c->stream>>>(ss);
@@ -613,8 +809,11 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       dfree(d->d_sampled_page);
       d->d_sampled_page = nullptr;
       d->sampled_cap = 0;
-      d->d_sampled_page = (uint8_t *)dmalloc((size_t)std::max<int64_t>(1, d->n_sel) * d->stride);  // tiled, cap rows
-      d->sampled_cap = std::max<int64_t>(1, d->n_sel);
+      // tiled, cap rows; 1/8 headroom (the page pitch is part of the build graph's key)
+      const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(d->n_sel, d->n_local),
+                                                                 d->n_sel + d->n_sel / 8 + 4096));
+      d->d_sampled_page = (uint8_t *)dmalloc((size_t)cap * d->stride);
+      d->sampled_cap = cap;
     }
     if (d->all_selected) {
       // f = 1: every page streams (H2D) and is re-laid out tiled on the device

@@ -43,6 +43,7 @@ struct RoundParams {
   double sg_inv, sh_inv;
   long long h_min;   // candidate valid iff H_L >= h_min and H_R >= h_min (exact form of R13)
   float sg_inv_f, sh_inv_f;
+  float fold_c, fold_lq;  // the float pre-filter's folded scales c = sg^2 / sh, lambda / sh (per round)
   int prefilter;     // 0: scales outside float's safe range -> every candidate evaluated exactly
 };
 
@@ -97,6 +98,9 @@ struct Work {
   int hist_grid = 0;
   RoundParams *d_rp = nullptr;     // device copy of the per-call scalars
   RoundParams *h_rp = nullptr;     // pinned staging
+  oocgb::DNode *h_dn = nullptr;    // pinned export staging (node records, control block, predict nodes):
+  oocgb::LevelCtl *h_ctl = nullptr;  // the tree's predict nodes go up asynchronously, so build_tree
+  oocgb::PNode *h_pn = nullptr;    // synchronises the host once per tree
   cudaGraphExec_t graph = nullptr; // captured level loop of the last key
   GraphKey key{};
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> graph_events;  // profiling
@@ -131,12 +135,14 @@ __device__ __forceinline__ long long clamp_ll(double x) {
 
 __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restrict__ ss, RoundParams *rp,
                              double lambda, double mcw, double eta, Seg *segs,
-                             Pair *pairs, LevelCtl *ctl, int n_sel, int n_fg, int target_items,
+                             Pair *pairs, LevelCtl *ctl, int n_sel_arg, int n_fg, int target_items,
                              int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
                              const int2 *q_in, int2 *q_out, int ridx_mode, int *chunk_pair, int2 *ent,
                              int ent_cap) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nth = gridDim.x * blockDim.x;
+  // n_sel_arg < 0: the sample's row count from the device sample state (graph independent of it)
+  const int n_sel = n_sel_arg >= 0 ? n_sel_arg : (int)ss->n_sel_local;
   {
     const long long cr = hist_chunk_rows(n_sel, 1, n_fg, target_items, kmax);
     const int nch = (int)((n_sel + cr - 1) / cr);
@@ -160,6 +166,8 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
     P.sh_inv = ldexp(1.0, -ss->e_h);
     P.sg_inv_f = ldexpf(1.0f, -ss->e_g);
     P.sh_inv_f = ldexpf(1.0f, -ss->e_h);
+    P.fold_c = P.sg_inv_f * P.sg_inv_f / P.sh_inv_f;
+    P.fold_lq = (float)lambda / P.sh_inv_f;
     // R13 exactly, in integers: hl = HL 2^-e_h is exact, so hl >= mcw <=> HL >= ceil(mcw 2^e_h)
     // and hl + lambda > 0 <=> HL >= floor(-lambda 2^e_h) + 1 (clamped to the int64 range)
     const long long t1 = clamp_ll(ceil(ldexp(mcw, ss->e_h)));
@@ -478,7 +486,7 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
   // terms are tL = c GL^2 / (HL + lq) with c = sg^2 / sh and lq = lambda / sh, the same values up
   // to rounding order as the unfolded form below; the gain and its bound scale by c exactly
   // (the pre-filter is on only when c and lq are normal floats, see k_init_build).
-  const float c = rp.sg_inv_f * rp.sg_inv_f / rp.sh_inv_f, lq = lamf / rp.sh_inv_f;
+  const float c = rp.fold_c, lq = rp.fold_lq;  // hoisted to k_init_build (same values)
   const float chalf = 0.5f * c, tolc = 0x1p-18f * c, K = 0.5f * tPf + gamf;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -978,7 +986,8 @@ struct PlanArgs {
   Pair *pairs;
   int *tile_seg;
   int *chunk_pair;  // histogram chunk -> pair (k_hist's item lookup)
-  int n, n_fg, target_items, kmax;
+  const long long *n_dev;  // the sample's rows (device sample state)
+  int n_fg, target_items, kmax;
   int2 *ent;        // eval work lists (EvalArgs::ent)
   int ent_cap;
 };
@@ -992,7 +1001,7 @@ __device__ unsigned long long g_part_t0 = ~0ull;  // trace build only: first par
 // 32-B rows for the bin gathers, consecutive destinations).  (u, thread) order is position order:
 // left/right ranks come from warp ballots plus a 64-entry (u, warp) scan.
 __global__ void __launch_bounds__(kPartThreads, 4)
-k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
+k_part_fused(const long long *__restrict__ n_dev, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
              const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, size_t pitch, int lgw,
              const int32_t *__restrict__ ridx, const int2 *__restrict__ q, int32_t *__restrict__ ridx_out,
              int2 *__restrict__ q_out, int *__restrict__ cur, const int *__restrict__ tile_seg, int plan_inline,
@@ -1009,8 +1018,11 @@ k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
   __shared__ int s_pre[8][kPartThreads / 32];  // (left | right << 16) per (u, warp), then exclusive prefix
   __shared__ int s_tot;
   const int n_segs = ctl->n_segs;
+  const int n = (int)*n_dev;  // the sample's rows (the grid covers the capacity)
+  const int n_tiles = (n + kPartTile - 1) / kPartTile;
   const int t0 = blockIdx.x * kPartTile;
   const int t1 = min(n, t0 + kPartTile);
+  if (t0 < n) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int rows[8], sg[8];
   int2 qs[8];
@@ -1019,7 +1031,7 @@ k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
     const int p = t0 + u * kPartThreads + threadIdx.x;
     if (p < t1) { rows[u] = ridx[p]; qs[u] = q[p]; }
   }
-  load_tile_segs(T, segs, n_segs, dn, tile_seg, blockIdx.x, gridDim.x);
+  load_tile_segs(T, segs, n_segs, dn, tile_seg, blockIdx.x, n_tiles);
   const bool staged = T.count <= kTileSegs;
   uint32_t rbits = 0, lbits = 0;  // right / left (of a split segment) per u
   {
@@ -1133,6 +1145,7 @@ k_part_fused(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ c
       q_out[pos] = qs[u];
     }
   }
+  }  // t0 < n
   if (!plan_inline) return;
   // world == 1: the last tile to finish plans the next level (its cursors are final).  The plan
   // reads only the cursors (atomics, at L2); the barrier + one thread's fence order this block's
@@ -1226,7 +1239,7 @@ __device__ void plan_level_loop(const PlanArgs &A) {
   for (int i = threadIdx.x; i < 2 * nseg_carry; i += T) A.cur_next[i] = 0;
   // tile -> first segment table of the next level (segs_next written above by this block)
   __syncthreads();
-  const int n_tiles = (A.n + kPartTile - 1) / kPartTile;
+  const int n_tiles = (int)((*A.n_dev + kPartTile - 1) / kPartTile);
   for (int sn = threadIdx.x; sn < nseg_carry; sn += T) {
     const Seg S = segs_next[sn];
     if (S.count == 0) continue;
@@ -1318,7 +1331,7 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
   const int ns = block_excl_scan(s < n_segs ? 1 + split : 0, &tot_s);
   const int np = block_excl_scan(split, &tot_p);
   Pair pr{};
-  const int n_tiles = (A.n + kPartTile - 1) / kPartTile;
+  const int n_tiles = (int)((*A.n_dev + kPartTile - 1) / kPartTile);
   // next-level segment starts staged in shared memory for the tile table (filled block-wide below)
   __shared__ int s_begin[2 * 1024];
   auto emit = [&](int idx, const Seg &C) {
@@ -1471,15 +1484,22 @@ static void ensure_work(oocgb_data d, int D) {
   Work *&w = d->work;
   const int m = d->m;
   const int n_fg = (m + kFG - 1) / kFG;
-  const int64_t n = std::max<int64_t>(1, d->n_sel);
+  // capacity: the build's CUDA graph depends on it, not on the sample's row count (which the kernels
+  // read from the device sample state), so a sampled round (n_sel varies) reuses the graph; a
+  // sample keeps 1/8 headroom up to the data's row count
+  const int64_t need = std::max<int64_t>(1, d->n_sel);
+  const int64_t n = d->all_selected ? need : std::min<int64_t>(std::max<int64_t>(need, d->n_local),
+                                                               need + need / 8 + 4096);
   const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
   const int hist_grid = c->num_sms * kHistCtasPerSm;
   const int target = hist_grid;
   const int64_t max_pairs = D > 0 ? (1LL << (D - 1)) : 1;
-  // bound of hist_chunk_rows' item count: C <= n_pairs - 1 + ceil(rows / kmax) + ceil(grid / n_fg)
-  int64_t items = target + (int64_t)n_fg * (((n + kmax - 1) / kmax) + max_pairs + 2) + n_fg;
+  // bound of hist_chunk_rows' item count: C <= 2 n_pairs - 1 + ceil(rows / kmax) + ceil(grid / n_fg)
+  auto items_for = [&](int64_t rows) { return target + (int64_t)n_fg * (((rows + kmax - 1) / kmax) + 2 * max_pairs + 2) + n_fg; };
+  const int64_t items = items_for(n);
   const bool need64 = c->coll || d->streamed;  // all-reduced / streamed int64 node histograms
-  if (w && w->cap_rows >= n && w->max_depth >= D && w->m == m && w->items_cap >= items && (!need64 || w->built64))
+  if (w && w->cap_rows >= need && w->max_depth >= D && w->m == m && w->items_cap >= items_for(need) &&
+      (!need64 || w->built64))
     return;
   free_work(d);
   w = new Work();
@@ -1513,6 +1533,9 @@ static void ensure_work(oocgb_data d, int D) {
   w->ctl = (LevelCtl *)dmalloc(sizeof(LevelCtl));
   w->d_rp = (RoundParams *)dmalloc(sizeof(RoundParams));
   OOCGB_CK(cudaMallocHost(&w->h_rp, sizeof(RoundParams)));
+  OOCGB_CK(cudaMallocHost(&w->h_dn, sizeof(DNode) * ((1LL << (D + 1)) - 1)));
+  OOCGB_CK(cudaMallocHost(&w->h_ctl, sizeof(LevelCtl)));
+  OOCGB_CK(cudaMallocHost(&w->h_pn, sizeof(PNode) * ((1LL << (D + 1)) - 1)));
   OOCGB_CK(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem));
 }
 
@@ -1528,6 +1551,9 @@ void free_work(oocgb_data d) {
   dfree(w->sw.slot_cur);
   d->streamed_row_node = nullptr;
   if (w->h_rp) cudaFreeHost(w->h_rp);
+  if (w->h_dn) cudaFreeHost(w->h_dn);
+  if (w->h_ctl) cudaFreeHost(w->h_ctl);
+  if (w->h_pn) cudaFreeHost(w->h_pn);
   drop_graph(w);
   delete w;
   d->work = nullptr;
@@ -1541,7 +1567,9 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   oocgb_ctx c = d->ctx;
   Work *w = d->work;
   const int m = d->m, n_fg = w->n_fg;
-  const int n = (int)d->n_sel;
+  // geometry from the capacity; the kernels read the sample's row count from the device
+  const int n = (int)w->cap_rows;
+  const long long *n_dev = &d->d_ss->n_sel_local;
   const int n_nodes = (1 << (D + 1)) - 1;
   const int kmax = (int)((0x7fffffffLL) >> d->quant_bits);
   const int target = w->hist_grid;  // one wave of items per level
@@ -1562,7 +1590,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   if (keep_debug) OOCGB_CK(cudaMemsetAsync(w->dbg, 0, sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1), c->stream));
   OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
-      w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta, w->segs[0], w->pairs, w->ctl, n, n_fg, target, kmax,
+      w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta, w->segs[0], w->pairs, w->ctl, -1, n_fg, target, kmax,
       D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode, w->chunk_pair, w->ent, w->ent_cap);
   OOCGB_CK(cudaGetLastError());
   int cur = 0;
@@ -1604,11 +1632,11 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     PA.cur = w->seg_cur[lv & 1]; PA.seg_cnt = c->coll ? w->seg_cnt : nullptr;
     PA.cur_next = w->seg_cur[(lv + 1) & 1]; PA.pairs = w->pairs; PA.tile_seg = w->tile_seg;
     PA.chunk_pair = w->chunk_pair;
-    PA.n = n; PA.n_fg = n_fg; PA.target_items = target; PA.kmax = kmax;
+    PA.n_dev = n_dev; PA.n_fg = n_fg; PA.target_items = target; PA.kmax = kmax;
     PA.ent = w->ent; PA.ent_cap = w->ent_cap;
     const bool inline_plan = !c->coll && n > 0;
     if (n > 0) {
-      k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
+      k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n_dev, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
                                                           d->gw == 64 ? 6 : 5,
                                                           w->ridx[cur], w->q[cur], w->ridx[cur ^ 1], w->q[cur ^ 1],
                                                           w->seg_cur[lv & 1], w->tile_seg, inline_plan ? 1 : 0, PA);
@@ -1670,8 +1698,9 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     size_t need = sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1);
     if (w->dbg_bytes < need) { drop_graph(w); dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
   }
-  GraphKey key{n, D, m, ridx_mode, keep_debug ? 1 : 0, c->profiling ? 1 : 0, c->world, lambda, gamma, mcw, eta,
-               bins, pitch, d->quant_bits};
+  // keyed by the capacity, not the sample's row count: sampled rounds replay one graph
+  GraphKey key{(int)w->cap_rows, D, m, ridx_mode, keep_debug ? 1 : 0, c->profiling ? 1 : 0, c->world, lambda, gamma,
+               mcw, eta, bins, pitch, d->quant_bits};
   if (c->host_coll) {
     // host-callback collectives synchronise the stream: run the level loop directly
     drop_graph(w);
@@ -1697,11 +1726,11 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   if (!c->host_coll) OOCGB_CK(cudaGraphLaunch(w->graph, c->stream));
   const int cur = w->final_cur;
   // export
-  std::vector<DNode> hn(n_nodes);
-  LevelCtl hctl;
-  OOCGB_CK(cudaMemcpyAsync(hn.data(), w->dnodes, sizeof(DNode) * n_nodes, cudaMemcpyDeviceToHost, c->stream));
-  OOCGB_CK(cudaMemcpyAsync(&hctl, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
+  const DNode *hn = w->h_dn;
+  OOCGB_CK(cudaMemcpyAsync(w->h_dn, w->dnodes, sizeof(DNode) * n_nodes, cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaMemcpyAsync(w->h_ctl, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
   OOCGB_CK(cudaStreamSynchronize(c->stream));
+  const LevelCtl hctl = *w->h_ctl;
   OOCGB_REQUIRE(hctl.error == 0, OOCGB_ERR_ARG, "build_tree: H + lambda <= 0 at a node (S:L406)");
   if (c->profiling) add_graph_timings(c, w);
   oocgb_tree t = new oocgb_tree_s();
@@ -1711,7 +1740,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   c->live_trees++;
   t->max_depth = D;
   t->nodes.resize(n_nodes);
-  std::vector<PNode> pn(n_nodes);
+  PNode *pn = w->h_pn;  // pinned: the H2D below is asynchronous (reused only after the next sync)
   for (int v = 0; v < n_nodes; ++v) {
     oocgb_node &o = t->nodes[v];
     o.feature = hn[v].feature;
@@ -1729,7 +1758,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
   t->ctx = c;
   t->pnodes_bytes = sizeof(PNode) * n_nodes;
   t->d_pnodes = (PNode *)pool_get(c, t->pnodes_bytes);
-  OOCGB_CK(cudaMemcpyAsync(t->d_pnodes, pn.data(), sizeof(PNode) * n_nodes, cudaMemcpyHostToDevice, c->stream));
+  OOCGB_CK(cudaMemcpyAsync(t->d_pnodes, pn, sizeof(PNode) * n_nodes, cudaMemcpyHostToDevice, c->stream));
   if (keep_debug) {
     t->debug = true;
     size_t cnt = hsz * (size_t)std::max(0, (1 << D) - 1);
@@ -1771,8 +1800,7 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
       }
     }
   }
-  OOCGB_CK(cudaStreamSynchronize(c->stream));
-  return t;
+  return t;  // one host synchronisation per tree (the export); predict nodes follow on the stream
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1975,11 +2003,11 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     launch_eval(A, n_slots, c->num_sms, c->stream);
   }
   // export (same as the in-core path)
-  std::vector<DNode> hn(n_nodes);
-  LevelCtl hctl;
-  OOCGB_CK(cudaMemcpyAsync(hn.data(), w->dnodes, sizeof(DNode) * n_nodes, cudaMemcpyDeviceToHost, c->stream));
-  OOCGB_CK(cudaMemcpyAsync(&hctl, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
+  const DNode *hn = w->h_dn;
+  OOCGB_CK(cudaMemcpyAsync(w->h_dn, w->dnodes, sizeof(DNode) * n_nodes, cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaMemcpyAsync(w->h_ctl, w->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
   OOCGB_CK(cudaStreamSynchronize(c->stream));
+  const LevelCtl hctl = *w->h_ctl;
   OOCGB_REQUIRE(hctl.error == 0, OOCGB_ERR_ARG, "build_tree: H + lambda <= 0 at a node (S:L406)");
   oocgb_tree t = new oocgb_tree_s();
   t->owner = d;
@@ -1988,7 +2016,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   c->live_trees++;
   t->max_depth = D;
   t->nodes.resize(n_nodes);
-  std::vector<PNode> pn(n_nodes);
+  PNode *pn = w->h_pn;  // pinned: the H2D below is asynchronous (reused only after the next sync)
   for (int v = 0; v < n_nodes; ++v) {
     oocgb_node &o = t->nodes[v];
     o.feature = hn[v].feature; o.split_bin = hn[v].split_bin; o.split_value = hn[v].split_value;
@@ -2001,7 +2029,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   t->ctx = c;
   t->pnodes_bytes = sizeof(PNode) * n_nodes;
   t->d_pnodes = (PNode *)pool_get(c, t->pnodes_bytes);
-  OOCGB_CK(cudaMemcpyAsync(t->d_pnodes, pn.data(), sizeof(PNode) * n_nodes, cudaMemcpyHostToDevice, c->stream));
+  OOCGB_CK(cudaMemcpyAsync(t->d_pnodes, pn, sizeof(PNode) * n_nodes, cudaMemcpyHostToDevice, c->stream));
   if (keep_debug) {
     t->debug = true;
     size_t cnt = hsz * (size_t)std::max(0, (1 << D) - 1);
