@@ -51,6 +51,8 @@ enum { OOCGB_SAMPLE_NONE = 0, OOCGB_SAMPLE_UNIFORM = 1, OOCGB_SAMPLE_MVS = 2, OO
 
 /* Exported tree node, heap order: children of i are 2i+1 (left: bin <= split_bin, i.e.
  * x <= split_value) and 2i+2.  feature = -1 leaf, -2 absent slot below a leaf.
+ * default_left (R27): a row MISSING the split feature goes left (1) or right (0); always 0 for
+ * data without missing values.
  * leaf_value = (float)(eta * -G/(H+lambda)) (Eq. 6, R15) is set for every present node.
  * sum_g/sum_h are the node's dequantised gradient sums over the SAMPLED rows (scaled by
  * 1/p); n_rows the number of sampled rows in the node, summed over all ranks.           */
@@ -63,6 +65,8 @@ typedef struct {
   double sum_g;
   double sum_h;
   int64_t n_rows;
+  int32_t default_left;
+  int32_t pad;
 } oocgb_node;
 
 typedef struct {
@@ -76,6 +80,8 @@ typedef struct {
   int64_t n_pages;        /* ELLPACK pages (1 for a single device page)                      */
   int64_t rows_per_page;  /* floor(page_bytes / row_stride), last page holds the remainder   */
   int64_t total_cuts;     /* sum_j B_j                                                       */
+  int32_t has_missing;    /* R27: some value is missing (NaN / absent CSR entry), symbol 255  */
+  int32_t pad;
 } oocgb_info;
 
 typedef struct {
@@ -119,10 +125,24 @@ int oocgb_ctx_create_hostcomm(int32_t device, int32_t rank, int32_t world, oocgb
  * sketch sample of <= 2^20 rows (all rows when n_rows_global <= 2^20), seed = `seed`.
  * page_bytes: ELLPACK page size (P:L326 uses 32 MiB); 0 = one page.  placement DEVICE keeps
  * the pages in HBM; PINNED_HOST keeps them in pinned host memory (out-of-core, Alg. 5 with
- * disk replaced by host RAM).  Errors: ERR_ARG (sizes, max_bin, non-finite X), ERR_NOMEM.  */
+ * disk replaced by host RAM).  Missing values (R27; the paper's pages are CSR):
+ * NaN marks a missing value; the cuts skip it, its symbol is 255 (so data with missing values
+ * needs max_bin <= 255) and every split learns a default direction for it.  Errors: ERR_ARG
+ * (sizes, max_bin, +-inf in X, missing values with max_bin 256), ERR_NOMEM.                */
 int oocgb_quantise(oocgb_ctx ctx, const float *X, int64_t n_rows, int64_t row0_global,
                    int64_t n_rows_global, int32_t n_features, int32_t max_bin,
                    int64_t page_bytes, int32_t placement, uint64_t seed, oocgb_data *out);
+
+/* Sparse CSR input (R27; "the training data is already parsed and written to disk
+ * in CSR pages"): row i of this rank holds values[indptr[i] .. indptr[i+1]) at feature indices
+ * indices[...] (each < n_features, no repeats within a row); absent entries are MISSING.
+ * indptr int64 [n_rows + 1] (indptr[0] may be non-zero: it is subtracted), indices int32 and
+ * values float32 [nnz]; host or device pointers.  Same cuts, pages and errors as
+ * oocgb_quantise on the dense matrix with NaN at the absent entries (bit-identical).       */
+int oocgb_quantise_csr(oocgb_ctx ctx, const int64_t *indptr, const int32_t *indices, const float *values,
+                       int64_t n_rows, int64_t row0_global, int64_t n_rows_global, int32_t n_features,
+                       int32_t max_bin, int64_t page_bytes, int32_t placement, uint64_t seed,
+                       oocgb_data *out);
 
 /* Streamed quantise (Alg. 3 + Alg. 5): sketch_begin, any number of sketch_push (pass 1, rows
  * in any order, each row pushed once), cuts_finalize, then pages_push with the rows in

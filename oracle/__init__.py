@@ -51,13 +51,15 @@ class OrcNode(ctypes.Structure):
         ("sum_g", ctypes.c_double),
         ("sum_h", ctypes.c_double),
         ("n_rows", ctypes.c_int64),
+        ("default_left", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
     ]
 
 
 NODE_DTYPE = np.dtype([
     ("feature", np.int32), ("split_bin", np.int32), ("split_value", np.float32),
     ("leaf_value", np.float32), ("gain", np.float64), ("sum_g", np.float64),
-    ("sum_h", np.float64), ("n_rows", np.int64),
+    ("sum_h", np.float64), ("n_rows", np.int64), ("default_left", np.int32), ("pad", np.int32),
 ])
 assert NODE_DTYPE.itemsize == ctypes.sizeof(OrcNode)
 
@@ -88,9 +90,9 @@ def _declare(L):
     L.orc_histogram.argtypes = [_p, _i32, _i32, _p, _i64, _p, _p, _p]
     L.orc_histogram.restype = None
     L.orc_build_tree.argtypes = [_p, _i32, _i32, _p, _p, _i64, _p, _p, _i32, _i32, _i32,
-                                 _d, _d, _d, _d, _p, _p, _p]
+                                 _d, _d, _d, _d, _i32, _p, _p, _p]
     L.orc_build_tree.restype = ctypes.c_int
-    L.orc_predict.argtypes = [_p, _i32, _i64, _p, _p]
+    L.orc_predict.argtypes = [_p, _i32, _i64, _p, _i32, _p]
     L.orc_predict.restype = None
     L.orc_logistic_grad.argtypes = [_p, _p, _i64, _p, _p]
     L.orc_logistic_grad.restype = None
@@ -222,9 +224,10 @@ def histogram(bins_: np.ndarray, m: int, rows, qg, qh) -> np.ndarray:
 # ---------------------------------------------------------------------------------------- O7-O10
 def build_tree(bins_: np.ndarray, m: int, cut_values, cut_ptrs, qg, qh, e_g: int, e_h: int,
                max_depth: int = 6, lam: float = 1.0, gamma: float = 0.0, mcw: float = 1.0,
-               eta: float = 0.1, want_hist: bool = False):
+               eta: float = 0.1, want_hist: bool = False, has_missing: bool = False):
     """O6-O10 on the selected rows (bins_ holds only the selected rows, in ascending global
-    order).  Returns (nodes structured array, leaf_of_row int32[n_sel], hist or None)."""
+    order).  has_missing (R27): symbol 255 is a missing value and every candidate is tried with
+    the missing rows on either side.  Returns (nodes, leaf_of_row int32[n_sel], hist or None)."""
     b = _c(bins_, np.uint8)
     n_sel = b.shape[0]
     cv = _c(cut_values, np.float32)
@@ -236,7 +239,7 @@ def build_tree(bins_: np.ndarray, m: int, cut_values, cut_ptrs, qg, qh, e_g: int
     lor = np.full(n_sel, -1, np.int32)
     hist = np.zeros(((1 << max_depth) - 1, m, 256, 2), np.int64) if want_hist else None
     rc = lib().orc_build_tree(_ptr(b), b.shape[1], m, _ptr(cp), _ptr(cv), n_sel, _ptr(qg), _ptr(qh),
-                              e_g, e_h, max_depth, lam, gamma, mcw, eta, _ptr(nodes), _ptr(lor),
+                              e_g, e_h, max_depth, lam, gamma, mcw, eta, int(has_missing), _ptr(nodes), _ptr(lor),
                               _ptr(hist) if want_hist else None)
     if rc != 0:
         raise OracleError(f"orc_build_tree rc={rc}")
@@ -244,11 +247,11 @@ def build_tree(bins_: np.ndarray, m: int, cut_values, cut_ptrs, qg, qh, e_g: int
 
 
 # ---------------------------------------------------------------------------------------- O11-O12
-def predict(bins_: np.ndarray, nodes: np.ndarray, margin: np.ndarray) -> np.ndarray:
+def predict(bins_: np.ndarray, nodes: np.ndarray, margin: np.ndarray, has_missing: bool = False) -> np.ndarray:
     b = _c(bins_, np.uint8)
     out = _c(margin, np.float32).copy()
     nd = np.ascontiguousarray(nodes, dtype=NODE_DTYPE)
-    lib().orc_predict(_ptr(b), b.shape[1], b.shape[0], _ptr(nd), _ptr(out))
+    lib().orc_predict(_ptr(b), b.shape[1], b.shape[0], _ptr(nd), int(has_missing), _ptr(out))
     return out
 
 
@@ -270,17 +273,17 @@ def auc_bruteforce(score, y) -> float:
 # ---------------------------------------------------------------------------------------- one round
 def boosting_round(bins_: np.ndarray, m: int, cut_values, cut_ptrs, margin, y, *, mode=SAMPLE_NONE,
                    ratio=1.0, mvs_lambda=1.0, seed=1, round_=0, max_depth=8, lam=1.0, gamma=0.0,
-                   mcw=1.0, eta=0.1, quant_bits=16, prev_tree=None):
+                   mcw=1.0, eta=0.1, quant_bits=16, prev_tree=None, has_missing=False):
     """One boosting round exactly as the product path runs it (SURVEY.md §3 stack 2):
     predict(tree_{t-1}) -> logistic gradients -> Sample -> fixed point -> BuildTree.
     Returns (tree nodes, new margin, sample dict)."""
     if prev_tree is not None:
-        margin = predict(bins_, prev_tree, margin)
+        margin = predict(bins_, prev_tree, margin, has_missing)
     g, h = logistic_grad(margin, y)
     s = sample(g, h, mode, ratio, mvs_lambda, seed, round_)
     sel = s["selected"].astype(bool)
     qg, e_g = quantise(s["gs"][sel], quant_bits)
     qh, e_h = quantise(s["hs"][sel], quant_bits)
     nodes, lor, _ = build_tree(bins_[sel], m, cut_values, cut_ptrs, qg, qh, e_g, e_h, max_depth,
-                               lam, gamma, mcw, eta)
+                               lam, gamma, mcw, eta, has_missing=has_missing)
     return nodes, margin, dict(s, e_g=e_g, e_h=e_h, qg=qg, qh=qh, leaf_of_row=lor)

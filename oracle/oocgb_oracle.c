@@ -28,6 +28,11 @@
  *                      Eq.6/Eq.8 closed forms, separable-feature tree, depth-0 leaf
  *   orc_predict        pinned: raw-value traversal == binned traversal, partition leaf map
  *   orc_logistic_grad  pinned: S:L486 closed form and finite differences
+ *
+ * Missing values (R27): NaN (dense input) = missing.  The cuts
+ * skip missing values, a missing value's symbol is 255 (data with missing values has at most
+ * 255 bins per feature), and every split candidate is tried with the missing rows on either side
+ * (the learned "default direction"); ties keep the lower bin, then missing-right.
  */
 #include <math.h>
 #include <stdint.h>
@@ -102,7 +107,8 @@ int orc_cuts(const float *X, int64_t n, int32_t m, int32_t max_bin, int64_t row0
     for (int64_t i = 0; i < n; ++i) {
       if (!orc_sketch_row_selected(n_global, seed, row0 + i)) continue;
       float x = X[i * m + j];
-      if (!isfinite(x)) { free(col); return 2; }
+      if (isnan(x)) continue;                  /* missing (R27): not part of the column */
+      if (isinf(x)) { free(col); return 2; }   /* reading 4 */
       double v = (double)x;
       if (v == 0.0) v = 0.0; /* canonicalise -0.0 (reading 4) */
       col[N++] = v;
@@ -145,8 +151,13 @@ int orc_bins(const float *X, int64_t n, int32_t m, const float *cut_values,
     for (int32_t j = 0; j < stride; ++j) bins[i * stride + j] = 0;
     for (int32_t j = 0; j < m; ++j) {
       float x = X[i * m + j];
-      if (!isfinite(x)) return 2;
       int32_t B = cut_ptrs[j + 1] - cut_ptrs[j];
+      if (isnan(x)) {                     /* missing (R27): symbol 255, needs B_j <= 255 */
+        if (B > 255) return 2;
+        bins[i * stride + j] = 255;
+        continue;
+      }
+      if (isinf(x)) return 2;
       int32_t b = B - 1;
       for (int32_t k = 0; k < B; ++k) {
         if (x <= cut_values[cut_ptrs[j] + k]) { b = k; break; }
@@ -386,6 +397,8 @@ typedef struct {
   double sum_g;
   double sum_h;
   int64_t n_rows;
+  int32_t default_left;  /* R27: rows missing the split feature go left */
+  int32_t pad;
 } orc_node;
 
 /* O7. EvaluateSplit (Eq. 8) by exhaustive enumeration over (j, b <= B_j - 2),
@@ -393,28 +406,35 @@ typedef struct {
  * Valid iff hL >= mcw, hR >= mcw and both H + lambda > 0 (R13).  Max gain, ties -> lowest j then lowest b (strict >
  * in ascending scan).  Returns 1 and fills (*bj, *bb, *bgain) when a split with gain > 0
  * exists (reading 13). */
+/* R27 (has_missing): every candidate is tried twice, missing rows right (dir 0: the left sums are
+ * the prefix) and left (dir 1: prefix + the missing bin 255's sums); scan order (j, b, dir). */
 static int orc_best_split(const int64_t *hist, int32_t m, const int32_t *cut_ptrs, int64_t G,
                           int64_t H, int e_g, int e_h, double lambda, double gamma, double mcw,
-                          int32_t *bj, int32_t *bb, double *bgain) {
+                          int has_missing, int32_t *bj, int32_t *bb, int32_t *bdir, double *bgain) {
   double gP = ldexp((double)G, -e_g), hP = ldexp((double)H, -e_h);
   double tP = (gP * gP) / (hP + lambda);
   int found = 0;
   double best = 0.0;
   for (int32_t j = 0; j < m; ++j) {
     int32_t B = cut_ptrs[j + 1] - cut_ptrs[j];
-    int64_t GL = 0, HL = 0;
+    int64_t Gm = has_missing ? hist[((int64_t)j * 256 + 255) * 2 + 0] : 0;
+    int64_t Hm = has_missing ? hist[((int64_t)j * 256 + 255) * 2 + 1] : 0;
+    int64_t GP = 0, HP = 0; /* prefix over the present bins 0..b */
     for (int32_t b = 0; b <= B - 2; ++b) {
-      GL += hist[((int64_t)j * 256 + b) * 2 + 0];
-      HL += hist[((int64_t)j * 256 + b) * 2 + 1];
-      int64_t GR = G - GL, HR = H - HL;
-      double gl = ldexp((double)GL, -e_g), hl = ldexp((double)HL, -e_h);
-      double gr = ldexp((double)GR, -e_g), hr = ldexp((double)HR, -e_h);
-      if (!(hl >= mcw && hr >= mcw && hl + lambda > 0.0 && hr + lambda > 0.0)) continue;
-      double tL = (gl * gl) / (hl + lambda);
-      double tR = (gr * gr) / (hr + lambda);
-      double gain = 0.5 * ((tL + tR) - tP) - gamma;
-      if (!found || gain > best) {
-        found = 1; best = gain; *bj = j; *bb = b;
+      GP += hist[((int64_t)j * 256 + b) * 2 + 0];
+      HP += hist[((int64_t)j * 256 + b) * 2 + 1];
+      for (int32_t dir = 0; dir <= (has_missing ? 1 : 0); ++dir) {
+        int64_t GL = GP + (dir ? Gm : 0), HL = HP + (dir ? Hm : 0);
+        int64_t GR = G - GL, HR = H - HL;
+        double gl = ldexp((double)GL, -e_g), hl = ldexp((double)HL, -e_h);
+        double gr = ldexp((double)GR, -e_g), hr = ldexp((double)HR, -e_h);
+        if (!(hl >= mcw && hr >= mcw && hl + lambda > 0.0 && hr + lambda > 0.0)) continue;
+        double tL = (gl * gl) / (hl + lambda);
+        double tR = (gr * gr) / (hr + lambda);
+        double gain = 0.5 * ((tL + tR) - tP) - gamma;
+        if (!found || gain > best) {
+          found = 1; best = gain; *bj = j; *bb = b; *bdir = dir;
+        }
       }
     }
   }
@@ -439,7 +459,7 @@ static float orc_leaf(int64_t G, int64_t H, int e_g, int e_h, double lambda, dou
 int orc_build_tree(const uint8_t *bins, int32_t stride, int32_t m, const int32_t *cut_ptrs,
                    const float *cut_values, int64_t n_sel, const int64_t *qg, const int64_t *qh,
                    int32_t e_g, int32_t e_h, int32_t max_depth, double lambda, double gamma,
-                   double mcw, double eta, orc_node *nodes, int32_t *leaf_of_row,
+                   double mcw, double eta, int32_t has_missing, orc_node *nodes, int32_t *leaf_of_row,
                    int64_t *hist_out) {
   if (max_depth < 0 || max_depth > 20) return 2;
   int64_t n_nodes = ((int64_t)1 << (max_depth + 1)) - 1;
@@ -451,7 +471,7 @@ int orc_build_tree(const uint8_t *bins, int32_t stride, int32_t m, const int32_t
   for (int64_t v = 0; v < n_nodes; ++v) {
     nodes[v].feature = -2; nodes[v].split_bin = 0; nodes[v].split_value = 0.0f;
     nodes[v].leaf_value = 0.0f; nodes[v].gain = 0.0; nodes[v].sum_g = 0.0;
-    nodes[v].sum_h = 0.0; nodes[v].n_rows = 0;
+    nodes[v].sum_h = 0.0; nodes[v].n_rows = 0; nodes[v].default_left = 0; nodes[v].pad = 0;
   }
   rows[0] = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_sel > 0 ? n_sel : 1));
   for (int64_t i = 0; i < n_sel; ++i) rows[0][i] = i;
@@ -478,21 +498,26 @@ int orc_build_tree(const uint8_t *bins, int32_t stride, int32_t m, const int32_t
       if (d == max_depth) continue; /* depth-D nodes are leaves */
       orc_histogram(bins, stride, m, rows[v], cnt[v], qg, qh, hist);
       if (hist_out) memcpy(hist_out + v * hsz, hist, sizeof(int64_t) * (size_t)hsz);
-      int32_t bj = -1, bb = -1;
+      int32_t bj = -1, bb = -1, bdir = 0;
       double bgain = 0.0;
-      if (!orc_best_split(hist, m, cut_ptrs, G, H, e_g, e_h, lambda, gamma, mcw, &bj, &bb, &bgain))
+      if (!orc_best_split(hist, m, cut_ptrs, G, H, e_g, e_h, lambda, gamma, mcw, has_missing, &bj, &bb,
+                          &bdir, &bgain))
         continue;
       nodes[v].feature = bj;
       nodes[v].split_bin = bb;
       nodes[v].split_value = cut_values[cut_ptrs[bj] + bb];
       nodes[v].gain = bgain;
-      /* O8. RepartitionInstances (Alg. 1): stable, bin <= b goes left */
+      nodes[v].default_left = bdir;
+      /* O8. RepartitionInstances (Alg. 1): stable, bin <= b goes left; a missing
+       * value (symbol 255, R27) goes the default direction */
       int64_t L = 2 * v + 1, R = 2 * v + 2;
       rows[L] = (int64_t *)malloc(sizeof(int64_t) * (size_t)(cnt[v] > 0 ? cnt[v] : 1));
       rows[R] = (int64_t *)malloc(sizeof(int64_t) * (size_t)(cnt[v] > 0 ? cnt[v] : 1));
       for (int64_t k = 0; k < cnt[v]; ++k) {
         int64_t r = rows[v][k];
-        if (bins[r * stride + bj] <= bb) rows[L][cnt[L]++] = r;
+        int b = bins[r * stride + bj];
+        int left = has_missing && b == 255 ? bdir : (b <= bb);
+        if (left) rows[L][cnt[L]++] = r;
         else rows[R][cnt[R]++] = r;
       }
       nodes[L].feature = -1;
@@ -508,14 +533,16 @@ int orc_build_tree(const uint8_t *bins, int32_t stride, int32_t m, const int32_t
   return 0;
 }
 
-/* O11. Eq. 1: margin_i (float32) += leaf(tree, bins_i); bin <= split_bin -> left. */
+/* O11. Eq. 1: margin_i (float32) += leaf(tree, bins_i); bin <= split_bin -> left;
+ * has_missing: symbol 255 (missing, R27) -> the node's default direction. */
 void orc_predict(const uint8_t *bins, int32_t stride, int64_t n, const orc_node *nodes,
-                 float *margin) {
+                 int32_t has_missing, float *margin) {
   for (int64_t i = 0; i < n; ++i) {
     int64_t v = 0;
     while (nodes[v].feature >= 0) {
       int b = bins[i * stride + nodes[v].feature];
-      v = (b <= nodes[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
+      int left = has_missing && b == 255 ? nodes[v].default_left : (b <= nodes[v].split_bin);
+      v = left ? 2 * v + 1 : 2 * v + 2;
     }
     margin[i] = margin[i] + nodes[v].leaf_value;
   }

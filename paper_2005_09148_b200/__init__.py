@@ -32,7 +32,7 @@ ABI_SYMBOLS = (
     "oocgb_tree_destroy", "oocgb_predict", "oocgb_update_margin", "oocgb_get_cuts",
     "oocgb_get_bins", "oocgb_get_sample", "oocgb_get_histogram", "oocgb_get_partition", "oocgb_get_row_order",
     "oocgb_get_timings", "oocgb_set_profiling", "oocgb_last_error", "oocgb_abi_version",
-    "oocgb_ctx_create_hostcomm", "oocgb_sample_goss", "oocgb_set_streaming",
+    "oocgb_ctx_create_hostcomm", "oocgb_sample_goss", "oocgb_set_streaming", "oocgb_quantise_csr",
 )
 
 COLLECTIVE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
@@ -49,12 +49,13 @@ class Node(ctypes.Structure):
     _fields_ = [("feature", ctypes.c_int32), ("split_bin", ctypes.c_int32),
                 ("split_value", ctypes.c_float), ("leaf_value", ctypes.c_float),
                 ("gain", ctypes.c_double), ("sum_g", ctypes.c_double), ("sum_h", ctypes.c_double),
-                ("n_rows", ctypes.c_int64)]
+                ("n_rows", ctypes.c_int64), ("default_left", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 NODE_DTYPE = np.dtype([("feature", np.int32), ("split_bin", np.int32), ("split_value", np.float32),
                        ("leaf_value", np.float32), ("gain", np.float64), ("sum_g", np.float64),
-                       ("sum_h", np.float64), ("n_rows", np.int64)])
+                       ("sum_h", np.float64), ("n_rows", np.int64), ("default_left", np.int32),
+                       ("pad", np.int32)])
 
 
 class Info(ctypes.Structure):
@@ -62,7 +63,8 @@ class Info(ctypes.Structure):
                 ("row0_global", ctypes.c_int64), ("n_features", ctypes.c_int32),
                 ("row_stride", ctypes.c_int32), ("max_bin", ctypes.c_int32),
                 ("placement", ctypes.c_int32), ("n_pages", ctypes.c_int64),
-                ("rows_per_page", ctypes.c_int64), ("total_cuts", ctypes.c_int64)]
+                ("rows_per_page", ctypes.c_int64), ("total_cuts", ctypes.c_int64),
+                ("has_missing", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class SampleInfo(ctypes.Structure):
@@ -120,6 +122,7 @@ def load_library():
         "oocgb_ctx_create_hostcomm": [i32, i32, i32, COLLECTIVE_FN, p, u64, p],
         "oocgb_sample_goss": [p, d, d, u64, u64, i32, p],
         "oocgb_set_streaming": [p, i32],
+        "oocgb_quantise_csr": [p, p, p, p, i64, i64, i64, i32, i32, i64, i32, u64, p],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -203,6 +206,20 @@ class Context:
         _check(load_library().oocgb_quantise(self._h, px, n, row0_global,
                                               n if n_rows_global is None else n_rows_global, m, max_bin,
                                               page_bytes, placement, seed, ctypes.byref(h)))
+        return Data(self, h)
+
+    def quantise_csr(self, indptr, indices, values, n_features: int, max_bin: int = 255, *, row0_global: int = 0,
+                     n_rows_global: int | None = None, page_bytes: int = 0, placement: int = PLACE_DEVICE,
+                     seed: int = 2) -> "Data":
+        """Sparse CSR rows (R27): absent entries are missing values (symbol 255, max_bin <= 255)."""
+        pp, k1 = _ptr(indptr, np.int64)
+        pi, k2 = _ptr(indices, np.int32)
+        pv, k3 = _ptr(values, np.float32)
+        n = int(indptr.shape[0]) - 1
+        h = ctypes.c_void_p()
+        _check(load_library().oocgb_quantise_csr(self._h, pp, pi, pv, n, row0_global,
+                                                  n if n_rows_global is None else n_rows_global, n_features,
+                                                  max_bin, page_bytes, placement, seed, ctypes.byref(h)))
         return Data(self, h)
 
     # Alg. 3 + Alg. 5, streamed

@@ -251,6 +251,7 @@ static void free_data(oocgb_data d) {
   dfree(d->d_cut_values); dfree(d->d_cut_ptrs); dfree(d->d_bins); dfree(d->d_sketch);
   dfree(d->d_sketch_count); dfree(d->d_g); dfree(d->d_h); dfree(d->d_sel_rows); dfree(d->d_q);
   dfree(d->d_sampled_page); dfree(d->d_gs); dfree(d->d_hs); dfree(d->d_tmp64); dfree(d->d_mvs); dfree(d->d_mvs_stats);
+  dfree(d->d_missing);
   for (int i = 0; i < 3; ++i) dfree(d->d_stage[i]);
   for (int i = 0; i < 2; ++i) dfree(d->d_arg[i]);
   for (int i = 0; i < 3; ++i) dfree(d->d_bstage[i]);
@@ -279,13 +280,35 @@ static void alloc_pages(oocgb_data d) {
 static void write_pages(oocgb_data d, const float *dX, int64_t row_local0, int64_t n) {
   oocgb_ctx c = d->ctx;
   int *d_err = (int *)((char *)c->d_small + 4096);
+  if (!d->d_missing) {
+    d->d_missing = (int *)dmalloc(sizeof(int));
+    OOCGB_CK(cudaMemsetAsync(d->d_missing, 0, sizeof(int), c->stream));
+  }
   OOCGB_CK(cudaMemsetAsync(d_err, 0, sizeof(int), c->stream));
   uint8_t *base = d->placement == OOCGB_PLACE_DEVICE ? d->d_bins : d->h_pages;
   bin_rows(d, dX, n, row_local0, base, d_err);
-  int herr = 0;
+  int herr = 0, hmiss = 0;
   OOCGB_CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaMemcpyAsync(&hmiss, d->d_missing, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   OOCGB_CK(cudaStreamSynchronize(c->stream));
-  OOCGB_REQUIRE(herr == 0, OOCGB_ERR_ARG, "quantise: non-finite value in X (dense path, R4)");
+  OOCGB_REQUIRE(herr != 2, OOCGB_ERR_ARG, "quantise: +-inf in X (R4; NaN marks a missing value)");
+  OOCGB_REQUIRE(herr != 5, OOCGB_ERR_ARG,
+                "quantise: missing values need max_bin <= 255 (symbol 255 marks a missing value, R27)");
+  OOCGB_REQUIRE(herr == 0, OOCGB_ERR_ARG, "quantise: bad value in X");
+  if (hmiss) d->has_missing = true;
+}
+
+// After the last page: every rank agrees on has_missing (it changes the split candidates, R27).
+static void finish_missing(oocgb_data d) {
+  oocgb_ctx c = d->ctx;
+  if (!c->coll) return;
+  unsigned long long *buf = (unsigned long long *)((char *)c->d_small + 8192);
+  unsigned long long v = d->has_missing ? 1 : 0;
+  OOCGB_CK(cudaMemcpyAsync(buf, &v, 8, cudaMemcpyHostToDevice, c->stream));
+  allreduce_max_u64(c, buf, 1);
+  OOCGB_CK(cudaMemcpyAsync(&v, buf, 8, cudaMemcpyDeviceToHost, c->stream));
+  OOCGB_CK(cudaStreamSynchronize(c->stream));
+  d->has_missing = v != 0;
 }
 
 // Run fn(dX_batch, row_offset, n_batch) over X (host or device) in device batches.
@@ -312,7 +335,7 @@ static void over_batches(oocgb_ctx c, const float *X, int64_t n, int m, F fn) {
 extern "C" {
 
 const char *oocgb_last_error(void) { return g_last_error.c_str(); }
-int32_t oocgb_abi_version(void) { return 1; }
+int32_t oocgb_abi_version(void) { return 2; }  // 2: oocgb_node.default_left, oocgb_info.has_missing, CSR input
 
 int oocgb_nccl_unique_id(uint8_t out[128]) {
   API_BEGIN
@@ -437,10 +460,76 @@ int oocgb_quantise(oocgb_ctx c, const float *X, int64_t n_rows, int64_t row0_glo
       write_pages(d, dX, r, nr);
     });
     d->rows_written = n_rows;
+    finish_missing(d);
   } catch (...) {
     free_data(d);
     throw;
   }
+  *out = d;
+  API_END
+}
+
+// Sparse CSR input (R27): the rows are expanded batch by batch to dense float32 with NaN at the
+// absent entries (csr_to_dense, on the device) and go through exactly the dense path's two passes,
+// so cuts and pages equal oocgb_quantise on the NaN-filled matrix.
+int oocgb_quantise_csr(oocgb_ctx c, const int64_t *indptr, const int32_t *indices, const float *values,
+                       int64_t n_rows, int64_t row0_global, int64_t n_rows_global, int32_t n_features,
+                       int32_t max_bin, int64_t page_bytes, int32_t placement, uint64_t seed, oocgb_data *out) {
+  API_BEGIN
+  OOCGB_REQUIRE(c && out && (indptr || n_rows == 0), OOCGB_ERR_ARG, "NULL argument");
+  OOCGB_REQUIRE(n_rows >= 0 && n_features > 0, OOCGB_ERR_ARG, "quantise_csr: bad sizes");
+  bind(c);
+  // row pointers on the host (sizes) and on the device (the scatter kernel)
+  std::vector<int64_t> hptr(n_rows + 1, 0);
+  if (n_rows >= 0 && indptr) {
+    if (is_device_ptr(indptr))
+      OOCGB_CK(cudaMemcpy(hptr.data(), indptr, sizeof(int64_t) * (n_rows + 1), cudaMemcpyDeviceToHost));
+    else
+      memcpy(hptr.data(), indptr, sizeof(int64_t) * (n_rows + 1));
+  }
+  const int64_t base = hptr[0], nnz = hptr[n_rows] - base;
+  OOCGB_REQUIRE(nnz >= 0 && (nnz == 0 || (indices && values)), OOCGB_ERR_ARG, "quantise_csr: bad indptr / arrays");
+  for (int64_t i = 0; i < n_rows; ++i)
+    OOCGB_REQUIRE(hptr[i + 1] >= hptr[i] && hptr[i + 1] - hptr[i] <= n_features, OOCGB_ERR_ARG,
+                  "quantise_csr: indptr must be non-decreasing with <= n_features entries per row");
+  int64_t *d_ptr = (int64_t *)dmalloc(sizeof(int64_t) * (n_rows + 1));
+  int32_t *d_idx = (int32_t *)dmalloc(sizeof(int32_t) * std::max<int64_t>(1, nnz));
+  float *d_val = (float *)dmalloc(sizeof(float) * std::max<int64_t>(1, nnz));
+  const int64_t batch = std::max<int64_t>(1, (256LL << 20) / ((int64_t)n_features * 4));
+  float *buf = (float *)dmalloc(sizeof(float) * (size_t)std::max<int64_t>(1, std::min(batch, n_rows)) * n_features);
+  oocgb_data d = nullptr;
+  try {
+    OOCGB_CK(cudaMemcpyAsync(d_ptr, hptr.data(), sizeof(int64_t) * (n_rows + 1), cudaMemcpyHostToDevice, c->stream));
+    if (nnz > 0) {
+      OOCGB_CK(cudaMemcpyAsync(d_idx, indices + base, sizeof(int32_t) * nnz, cudaMemcpyDefault, c->stream));
+      OOCGB_CK(cudaMemcpyAsync(d_val, values + base, sizeof(float) * nnz, cudaMemcpyDefault, c->stream));
+    }
+    int *d_err = (int *)((char *)c->d_small + 12288);
+    OOCGB_CK(cudaMemsetAsync(d_err, 0, sizeof(int), c->stream));
+    d = new_data(c, n_rows, row0_global, n_rows_global, n_features, max_bin, page_bytes, placement, seed);
+    auto each_batch = [&](auto fn) {
+      for (int64_t r = 0; r < n_rows; r += batch) {
+        const int64_t nr = std::min(batch, n_rows - r);
+        csr_to_dense(c, d_ptr, d_idx, d_val, base, r, nr, n_features, buf, d_err);
+        fn(buf, r, nr);
+        OOCGB_CK(cudaStreamSynchronize(c->stream));
+      }
+      int herr = 0;
+      OOCGB_CK(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+      OOCGB_REQUIRE(herr == 0, OOCGB_ERR_ARG, "quantise_csr: a column index outside [0, n_features)");
+    };
+    each_batch([&](const float *dX, int64_t r, int64_t nr) { sketch_append(d, dX, row0_global + r, nr); });
+    cuts_finalize(d);
+    alloc_pages(d);
+    each_batch([&](const float *dX, int64_t r, int64_t nr) { write_pages(d, dX, r, nr); });
+    d->rows_written = n_rows;
+    finish_missing(d);
+  } catch (...) {
+    if (d) free_data(d);
+    dfree(d_ptr); dfree(d_idx); dfree(d_val); dfree(buf);
+    throw;
+  }
+  dfree(d_ptr); dfree(d_idx); dfree(d_val); dfree(buf);
   *out = d;
   API_END
 }
@@ -491,6 +580,7 @@ int oocgb_pages_push(oocgb_data d, const float *X, int64_t row0_global, int64_t 
     write_pages(d, dX, base + r, nr);
   });
   d->rows_written += n;
+  if (d->rows_written == d->n_local) finish_missing(d);
   API_END
 }
 
@@ -515,6 +605,7 @@ int oocgb_quantise_like(oocgb_data ref, const float *X, int64_t n_rows, int32_t 
     alloc_pages(d);
     over_batches(c, X, n_rows, d->m, [&](const float *dX, int64_t r, int64_t nr) { write_pages(d, dX, r, nr); });
     d->rows_written = n_rows;
+    d->has_missing = d->has_missing || ref->has_missing;
   } catch (...) {
     free_data(d);
     throw;
@@ -536,6 +627,8 @@ int oocgb_data_info(oocgb_data d, oocgb_info *out) {
   out->n_pages = d->n_pages;
   out->rows_per_page = d->rows_per_page;
   out->total_cuts = (int64_t)d->h_cut_values.size();
+  out->has_missing = d->has_missing ? 1 : 0;
+  out->pad = 0;
   API_END
 }
 

@@ -83,6 +83,8 @@ struct DNode {
   double sum_g, sum_h;
   long long n_rows;    // global sampled rows
   long long Gq, Hq;    // fixed-point sums (global)
+  int32_t default_left;  // R27: missing values (symbol 255) go left
+  int32_t pad;
 };
 
 // Row segment of the partition at one depth (pass-through segments carry leaves).
@@ -109,7 +111,7 @@ struct Pair {
 // Best split candidate of one (node, feature).
 struct Cand {
   double gain;
-  int32_t bin;
+  int32_t bin;         // candidate key 2 b + dir (dir 1: missing values left, R27)
   int32_t valid;
   long long GL, HL;
 };
@@ -178,8 +180,15 @@ struct PNode {          // compact node for predict
   int32_t feature;
   int32_t split_bin;
   float leaf;
-  int32_t pad;
+  int32_t default_left;  // R27
 };
+
+// RepartitionInstances / predict rule (R27): symbol 255 of data with missing values follows the
+// node's default direction; every other symbol goes left iff bin <= split_bin (for data without
+// missing values default_left is 0, so the rule reduces to bin <= split_bin)
+__host__ __device__ __forceinline__ bool goes_left(int b, int split_bin, int default_left) {
+  return b <= split_bin || (b == 255 && default_left);
+}
 
 }  // namespace oocgb
 
@@ -225,6 +234,8 @@ struct oocgb_data_s {
   std::vector<float> h_cut_values;
   std::vector<int32_t> h_cut_ptrs;
   bool cuts_ready = false;
+  bool has_missing = false;     // R27: some value was missing (NaN / absent CSR entry)
+  int *d_missing = nullptr;     // device flag set by the binning kernel
   // ELLPACK (R5-R6)
   // Tiled ELLPACK (R5): pages of rows_per_page rows; inside a page the symbols of
   // feature group g (features 32g..32g+31) of all the page's rows are contiguous:
@@ -311,6 +322,8 @@ bool is_device_ptr(const void *p);
 void sketch_append(oocgb_data d, const float *dX, int64_t row0_global, int64_t n);
 void cuts_finalize(oocgb_data d);
 void bin_rows(oocgb_data d, const float *dX, int64_t n, int64_t row_local0, uint8_t *out_base, int *d_err);
+void csr_to_dense(oocgb_ctx c, const int64_t *d_indptr, const int32_t *d_indices, const float *d_values,
+                  int64_t base, int64_t r0, int64_t nr, int m, float *d_out, int *d_err);
 
 // sample.cu
 void logistic_gradients(oocgb_data d, const float *d_margin, const float *d_labels);

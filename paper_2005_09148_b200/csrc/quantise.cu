@@ -14,8 +14,12 @@
 
 namespace oocgb {
 
-// Order-preserving float -> uint32 key, -0.0 canonicalised to +0.0 (R4).
+// Order-preserving float -> uint32 key, -0.0 canonicalised to +0.0 (R4).  A missing value (NaN,
+// R27) gets the largest key 0xFFFFFFFF, above every finite key (<= 0xFF7FFFFF): it sorts last and
+// the cut extraction stops before it (like the all-gather's padding rows).
+constexpr uint32_t kMissingKey = 0xFFFFFFFFu;
 __device__ __forceinline__ uint32_t float_key(float x) {
+  if (isnan(x)) return kMissingKey;
   if (x == 0.0f) x = 0.0f;
   uint32_t u = __float_as_uint(x);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
@@ -49,7 +53,7 @@ __global__ void k_sketch_append(const float *__restrict__ X, int64_t n, int m, i
     uint32_t *out = sample + (int64_t)slot * m;
     for (int j = lane; j < m; j += 32) {
       float x = xr[j];
-      if (!isfinite(x)) atomicExch(err, 2);
+      if (isinf(x)) atomicExch(err, 2);  // R4; NaN = missing (R27)
       out[j] = float_key(x);
     }
   }
@@ -74,11 +78,21 @@ __global__ void k_transpose_keys(const uint32_t *__restrict__ in, int64_t N, int
   }
 }
 
-// One block per feature over its sorted keys s[0..N): O1 steps 3-5.
-__global__ void k_extract_cuts(const uint32_t *__restrict__ sorted, int64_t N, int B,
+// One block per feature over its sorted keys s[0..N): O1 steps 3-5 on the feature's present
+// values, s[0..N_j) with N_j = the first missing / padding key (R27).
+__global__ void k_extract_cuts(const uint32_t *__restrict__ sorted, int64_t N_all, int B,
                                float *cuts_out /*[m][256]*/, int *cnt_out /*[m]*/) {
   int j = blockIdx.x;
-  const uint32_t *s = sorted + (int64_t)j * N;
+  const uint32_t *s = sorted + (int64_t)j * N_all;
+  int64_t N;
+  {  // lower_bound(s, kMissingKey): every thread runs the same binary search
+    int64_t lo = 0, hi = N_all;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (s[mid] < kMissingKey) lo = mid + 1; else hi = mid;
+    }
+    N = lo;
+  }
   __shared__ unsigned long long distinct;
   __shared__ uint32_t vals[256];
   __shared__ int nvals;
@@ -136,7 +150,8 @@ __global__ void k_extract_cuts(const uint32_t *__restrict__ sorted, int64_t N, i
 // output is fully coalesced (device pages, or pinned host pages written zero-copy over PCIe).
 __global__ void k_bin_rows(const float *__restrict__ X, int64_t n, int m, int n_fg, int gw, int stride,
                            int64_t row_local0, int64_t rpp, const float *__restrict__ cuts,
-                           const int *__restrict__ ptrs, uint8_t *__restrict__ out, int *err, int rowmajor) {
+                           const int *__restrict__ ptrs, uint8_t *__restrict__ out, int *err, int rowmajor,
+                           int *missing) {
   const int64_t total = (int64_t)n_fg * n * 8;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -150,9 +165,15 @@ __global__ void k_bin_rows(const float *__restrict__ X, int64_t n, int m, int n_
       const int j = g * 32 + u * 4 + c;
       if (j >= m) break;
       const float x = X[r * m + j];
-      if (!isfinite(x)) { atomicExch(err, 2); continue; }
       const int lo = __ldg(ptrs + j), hi = __ldg(ptrs + j + 1);
       const int B = hi - lo;
+      if (isnan(x)) {  // missing (R27): symbol 255; a feature with 256 bins cannot hold it
+        word |= 255u << (8 * c);
+        if (B > 255) atomicExch(err, 5);
+        if (*missing == 0) atomicExch(missing, 1);
+        continue;
+      }
+      if (isinf(x)) { atomicExch(err, 2); continue; }
       int a = 0, bnd = B;  // lower_bound: smallest b with x <= c_b
       while (a < bnd) {
         const int mid = (a + bnd) >> 1;
@@ -194,7 +215,7 @@ void sketch_append(oocgb_data d, const float *dX, int64_t row0_global, int64_t n
   int herr = 0;
   OOCGB_CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   OOCGB_CK(cudaStreamSynchronize(c->stream));
-  OOCGB_REQUIRE(herr != 2, OOCGB_ERR_ARG, "quantise: non-finite value in X (dense path, R4)");
+  OOCGB_REQUIRE(herr != 2, OOCGB_ERR_ARG, "quantise: +-inf in X (R4; NaN marks a missing value)");
   OOCGB_REQUIRE(herr != 3, OOCGB_ERR_NOMEM, "quantise: sketch sample exceeded its capacity");
 }
 
@@ -334,6 +355,32 @@ void cuts_finalize(oocgb_data d) {
   d->cuts_ready = true;
 }
 
+// CSR rows [r0, r0 + nr) -> dense float32 [nr][m] with NaN (missing, R27) at the absent entries:
+// the buffer is pre-filled with 0xFF bytes (a NaN), then one warp per row scatters its entries.
+__global__ void k_csr_scatter(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+                              const float *__restrict__ values, int64_t base, int64_t r0, int64_t nr, int m,
+                              float *__restrict__ out, int *err) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < nr;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = indptr[r0 + r] - base, e = indptr[r0 + r + 1] - base;
+    for (int64_t k = b + lane; k < e; k += 32) {
+      const int j = indices[k];
+      if (j < 0 || j >= m) { atomicExch(err, 6); continue; }
+      out[r * m + j] = values[k];
+    }
+  }
+}
+
+void csr_to_dense(oocgb_ctx c, const int64_t *d_indptr, const int32_t *d_indices, const float *d_values,
+                  int64_t base, int64_t r0, int64_t nr, int m, float *d_out, int *d_err) {
+  if (nr <= 0) return;
+  OOCGB_CK(cudaMemsetAsync(d_out, 0xFF, sizeof(float) * (size_t)nr * m, c->stream));
+  const int blocks = (int)std::min<int64_t>((nr + 7) / 8, (int64_t)c->num_sms * 16);
+  k_csr_scatter<<<blocks, 256, 0, c->stream>>>(d_indptr, d_indices, d_values, base, r0, nr, m, d_out, d_err);
+  OOCGB_CK(cudaGetLastError());
+}
+
 void bin_rows(oocgb_data d, const float *dX, int64_t n, int64_t row_local0, uint8_t *out_base, int *d_err) {
   oocgb_ctx c = d->ctx;
   if (n <= 0) return;
@@ -342,7 +389,7 @@ void bin_rows(oocgb_data d, const float *dX, int64_t n, int64_t row_local0, uint
   k_bin_rows<<<blocks, 256, 0, c->stream>>>(dX, n, d->m, d->n_fg, d->gw, d->stride, row_local0, d->rows_per_page,
                                             d->d_cut_values,
                                             d->d_cut_ptrs, out_base, d_err,
-                                            d->placement == OOCGB_PLACE_PINNED_HOST ? 1 : 0);
+                                            d->placement == OOCGB_PLACE_PINNED_HOST ? 1 : 0, d->d_missing);
   OOCGB_CK(cudaGetLastError());
 }
 

@@ -48,13 +48,14 @@ struct RoundParams {
 };
 
 struct GraphKey {
-  int n, D, m, ridx_mode, keep_debug, profiling, world;
+  int n, D, m, ridx_mode, keep_debug, profiling, world, has_missing;
   double lambda, gamma, mcw, eta;
   const void *bins;
   size_t pitch;
   int quant_bits;
   bool operator==(const GraphKey &o) const {
     return n == o.n && D == o.D && m == o.m && ridx_mode == o.ridx_mode && keep_debug == o.keep_debug &&
+           has_missing == o.has_missing &&
            profiling == o.profiling && world == o.world && lambda == o.lambda && gamma == o.gamma &&
            mcw == o.mcw && eta == o.eta && bins == o.bins && pitch == o.pitch && quant_bits == o.quant_bits;
   }
@@ -399,6 +400,7 @@ struct EvalArgs {
   double eta;
   const int2 *ent;  // per-level work lists of (pair, side): general [0, n_ew), narrow [ent_cap, + n_en)
   int ent_cap;
+  int has_missing;  // R27: bin 255 holds missing values; candidates in both default directions
 };
 
 __device__ __forceinline__ int warp_excl_scan_i(int v, int lane, int &total) {
@@ -443,9 +445,10 @@ __device__ __forceinline__ double gain_exact(long long GL, long long HL, long lo
 //    the result is identical to evaluating every candidate in double.
 // I = int for nodes with <= kmax rows (every partial sum is then exact in int32), else long long.
 // Returns the lane that owns the winning bin (it wrote the candidate), or 0.
-template <typename I>
-__device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (&g)[8], const I (&h)[8],
-                         const RoundParams &rp, const long long G_, const long long H_) {
+template <typename I, bool MISS>
+__device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, const I (&g)[8], const I (&h)[8],
+                              const RoundParams &rp, const long long G_, const long long H_, const I Gm,
+                              const I Hm) {
   const int B = A.cut_ptrs[j + 1] - A.cut_ptrs[j];
   const I G = (I)G_, H = (I)H_;
   I lg = 0, lh = 0;
@@ -476,71 +479,50 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
   // error with a >= 6x margin (tL, tR, tP >= 0: squares over positive denominators).  Its per-node
   // part is hoisted; with the pre-filter off every valid candidate survives (tol = inf).
   const float tol0 = rp.prefilter ? 0x1p-18f * (tPf + fabsf(gamf)) + 0x1p-100f : INFINITY;
-  // pass 1: float gains; ub = gain + tol (inf for a non-finite term: always re-evaluated)
-  float ub[8];
-  unsigned vmask = 0;
-  I GL = eg, HL = eh;
-  float Lmax = -INFINITY;
-#if OOCGB_EVAL_FOLD
   // Folded scales, branch-free: with sg = 2^-e_g, sh = 2^-e_h (exact powers of two) the float
   // terms are tL = c GL^2 / (HL + lq) with c = sg^2 / sh and lq = lambda / sh, the same values up
-  // to rounding order as the unfolded form below; the gain and its bound scale by c exactly
-  // (the pre-filter is on only when c and lq are normal floats, see k_init_build).
+  // to rounding order as the unfolded form; the gain and its bound scale by c exactly (the
+  // pre-filter is on only when c and lq are normal floats, see k_init_build).
   const float c = rp.fold_c, lq = rp.fold_lq;  // hoisted to k_init_build (same values)
   const float chalf = 0.5f * c, tolc = 0x1p-18f * c, K = 0.5f * tPf + gamf;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    GL += g[i];
-    HL += h[i];
-    const int b = lane * 8 + i;
-    // an empty bin repeats the previous candidate exactly, which wins the tie (lower bin)
-    const bool v = b <= B - 2 && ((g[i] | h[i]) != 0 || b == 0) && HL >= hmin && HL <= hmax;
-    const float GLf = (float)GL, HLf = (float)HL, GRf = (float)(G - GL), HRf = (float)(H - HL);
+  // candidate key 2 b + dir: dir 0 = missing rows right (left sums = the prefix), dir 1 = missing
+  // rows left (prefix + the missing bin's sums; MISS only, R27)
+  float ub[MISS ? 2 : 1][8];
+  unsigned vmask = 0;  // bit 2 i + dir
+  float Lmax = -INFINITY;
+  auto pre = [&](I GLx, I HLx, bool vb, float &u, int bit) {
+    const bool v = vb && HLx >= hmin && HLx <= hmax;
+    const float GLf = (float)GLx, HLf = (float)HLx, GRf = (float)(G - GLx), HRf = (float)(H - HLx);
     const float T = __fdividef(GLf * GLf, HLf + lq) + __fdividef(GRf * GRf, HRf + lq);
     const float gain = chalf * T - K;
     const float tol = tolc * T + tol0;  // NaN / inf when a term is not finite
     const bool fin = tol < INFINITY;
-    vmask |= v ? 1u << i : 0u;
-    ub[i] = v ? (fin ? gain + tol : INFINITY) : -INFINITY;
+    vmask |= v ? 1u << bit : 0u;
+    u = v ? (fin ? gain + tol : INFINITY) : -INFINITY;
     Lmax = fmaxf(Lmax, (v && fin) ? gain - tol : -INFINITY);
-  }
-#else
+  };
+  // pass 1: float gains; ub = gain + tol (inf for a non-finite term: always re-evaluated)
+  I GL = eg, HL = eh;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     GL += g[i];
     HL += h[i];
     const int b = lane * 8 + i;
     // an empty bin repeats the previous candidate exactly, which wins the tie (lower bin)
-    const bool v = b <= B - 2 && ((g[i] | h[i]) != 0 || b == 0) && HL >= hmin && HL <= hmax;
-    ub[i] = -INFINITY;
-    if (v) {
-      vmask |= 1u << i;
-      const float gl = (float)GL * rp.sg_inv_f, hl = (float)HL * rp.sh_inv_f;
-      const float gr = (float)(G - GL) * rp.sg_inv_f, hr = (float)(H - HL) * rp.sh_inv_f;
-      const float tL = __fdividef(gl * gl, hl + lamf);  // <= 2 ulp (denominator in range, see guard)
-      const float tR = __fdividef(gr * gr, hr + lamf);
-      const float S = tL + tR;
-      const float gain = 0.5f * (S - tPf) - gamf;
-      const float tol = 0x1p-18f * S + tol0;  // NaN / inf when a term is not finite
-      if (tol < INFINITY) {
-        ub[i] = gain + tol;
-        Lmax = fmaxf(Lmax, gain - tol);
-      } else {
-        ub[i] = INFINITY;
-      }
-    }
+    const bool vb = b <= B - 2 && ((g[i] | h[i]) != 0 || b == 0);
+    pre(GL, HL, vb, ub[0][i], 2 * i);
+    if constexpr (MISS) pre(GL + Gm, HL + Hm, vb, ub[MISS ? 1 : 0][i], 2 * i + 1);
   }
-#endif
 #pragma unroll
   for (int o = 16; o; o >>= 1) Lmax = fmaxf(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, o));
-  // pass 2: exact double gains of the survivors
+  // pass 2: exact double gains of the survivors, in key order (strict > keeps the lower key)
   double tP = 0.0;
   {
     const double gP = __dmul_rn((double)G, rp.sg_inv), hP = __dmul_rn((double)H, rp.sh_inv);
     tP = __ddiv_rn(__dmul_rn(gP, gP), __dadd_rn(hP, A.lambda));
   }
   double best = 0.0;
-  int bbin = 0x7fffffff, have = 0;
+  int bkey = 0x7fffffff, have = 0;
   long long bGL = 0, bHL = 0;
   GL = eg;
   HL = eh;
@@ -548,15 +530,21 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
   for (int i = 0; i < 8; ++i) {
     GL += g[i];
     HL += h[i];
-    if (((vmask >> i) & 1u) && ub[i] >= Lmax) {
-      const double gain = gain_exact(GL, HL, G, H, tP, rp.sg_inv, rp.sh_inv, A.lambda, A.gamma);
-      if (!have || gain > best) { have = 1; best = gain; bbin = lane * 8 + i; bGL = (long long)GL; bHL = (long long)HL; }
+#pragma unroll
+    for (int dir = 0; dir < (MISS ? 2 : 1); ++dir) {
+      if (((vmask >> (2 * i + dir)) & 1u) && ub[dir][i] >= Lmax) {
+        const I GLx = dir ? GL + Gm : GL, HLx = dir ? HL + Hm : HL;
+        const double gain = gain_exact(GLx, HLx, G, H, tP, rp.sg_inv, rp.sh_inv, A.lambda, A.gamma);
+        if (!have || gain > best) {
+          have = 1; best = gain; bkey = 2 * (lane * 8 + i) + dir; bGL = (long long)GLx; bHL = (long long)HLx;
+        }
+      }
     }
   }
-  // warp argmax over (gain, bin): larger gain, then lower bin; invalid = -inf.  Only the pair is
-  // shuffled; the lane that owns the winning bin writes its own G_L, H_L.
+  // warp argmax over (gain, key): larger gain, then lower key; invalid = -inf.  Only the pair is
+  // shuffled; the lane that owns the winning key writes its own G_L, H_L.
   double bg = have ? best : -INFINITY;
-  int bb = have ? bbin : 0x7fffffff;
+  int bb = have ? bkey : 0x7fffffff;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     const double og = __shfl_xor_sync(0xffffffffu, bg, o);
@@ -564,7 +552,7 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
     if (og > bg || (og == bg && ob < bb)) { bg = og; bb = ob; }
   }
   const bool any = bb != 0x7fffffff;
-  const int owner = any ? (bb >> 3) : 0;
+  const int owner = any ? (bb >> 4) : 0;  // 16 keys (8 bins x 2 directions) per lane
   if (lane == owner) {
     const int slot = node - level_first(A.d);
     Cand cd;
@@ -576,6 +564,20 @@ __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (
     A.cand[(size_t)slot * A.m + j] = cd;
   }
   return owner;
+}
+
+// EvaluateSplit of one node for feature j (see eval_node_impl).  With missing values (R27) the
+// missing bin 255 (lane 31's last element) holds the rows missing feature j; a feature with
+// missing rows in this node also tries every candidate with those rows on the left.
+template <typename I, bool HAS_MISSING>
+__device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (&g)[8],
+                                         const I (&h)[8], const RoundParams &rp, const long long G_,
+                                         const long long H_) {
+  if constexpr (HAS_MISSING) {  // a separate kernel instantiation: dense data keeps its registers
+    const I Gm = __shfl_sync(0xffffffffu, g[7], 31), Hm = __shfl_sync(0xffffffffu, h[7], 31);
+    if (Gm != 0 || Hm != 0) return eval_node_impl<I, true>(A, node, j, lane, g, h, rp, G_, H_, Gm, Hm);
+  }
+  return eval_node_impl<I, false>(A, node, j, lane, g, h, rp, G_, H_, (I)0, (I)0);
 }
 
 __device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)[8], const long long (&h)[8]) {
@@ -591,6 +593,7 @@ __device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)
 // consecutive bins 8 lane .. 8 lane + 7 for the scan and the evaluation.
 constexpr int kEvalWarps = 4;  // 4-warp blocks: measured best of 1, 2, 4, 8
 constexpr int kEvalBlocksWide = 4, kEvalBlocksNarrow = 6;  // resident blocks per SM (registers)
+template <bool HAS_MISSING>
 __device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int side, int j, int lane,
                                                longlong2 *tl) {
   const Pair P = A.pairs[p];
@@ -689,14 +692,15 @@ __device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int sid
     int g32[8], h32[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) { g32[i] = (int)g[i]; h32[i] = (int)h[i]; }
-    eval_node<int>(A, node, j, lane, g32, h32, rp, nodeG, nodeH);
+    eval_node<int, HAS_MISSING>(A, node, j, lane, g32, h32, rp, nodeG, nodeH);
   } else {
-    eval_node<long long>(A, node, j, lane, g, h, rp, nodeG, nodeH);
+    eval_node<long long, HAS_MISSING>(A, node, j, lane, g, h, rp, nodeG, nodeH);
   }
 }
 
 // Persistent warps over the level's work list: item t = (entry t / m, feature t % m), entry =
 // (pair, side) written by the plan (general list: nodes with > kmax rows, streamed levels).
+template <bool HAS_MISSING>
 __global__ void __launch_bounds__(kEvalWarps * 32, kEvalBlocksWide) k_eval(EvalArgs A) {
   __shared__ longlong2 tile[kEvalWarps][256 + 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -705,7 +709,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, kEvalBlocksWide) k_eval(EvalA
   for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < n_items; t += nw) {
     const int e = t / A.m;
     const int2 en = A.ent[e];
-    eval_item_wide(A, en.x, en.y, t - e * A.m, lane, tile[wib]);
+    eval_item_wide<HAS_MISSING>(A, en.x, en.y, t - e * A.m, lane, tile[wib]);
   }
 }
 
@@ -716,6 +720,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, kEvalBlocksWide) k_eval(EvalA
 #ifndef OOCGB_EVAL_NARROW_MINB
 #define OOCGB_EVAL_NARROW_MINB 6  // 80 registers, no spills (= kEvalBlocksNarrow)
 #endif
+template <bool HAS_MISSING>
 __device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int side, int j, int lane, int2 *tl) {
   const Pair P = A.pairs[p];
   const int node = side ? P.derived : P.built;
@@ -794,10 +799,11 @@ __device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int s
   }
   __syncwarp();  // the tile is reused by the warp's next item
   const RoundParams rp = *A.rp;
-  eval_node<int>(A, node, j, lane, g, h, rp, nodeG, nodeH);
+  eval_node<int, HAS_MISSING>(A, node, j, lane, g, h, rp, nodeG, nodeH);
 }
 
 // Persistent warps over the level's narrow list (nodes with <= kmax global rows, from the plan).
+template <bool HAS_MISSING>
 __global__ void __launch_bounds__(kEvalWarps * 32, OOCGB_EVAL_NARROW_MINB) k_eval_narrow(EvalArgs A) {
   __shared__ int2 tile2[kEvalWarps][256 + 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -806,7 +812,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32, OOCGB_EVAL_NARROW_MINB) k_eva
   for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < n_items; t += nw) {
     const int e = t / A.m;
     const int2 en = A.ent[A.ent_cap + e];
-    eval_item_narrow(A, en.x, en.y, t - e * A.m, lane, tile2[wib]);
+    eval_item_narrow<HAS_MISSING>(A, en.x, en.y, t - e * A.m, lane, tile2[wib]);
   }
 }
 
@@ -864,8 +870,9 @@ k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Ca
     if (best.have && best.gain > 0.0) {
       DNode &nd = dn[node];
       nd.feature = best.j;
-      nd.split_bin = best.bin;
-      nd.split_value = cut_values[cut_ptrs[best.j] + best.bin];
+      nd.split_bin = best.bin >> 1;      // candidate key 2 b + dir (R27)
+      nd.default_left = best.bin & 1;
+      nd.split_value = cut_values[cut_ptrs[best.j] + (best.bin >> 1)];
       nd.gain = best.gain;
       DNode L{}, R{};
       L.feature = -1;
@@ -881,9 +888,15 @@ k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Ca
 
 static void launch_eval(const EvalArgs &A, int max_pairs, int num_sms, cudaStream_t st) {
   const int64_t blocks = ((int64_t)max_pairs * A.m * 2 + kEvalWarps - 1) / kEvalWarps;
-  k_eval<<<(unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * kEvalBlocksWide), kEvalWarps * 32, 0, st>>>(A);
-  k_eval_narrow<<<(unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * OOCGB_EVAL_NARROW_MINB), kEvalWarps * 32, 0,
-                  st>>>(A);
+  const unsigned gw = (unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * kEvalBlocksWide);
+  const unsigned gn = (unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * OOCGB_EVAL_NARROW_MINB);
+  if (A.has_missing) {  // R27: candidates in both default directions
+    k_eval<true><<<gw, kEvalWarps * 32, 0, st>>>(A);
+    k_eval_narrow<true><<<gn, kEvalWarps * 32, 0, st>>>(A);
+  } else {
+    k_eval<false><<<gw, kEvalWarps * 32, 0, st>>>(A);
+    k_eval_narrow<false><<<gn, kEvalWarps * 32, 0, st>>>(A);
+  }
   k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, st>>>(A.d, A.m, A.pairs, A.ctl, A.cand, A.dn, A.cut_values,
                                                          A.cut_ptrs, A.rp, A.lambda, A.eta);
   OOCGB_CK(cudaGetLastError());
@@ -938,7 +951,7 @@ __device__ __forceinline__ void load_tile_segs(TileSegs &T, const Seg *__restric
     T.end[k] = S.begin + S.count;
     const DNode &nd = dn[S.node];
     T.feat[k] = nd.feature;
-    T.sbin[k] = nd.split_bin;
+    T.sbin[k] = nd.split_bin | (nd.default_left << 9);  // bit 9: missing values go left (R27)
   }
   __syncthreads();
 }
@@ -1054,7 +1067,7 @@ k_part_fused(const long long *__restrict__ n_dev, const Seg *__restrict__ segs, 
           while (segs[k].begin + segs[k].count <= p) ++k;
           const DNode &nd = dn[segs[k].node];
           f = nd.feature;
-          sb[u] = nd.split_bin;
+          sb[u] = nd.split_bin | (nd.default_left << 9);
         }
         sg[u] = k;
       }
@@ -1064,7 +1077,7 @@ k_part_fused(const long long *__restrict__ n_dev, const Seg *__restrict__ segs, 
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (sb[u] & 0x100) {
-        if (b[u] > (sb[u] & 0xff)) rbits |= 1u << u; else lbits |= 1u << u;
+        if (goes_left(b[u], sb[u] & 0xff, (sb[u] >> 9) & 1)) lbits |= 1u << u; else rbits |= 1u << u;
       }
   }
   const uint32_t lt = (1u << lane) - 1u;
@@ -1451,7 +1464,8 @@ __global__ void k_predict(const uint8_t *__restrict__ bins, size_t row_step, siz
       int v = 0;
       while (nd[v].feature >= 0) {
         const int f = nd[v].feature;
-        v = (row[(size_t)(f >> lgw) * pitch + (f & gmask)] <= nd[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
+        v = goes_left(row[(size_t)(f >> lgw) * pitch + (f & gmask)], nd[v].split_bin, nd[v].default_left) ? 2 * v + 1
+                                                                                                         : 2 * v + 2;
       }
       mg = mg + nd[v].leaf;
     }
@@ -1623,7 +1637,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 0;
     A.cut_values = d->d_cut_values; A.eta = eta;
-    A.ent = w->ent; A.ent_cap = w->ent_cap;
+    A.ent = w->ent; A.ent_cap = w->ent_cap; A.has_missing = d->has_missing ? 1 : 0;
     launch_eval(A, max_pairs, c->num_sms, c->stream);
     mark(1, false);
     mark(2, true);
@@ -1699,8 +1713,8 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     if (w->dbg_bytes < need) { drop_graph(w); dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
   }
   // keyed by the capacity, not the sample's row count: sampled rounds replay one graph
-  GraphKey key{(int)w->cap_rows, D, m, ridx_mode, keep_debug ? 1 : 0, c->profiling ? 1 : 0, c->world, lambda, gamma,
-               mcw, eta, bins, pitch, d->quant_bits};
+  GraphKey key{(int)w->cap_rows, D, m, ridx_mode, keep_debug ? 1 : 0, c->profiling ? 1 : 0, c->world,
+               d->has_missing ? 1 : 0, lambda, gamma, mcw, eta, bins, pitch, d->quant_bits};
   if (c->host_coll) {
     // host-callback collectives synchronise the stream: run the level loop directly
     drop_graph(w);
@@ -1751,9 +1765,11 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     o.sum_g = hn[v].sum_g;
     o.sum_h = hn[v].sum_h;
     o.n_rows = hn[v].n_rows;
+    o.default_left = hn[v].feature >= 0 ? hn[v].default_left : 0;
+    o.pad = 0;
     if (o.feature == -2) { o.split_bin = 0; o.split_value = 0; o.leaf_value = 0; o.gain = 0; o.sum_g = 0; o.sum_h = 0; o.n_rows = 0; }
     if (o.feature == -1) { o.split_bin = 0; o.split_value = 0; o.gain = 0; }
-    pn[v] = PNode{o.feature, o.split_bin, o.leaf_value, 0};
+    pn[v] = PNode{o.feature, o.split_bin, o.leaf_value, o.default_left};
   }
   t->ctx = c;
   t->pnodes_bytes = sizeof(PNode) * n_nodes;
@@ -1826,7 +1842,7 @@ __global__ void k_stream_assign(const uint8_t *__restrict__ batch, int stride, i
     if (update) {
       const int f = dn[v].feature;
       if (f >= 0) {
-        v = (batch[(size_t)i * stride + f] <= dn[v].split_bin) ? 2 * v + 1 : 2 * v + 2;
+        v = goes_left(batch[(size_t)i * stride + f], dn[v].split_bin, dn[v].default_left) ? 2 * v + 1 : 2 * v + 2;
         row_node[r0 + i] = v;
         atomicAdd((unsigned long long *)&dn[v].n_rows, 1ull);
       }
@@ -1999,7 +2015,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     A.cut_ptrs = d->d_cut_ptrs; A.dn = w->dnodes; A.cand = w->cand;
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 1;
     A.cut_values = d->d_cut_values; A.eta = eta;
-    A.ent = w->ent; A.ent_cap = w->ent_cap;
+    A.ent = w->ent; A.ent_cap = w->ent_cap; A.has_missing = d->has_missing ? 1 : 0;
     launch_eval(A, n_slots, c->num_sms, c->stream);
   }
   // export (same as the in-core path)
@@ -2022,9 +2038,11 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     o.feature = hn[v].feature; o.split_bin = hn[v].split_bin; o.split_value = hn[v].split_value;
     o.leaf_value = hn[v].leaf_value; o.gain = hn[v].gain; o.sum_g = hn[v].sum_g; o.sum_h = hn[v].sum_h;
     o.n_rows = hn[v].n_rows;
+    o.default_left = hn[v].feature >= 0 ? hn[v].default_left : 0;
+    o.pad = 0;
     if (o.feature == -2) { o.split_bin = 0; o.split_value = 0; o.leaf_value = 0; o.gain = 0; o.sum_g = 0; o.sum_h = 0; o.n_rows = 0; }
     if (o.feature == -1) { o.split_bin = 0; o.split_value = 0; o.gain = 0; }
-    pn[v] = PNode{o.feature, o.split_bin, o.leaf_value, 0};
+    pn[v] = PNode{o.feature, o.split_bin, o.leaf_value, o.default_left};
   }
   t->ctx = c;
   t->pnodes_bytes = sizeof(PNode) * n_nodes;

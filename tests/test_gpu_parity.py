@@ -529,3 +529,156 @@ def test_state_errors(ctx):
         d.set_gradients(np.zeros(99, np.float32), np.ones(99, np.float32))
     assert e.value.status == ob.ERR_ARG
     d.close()
+
+
+# ------------------------------------------------------------------------------ R27 missing values
+def _missing_data(n, m, seed, rates=None):
+    """make_classification rows with missing values (NaN): per-feature missing rates, one feature
+    entirely missing when m >= 4, and in feature 1 the missingness depends on the label (so the
+    default direction carries signal)."""
+    X, y = synth.make_classification(n, m, seed=seed)
+    rng = np.random.default_rng(seed)
+    rates = rates if rates is not None else rng.uniform(0.0, 0.5, size=m)
+    for j in range(m):
+        X[rng.random(n) < rates[j], j] = np.nan
+    if m >= 2:
+        X[(y > 0.5) & (rng.random(n) < 0.6), 1] = np.nan
+    if m >= 4:
+        X[:, 3] = np.nan
+    return X, y
+
+
+MISS_CASES = [
+    # n, m, depth, mode, ratio
+    (3000, 6, 5, 0, 1.0),
+    (20000, 24, 7, 0, 1.0),
+    (20000, 33, 6, 2, 0.3),
+    (60000, 12, 9, 0, 1.0),
+]
+
+
+@pytest.mark.parametrize("n,m,depth,mode,ratio", MISS_CASES)
+def test_tree_with_missing_bit_exact(ctx, n, m, depth, mode, ratio):
+    """R27 on the GPU: cuts skip missing values, symbol 255, both default directions evaluated,
+    missing rows partitioned / predicted by the learned direction -- every tree field (with
+    default_left), node histogram, leaf of every row and prediction bit-exact vs the oracle."""
+    X, y = _missing_data(n, m, seed=40 + n + m)
+    cv, cp = oracle.cuts(X, 255, seed=2)
+    B = oracle.bins(X, cv, cp)
+    d = ctx.quantise(X, 255)
+    assert d.info()["has_missing"] == 1
+    gv, gp = d.get_cuts()
+    np.testing.assert_array_equal(gp, cp)
+    assert gv.tobytes() == cv.tobytes()
+    np.testing.assert_array_equal(d.get_bins(), B)
+    margin = np.random.default_rng(n).normal(scale=0.5, size=n).astype(np.float32)
+    g, h = oracle.logistic_grad(margin, y)
+    s = oracle.sample(g, h, mode, ratio, 1.0, 1, 0)
+    sel = s["selected"].astype(bool)
+    qg, e_g = oracle.quantise(s["gs"][sel], 16)
+    qh, e_h = oracle.quantise(s["hs"][sel], 16)
+    on, olor, ohist = oracle.build_tree(B[sel], m, cv, cp, qg, qh, e_g, e_h, depth, 1.0, 0.0, 1.0, 0.1,
+                                        want_hist=True, has_missing=True)
+    assert (on["default_left"][on["feature"] >= 0] == 1).any(), "fixture should learn a default-left split"
+    d.set_gradients(g, h)
+    info = d.sample(mode, ratio, 1.0, 1, 0, 16)
+    t = d.build_tree(depth, 1.0, 0.0, 1.0, 0.1, keep_debug=True)
+    gn = t.export()
+    for f in on.dtype.names:
+        np.testing.assert_array_equal(gn[f], on[f], err_msg=f)
+    for v in range((1 << depth) - 1):
+        if on["feature"][v] != -2:
+            np.testing.assert_array_equal(t.get_histogram(v), ohist[v], err_msg=f"node {v}")
+    np.testing.assert_array_equal(t.get_partition(info["n_selected_local"]), olor)
+    check_row_order(t.get_row_order(info["n_selected_local"]), on, olor)
+    m0 = np.random.default_rng(1).normal(size=n).astype(np.float32)
+    om = oracle.predict(B, on, m0, has_missing=True)
+    np.testing.assert_array_equal(d.predict([t], m0.copy()), om)
+    if mode == 0:
+        np.testing.assert_array_equal(d.update_margin(t, m0.copy()), om)
+    t.close()
+    d.close()
+
+
+def test_csr_input_equals_dense_with_missing(ctx):
+    """oocgb_quantise_csr (the pages come from CSR): absent entries are missing; cuts,
+    bins and the tree equal oocgb_quantise on the dense matrix with NaN there, and the oracle.
+    The CSR arrays are passed from the host and from the device, with a non-zero indptr[0]."""
+    import scipy.sparse as sp
+    import torch
+    n, m, depth = 15000, 20, 6
+    X, y = _missing_data(n, m, seed=77)
+    # CSR of the present values (an explicit 0.0 stays a present value)
+    mask = ~np.isnan(X)
+    rows, cols = np.nonzero(mask)
+    csr = sp.csr_matrix((X[mask], (rows, cols)), shape=(n, m))
+    csr.sort_indices()
+    indptr = csr.indptr.astype(np.int64) + 5          # a non-zero base offset
+    indices = np.concatenate([np.zeros(5, np.int32), csr.indices.astype(np.int32)])
+    values = np.concatenate([np.zeros(5, np.float32), csr.data.astype(np.float32)])
+    dense = ctx.quantise(X, 255)
+    for src in ("host", "device"):
+        if src == "host":
+            dc = ctx.quantise_csr(indptr, indices, values, m, 255)
+        else:
+            dc = ctx.quantise_csr(torch.from_numpy(indptr).cuda(), torch.from_numpy(indices).cuda(),
+                                  torch.from_numpy(values).cuda(), m, 255)
+        assert dc.info()["has_missing"] == 1
+        a, b = dense.get_cuts(), dc.get_cuts()
+        assert a[0].tobytes() == b[0].tobytes() and np.array_equal(a[1], b[1])
+        np.testing.assert_array_equal(dc.get_bins(), dense.get_bins())
+        g, h = oracle.logistic_grad(np.zeros(n, np.float32), y)
+        trees = []
+        for dd in (dense, dc):
+            dd.set_gradients(g, h)
+            dd.sample(0, 1.0)
+            tt = dd.build_tree(depth)
+            trees.append(tt.export())
+            tt.close()
+        for f in trees[0].dtype.names:
+            np.testing.assert_array_equal(trees[0][f], trees[1][f], err_msg=f)
+        dc.close()
+    dense.close()
+
+
+def test_missing_values_with_max_bin_256_rejected(ctx):
+    rng = np.random.default_rng(5)
+    X = rng.normal(size=(5000, 3)).astype(np.float32)
+    X[7, 1] = np.nan
+    with pytest.raises(ob.OocgbError) as e:
+        ctx.quantise(X, 256)
+    assert e.value.status == ob.ERR_ARG
+    X[8, 2] = np.inf
+    with pytest.raises(ob.OocgbError) as e:
+        ctx.quantise(X, 255)
+    assert e.value.status == ob.ERR_ARG
+
+
+def test_missing_out_of_core_and_streamed(ctx):
+    """Missing values through the pinned-page paths: Alg. 7 compaction (MVS) and the Alg. 6
+    streamed build (f = 1) give the oracle's trees."""
+    n, m = 20000, 16
+    X, y = _missing_data(n, m, seed=91)
+    cv, cp = oracle.cuts(X, 255, seed=2)
+    B = oracle.bins(X, cv, cp)
+    g, h = oracle.logistic_grad(np.random.default_rng(3).normal(size=n).astype(np.float32), y)
+    for mode, ratio, streamed in [(2, 0.3, False), (0, 1.0, True)]:
+        d = ctx.quantise(X, 255, page_bytes=3000 * 32, placement=ob.PLACE_PINNED_HOST)
+        if streamed:
+            d.set_streaming(True)
+        s = oracle.sample(g, h, mode, ratio, 1.0, 5, 2)
+        sel = s["selected"].astype(bool)
+        qg, e_g = oracle.quantise(s["gs"][sel], 16)
+        qh, e_h = oracle.quantise(s["hs"][sel], 16)
+        on, olor, _ = oracle.build_tree(B[sel], m, cv, cp, qg, qh, e_g, e_h, 6, has_missing=True)
+        d.set_gradients(g, h)
+        info = d.sample(mode, ratio, 1.0, 5, 2, 16)
+        t = d.build_tree(6, keep_debug=True)
+        gn = t.export()
+        for f in on.dtype.names:
+            np.testing.assert_array_equal(gn[f], on[f], err_msg=f"streamed={streamed}: {f}")
+        np.testing.assert_array_equal(t.get_partition(info["n_selected_local"]), olor)
+        m0 = np.zeros(n, np.float32)
+        np.testing.assert_array_equal(d.predict([t], m0.copy()), oracle.predict(B, on, m0, has_missing=True))
+        t.close()
+        d.close()

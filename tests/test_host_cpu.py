@@ -33,7 +33,7 @@ def test_library_exports_every_header_symbol():
     import paper_2005_09148_b200 as ob
     assert sorted(ob.ABI_SYMBOLS) == _header_symbols()
     L = ob.load_library()
-    assert L.oocgb_abi_version() == 1
+    assert L.oocgb_abi_version() == 2  # 2: default_left, has_missing, CSR input (R27)
 
 
 def test_library_is_sm100a():

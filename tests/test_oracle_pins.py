@@ -630,3 +630,182 @@ def test_boosting_round_reduces_loss():
         mm = margin.astype(np.float64)
         losses.append(np.mean(np.log1p(np.exp(-np.where(y > 0, mm, -mm)))))
     assert all(b < a for a, b in zip(losses, losses[1:]))
+
+
+# ------------------------------------------------------------------------------ R27 missing values
+def _greedy_raw_missing(X, qg, qh, e_g, e_h, rows, depth, D, lam, gamma, mcw, out, v):
+    """Exact greedy with missing values (NaN) straight from the raw rows: for every feature, every
+    threshold t among the feature's present distinct values over ALL rows but the largest (its
+    cut points) and both default directions (missing rows right, then left), left = {x <= t}
+    (+ the missing rows for 'left'); so a node can also split present-vs-missing.  Python ints for
+    the sums, Python floats for Eq. 8, (feature, t, direction) order with strict > (R13, R27)."""
+    G, H = int(qg[rows].sum()), int(qh[rows].sum())
+    out[v] = dict(G=G, H=H, n=len(rows), feature=-1)
+    if depth == D or len(rows) == 0:
+        return
+    sc_g, sc_h = 2.0 ** -e_g, 2.0 ** -e_h
+    gP, hP = G * sc_g, H * sc_h
+    tP = (gP * gP) / (hP + lam)
+    best = None
+    for j in range(X.shape[1]):
+        col = X[rows, j]
+        miss = np.isnan(col)
+        allv = X[:, j]
+        vals = np.unique(allv[~np.isnan(allv)])  # the feature's cut points (max_bin >= distinct)
+        for t in vals[:-1]:
+            for dleft in (0, 1):
+                L = rows[(col <= t) | (miss & bool(dleft))]
+                GL, HL = int(qg[L].sum()), int(qh[L].sum())
+                gl, hl, gr, hr = GL * sc_g, HL * sc_h, (G - GL) * sc_g, (H - HL) * sc_h
+                if not (hl >= mcw and hr >= mcw):
+                    continue
+                gain = 0.5 * (((gl * gl) / (hl + lam) + (gr * gr) / (hr + lam)) - tP) - gamma
+                if best is None or gain > best[0]:
+                    best = (gain, j, float(t), dleft, L)
+    if best is None or best[0] <= 0:
+        return
+    gain, j, t, dleft, L = best
+    out[v].update(feature=j, value=t, gain=gain, default_left=dleft)
+    R = np.setdiff1d(rows, L)
+    _greedy_raw_missing(X, qg, qh, e_g, e_h, L, depth + 1, D, lam, gamma, mcw, out, 2 * v + 1)
+    _greedy_raw_missing(X, qg, qh, e_g, e_h, R, depth + 1, D, lam, gamma, mcw, out, 2 * v + 2)
+
+
+def _with_missing(rng, X, rates):
+    X = X.copy()
+    for j, r in enumerate(rates):
+        X[rng.random(X.shape[0]) < r, j] = np.nan
+    return X
+
+
+def test_cuts_bins_skip_missing_values():
+    """R27: the cuts of a feature are the R1 cuts of its present values (np.unique / the ceil rank
+    of np.sort on the non-NaN values); a missing value's symbol is 255; an all-missing feature
+    gets the single cut 0.0 (R1 step 5)."""
+    rng = np.random.default_rng(31)
+    X = rng.normal(size=(3000, 4)).astype(np.float32)
+    X[:, 1] = np.round(X[:, 1] * 2)  # few distinct values
+    X = _with_missing(rng, X, [0.2, 0.5, 0.0, 1.0])
+    B = 64
+    cv, cp = oracle.cuts(X, B)
+    for j in range(4):
+        pres = np.sort(X[~np.isnan(X[:, j]), j])
+        c = cv[cp[j]:cp[j + 1]]
+        if len(pres) == 0:
+            assert list(c) == [0.0]
+        elif len(np.unique(pres)) <= B:
+            np.testing.assert_array_equal(c, np.unique(pres))
+        else:
+            N = len(pres)
+            idx = (np.arange(1, B + 1) * N + B - 1) // B
+            np.testing.assert_array_equal(c, np.unique(pres[idx - 1]))
+    bins = oracle.bins(X, cv, cp)
+    for j in range(4):
+        miss = np.isnan(X[:, j])
+        assert np.all(bins[miss, j] == 255)
+        c = cv[cp[j]:cp[j + 1]]
+        exp = np.minimum(np.searchsorted(c, X[~miss, j], side="left"), len(c) - 1)
+        np.testing.assert_array_equal(bins[~miss, j], exp)
+
+
+def test_missing_values_need_max_bin_255():
+    """Symbol 255 marks a missing value, so a feature with 256 bins cannot hold one (ERR_ARG)."""
+    rng = np.random.default_rng(32)
+    X = rng.normal(size=(2000, 1)).astype(np.float32)
+    cv, cp = oracle.cuts(X, 256)
+    assert cp[1] == 256
+    X[5, 0] = np.nan
+    with pytest.raises(oracle.OracleError):
+        oracle.bins(X, cv, cp)
+    cv, cp = oracle.cuts(X, 255)
+    assert oracle.bins(X, cv, cp)[5, 0] == 255
+
+
+@pytest.mark.parametrize("trial", range(10))
+def test_tree_with_missing_equals_exhaustive_greedy(trial):
+    """R27: the binned oracle with missing values (symbol 255, both default directions) equals the
+    exact greedy tree computed from the raw values with NaN, node by node (feature, value,
+    default direction, gain, sums); every row satisfies its path predicates with missing values
+    following the default directions."""
+    rng = np.random.default_rng(300 + trial)
+    n = int(rng.integers(10, 200))
+    m = int(rng.integers(1, 5))
+    X = np.round(rng.normal(size=(n, m)) * (2 + trial % 3)).astype(np.float32)
+    X = _with_missing(rng, X, rng.uniform(0.0, 0.6, size=m))
+    y = (rng.random(n) < 0.5).astype(np.float32)
+    g, h = oracle.logistic_grad(rng.normal(size=n).astype(np.float32), y)
+    qg, e_g = oracle.quantise(g.astype(np.float64), 16)
+    qh, e_h = oracle.quantise(h.astype(np.float64), 16)
+    cv, cp = oracle.cuts(X, 255)
+    B = oracle.bins(X, cv, cp)
+    D = 4
+    lam, gamma, mcw = [(1.0, 0.0, 1e-3), (0.5, 0.01, 0.0), (1.0, 0.0, 0.2)][trial % 3]
+    nodes, lor, _ = oracle.build_tree(B, m, cv, cp, qg, qh, e_g, e_h, D, lam, gamma, mcw, 1.0, has_missing=True)
+    ref = {}
+    _greedy_raw_missing(X, qg, qh, e_g, e_h, np.arange(n), 0, D, lam, gamma, mcw, ref, 0)
+    for v, r in ref.items():
+        assert nodes["n_rows"][v] == r["n"]
+        assert nodes["sum_g"][v] == r["G"] * 2.0 ** -e_g
+        assert nodes["feature"][v] == r["feature"], f"node {v}"
+        if r["feature"] >= 0:
+            assert nodes["split_value"][v] == np.float32(r["value"])
+            assert nodes["default_left"][v] == r["default_left"], f"node {v}"
+            assert abs(nodes["gain"][v] - r["gain"]) <= 1e-9 * max(1.0, abs(r["gain"]))
+    for i in range(n):
+        v = lor[i]
+        while v > 0:
+            p = (v - 1) // 2
+            x = X[i, nodes["feature"][p]]
+            goes_left = bool(nodes["default_left"][p]) if np.isnan(x) else x <= nodes["split_value"][p]
+            assert goes_left == (v == 2 * p + 1)
+            v = p
+
+
+def test_missing_rows_pick_their_side():
+    """A fixture where only the default direction differs between the candidates: feature 0 is 0
+    on rows 0-29 (g = +1), 1 on rows 30-59 (g = +0.9) and missing on rows 60-89 (g = -1); its one
+    threshold (bin 0) is tried with the missing rows on either side, and the partition follows the
+    default direction the split records (R27)."""
+    n = 90
+    X = np.zeros((n, 1), np.float32)
+    X[30:60, 0] = 1.0
+    X[60:, 0] = np.nan
+    g = np.where(np.arange(n) < 60, 1.0, -1.0)
+    g[30:60] = 0.9
+    h = np.full(n, 0.25)
+    qg, e_g = oracle.quantise(g, 16)
+    qh, e_h = oracle.quantise(h, 16)
+    cv, cp = oracle.cuts(X, 255)
+    B = oracle.bins(X, cv, cp)
+    nodes, lor, _ = oracle.build_tree(B, 1, cv, cp, qg, qh, e_g, e_h, 1, 1.0, 0.0, 0.0, 1.0, has_missing=True)
+    assert nodes["feature"][0] == 0 and nodes["split_bin"][0] == 0
+    exp_left = set(range(30)) if nodes["default_left"][0] == 0 else set(range(30)) | set(range(60, 90))
+    assert set(np.nonzero(lor == 1)[0]) == exp_left
+    assert nodes["gain"][0] > 0
+
+
+def test_predict_with_missing_follows_default_direction():
+    """Binned predict (symbol 255 -> the node's default direction) equals a raw traversal of the
+    tree on the values with NaN."""
+    rng = np.random.default_rng(33)
+    n, m = 400, 3
+    X = _with_missing(rng, np.round(rng.normal(size=(n, m)) * 3).astype(np.float32), [0.3, 0.1, 0.5])
+    y = (rng.random(n) < 0.5).astype(np.float32)
+    g, h = oracle.logistic_grad(rng.normal(size=n).astype(np.float32), y)
+    qg, e_g = oracle.quantise(g.astype(np.float64), 16)
+    qh, e_h = oracle.quantise(h.astype(np.float64), 16)
+    cv, cp = oracle.cuts(X, 255)
+    B = oracle.bins(X, cv, cp)
+    nodes, _, _ = oracle.build_tree(B, m, cv, cp, qg, qh, e_g, e_h, 5, 1.0, 0.0, 0.1, 1.0, has_missing=True)
+    assert (nodes["default_left"][nodes["feature"] >= 0] == 1).any()
+    m0 = rng.normal(size=n).astype(np.float32)
+    got = oracle.predict(B, nodes, m0, has_missing=True)
+    exp = m0.copy()
+    for i in range(n):
+        v = 0
+        while nodes["feature"][v] >= 0:
+            x = X[i, nodes["feature"][v]]
+            left = bool(nodes["default_left"][v]) if np.isnan(x) else x <= nodes["split_value"][v]
+            v = 2 * v + 1 if left else 2 * v + 2
+        exp[i] = exp[i] + nodes["leaf_value"][v]
+    np.testing.assert_array_equal(got, exp)
