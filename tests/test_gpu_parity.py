@@ -77,11 +77,17 @@ def test_cuts_heavy_ties_more_than_B_distinct(ctx, n, max_bin, tie_frac):
 
 
 def test_nonfinite_rejected(ctx):
+    """R4: +-inf is rejected; a NaN is a missing value (R27), accepted whenever the feature's bins
+    leave symbol 255 free (here every feature has one bin)."""
     X = np.ones((10, 3), np.float32)
-    X[4, 1] = np.nan
+    X[4, 1] = np.inf
     with pytest.raises(ob.OocgbError) as e:
         ctx.quantise(X, 256)
     assert e.value.status == ob.ERR_ARG
+    X[4, 1] = np.nan
+    d = ctx.quantise(X, 256)
+    assert d.info()["has_missing"] == 1 and d.get_bins()[4, 1] == 255
+    d.close()
 
 
 def test_sketch_sample_large_n(ctx):
