@@ -71,6 +71,7 @@ const NcclApi &nccl_api() {
   api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
   api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
   api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
+  api.ReduceScatter = (decltype(api.ReduceScatter))sym("ncclReduceScatter");
   api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
   loaded = true;
   return api;
@@ -116,6 +117,37 @@ void allgather_u32(oocgb_ctx c, const uint32_t *d_send, uint32_t *d_recv, size_t
     return;
   }
   OOCGB_NCCL(nccl_api().AllGather(d_send, d_recv, count, ncclUint32, c->comm, c->stream));
+}
+
+void allgather_i64_inplace(oocgb_ctx c, long long *d_buf, size_t count) {
+  if (!c->coll || count == 0) return;
+  if (c->host_coll) {  // the transport gathers by summing blocks that are zero outside their owner
+    std::vector<long long> h(count * c->world, 0);
+    OOCGB_CK(cudaMemcpyAsync(h.data() + (size_t)c->rank * count, d_buf + (size_t)c->rank * count, 8 * count,
+                             cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    OOCGB_REQUIRE(c->host_coll(2, 0, h.data(), (int64_t)count, c->host_coll_user) == 0, OOCGB_ERR_DEVICE,
+                  "host collective (all-gather) failed");
+    OOCGB_CK(cudaMemcpyAsync(d_buf, h.data(), 8 * count * c->world, cudaMemcpyHostToDevice, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
+  OOCGB_NCCL(nccl_api().AllGather(d_buf + (size_t)c->rank * count, d_buf, count, ncclInt64, c->comm, c->stream));
+}
+void reduce_scatter_i64(oocgb_ctx c, const long long *d_send, long long *d_recv, size_t count) {
+  if (!c->coll || count == 0) return;
+  if (c->host_coll) {  // all-reduce of every block, then keep this rank's
+    std::vector<long long> h(count * c->world);
+    OOCGB_CK(cudaMemcpyAsync(h.data(), d_send, 8 * count * c->world, cudaMemcpyDeviceToHost, c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    OOCGB_REQUIRE(c->host_coll(0, 0, h.data(), (int64_t)(count * c->world), c->host_coll_user) == 0,
+                  OOCGB_ERR_DEVICE, "host collective (reduce-scatter) failed");
+    OOCGB_CK(cudaMemcpyAsync(d_recv, h.data() + (size_t)c->rank * count, 8 * count, cudaMemcpyHostToDevice,
+                             c->stream));
+    OOCGB_CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
+  OOCGB_NCCL(nccl_api().ReduceScatter(d_send, d_recv, count, ncclInt64, ncclSum, c->comm, c->stream));
 }
 
 cudaEvent_t pool_event(oocgb_ctx c) {

@@ -41,6 +41,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*ReduceScatter)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   const char *(*GetErrorString)(ncclResult_t);
 };
 const NcclApi &nccl_api();
@@ -346,6 +347,10 @@ void free_work(oocgb_data d);
 void allreduce_sum_i64(oocgb_ctx c, long long *d_buf, size_t count);
 void allreduce_max_u64(oocgb_ctx c, unsigned long long *d_buf, size_t count);
 void allgather_u32(oocgb_ctx c, const uint32_t *d_send, uint32_t *d_recv, size_t count);
+// in place: buf holds world blocks of `count` int64, this rank's block filled (P:L188-190 exchange)
+void allgather_i64_inplace(oocgb_ctx c, long long *d_buf, size_t count);
+// send holds world blocks of `count` int64; recv gets the sum over ranks of this rank's block
+void reduce_scatter_i64(oocgb_ctx c, const long long *d_send, long long *d_recv, size_t count);
 
 // profiling: when ctx->profiling, records an event pair around a phase on the ctx stream
 // (no synchronisation); oocgb_get_timings() later sums the elapsed times into timings[slot].

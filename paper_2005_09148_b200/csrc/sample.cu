@@ -626,6 +626,7 @@ static MvsDev *mvs_state(oocgb_data d) {
   if (!d->d_mvs) {
     d->d_mvs = dmalloc(sizeof(MvsDev));
     d->d_mvs_stats = (unsigned long long *)dmalloc(sizeof(unsigned long long) * 3 * kMvsBuckets);
+    OOCGB_CK(cudaMemsetAsync(d->d_mvs, 0, sizeof(MvsDev), c->stream));  // every field defined
   }
   if (!c->mvs_attr) {  // per ctx (= per device)
     OOCGB_CK(cudaFuncSetAttribute(k_mvs_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, kMvsDecideSmem));

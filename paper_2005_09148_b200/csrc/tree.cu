@@ -88,6 +88,8 @@ struct Work {
   int *partial = nullptr;
   long long *phist[2] = {nullptr, nullptr};
   long long *built64 = nullptr;
+  long long *rs_send = nullptr;  // world > 1: reduce-scatter send buffer [rank][pair][msl][256][2]
+  int msl = 0, max_slots = 0;    // features per rank slice; candidate slots per level
   oocgb::Cand *cand = nullptr;
   int2 *ent = nullptr;  // eval work lists [2][ent_cap]
   int ent_cap = 0;
@@ -353,10 +355,13 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
   }
 }
 
-// Multi-GPU: sum a pair's s32 chunk partials into an int64 [pair][m][256][2] buffer that is
-// then all-reduced.  Thread per (pair, feature, bin).
+// Multi-GPU: sum a pair's s32 chunk partials into int64 histograms that are then reduce-scattered
+// over the ranks ("summed across all GPUs"; each rank receives the sums of its feature
+// slice and evaluates only those features).  Thread per (pair, feature, bin).
+// Multi-GPU (world > 1): the send buffer of the reduce-scatter is sliced by feature owner: rank r
+// owns features [r msl, (r + 1) msl) and receives block r = [pair][feature - r msl][256][2].
 __global__ void k_reduce_partials(const int *__restrict__ partial, const Pair *__restrict__ pairs,
-                                  const LevelCtl *__restrict__ ctl, int m, int n_fg,
+                                  const LevelCtl *__restrict__ ctl, int m, int n_fg, int msl, int lvl_pairs,
                                   long long *__restrict__ out) {
   const int n_pairs = ctl->n_pairs;
   int64_t total = (int64_t)n_pairs * m * kBins;
@@ -373,8 +378,10 @@ __global__ void k_reduce_partials(const int *__restrict__ partial, const Pair *_
       g += v.x;
       h += v.y;
     }
-    out[t * 2] = g;
-    out[t * 2 + 1] = h;
+    const int r = j / msl;
+    const size_t o = (((size_t)r * lvl_pairs + p) * msl + (j - r * msl)) * kBins + b;
+    out[o * 2] = g;
+    out[o * 2 + 1] = h;
   }
 }
 
@@ -401,7 +408,17 @@ struct EvalArgs {
   const int2 *ent;  // per-level work lists of (pair, side): general [0, n_ew), narrow [ent_cap, + n_en)
   int ent_cap;
   int has_missing;  // R27: bin 255 holds missing values; candidates in both default directions
+  // feature slice (world > 1: this rank evaluates features [f0, f0 + mf) from reduce-scattered
+  // histograms whose rows hold hm = msl features; world == 1: f0 = 0, mf = hm = msl = m)
+  int f0, mf, hm, msl, max_slots;
 };
+
+// candidates [owner rank][slot][msl]: rank r writes features [r msl, (r + 1) msl) into block r,
+// the blocks are all-gathered, and every rank's k_finalize reads all m features
+__host__ __device__ __forceinline__ size_t cand_index(int msl, int max_slots, int slot, int j) {
+  const int r = j / msl;
+  return ((size_t)r * max_slots + slot) * msl + (j - r * msl);
+}
 
 __device__ __forceinline__ int warp_excl_scan_i(int v, int lane, int &total) {
   int incl = v;
@@ -561,7 +578,7 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
     cd.valid = any ? 1 : 0;
     cd.GL = any ? bGL : 0;
     cd.HL = any ? bHL : 0;
-    A.cand[(size_t)slot * A.m + j] = cd;
+    A.cand[cand_index(A.msl, A.max_slots, slot, j)] = cd;
   }
   return owner;
 }
@@ -603,25 +620,27 @@ __device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int sid
   const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;  // prefetched for eval_node
   const long long nodeRows = A.dn[node].n_rows;
   long long g[8], h[8];  // strided: element i is bin 32 i + lane
-  const size_t hsz = (size_t)A.m * kBins * 2;
+  const size_t hsz = (size_t)A.hm * kBins * 2;  // built64 / parent rows: this rank's feature slice
+  const int jl = j - A.f0;
+  const size_t dsz = (size_t)A.m * kBins * 2;    // debug dumps: every feature
   longlong2 par[8];
   if (side) {  // parent loads first so they overlap the chunk loads
     const int ps = P.parent - level_first(A.d - 1);
     if (P.compact & 1) {  // compact s32 parent (exact: |sum| < 2^31)
-      const int2 *src = reinterpret_cast<const int2 *>(A.phist_prev + (size_t)ps * hsz) + (size_t)j * kBins;
+      const int2 *src = reinterpret_cast<const int2 *>(A.phist_prev + (size_t)ps * hsz) + (size_t)jl * kBins;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int2 v = __ldg(src + 32 * i + lane);
         par[i] = make_longlong2(v.x, v.y);
       }
     } else {
-      const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + (size_t)j * kBins * 2);
+      const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + (size_t)jl * kBins * 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i) par[i] = __ldg(src + 32 * i + lane);
     }
   }
   if (A.built64) {
-    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.built64 + (size_t)p * hsz + (size_t)j * kBins * 2);
+    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.built64 + (size_t)p * hsz + (size_t)jl * kBins * 2);
 #pragma unroll
     for (int i = 0; i < 8; ++i) { longlong2 v = src[32 * i + lane]; g[i] = v.x; h[i] = v.y; }
   } else {
@@ -657,17 +676,17 @@ __device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int sid
   const int f_d = level_first(A.d);
   if (A.d <= A.D - 2 && !A.streamed) {
     if (P.compact & (side ? 4 : 2)) {
-      int2 *dst = reinterpret_cast<int2 *>(A.phist_next + (size_t)(node - f_d) * hsz) + (size_t)j * kBins;
+      int2 *dst = reinterpret_cast<int2 *>(A.phist_next + (size_t)(node - f_d) * hsz) + (size_t)jl * kBins;
 #pragma unroll
       for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_int2((int)g[i], (int)h[i]);
     } else {
-      longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)j * kBins * 2);
+      longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)jl * kBins * 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
     }
   }
   if (A.dbg) {
-    longlong2 *dst = reinterpret_cast<longlong2 *>(A.dbg + (size_t)node * hsz + (size_t)j * kBins * 2);
+    longlong2 *dst = reinterpret_cast<longlong2 *>(A.dbg + (size_t)node * dsz + (size_t)j * kBins * 2);
 #pragma unroll
     for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
   }
@@ -704,12 +723,12 @@ template <bool HAS_MISSING>
 __global__ void __launch_bounds__(kEvalWarps * 32, kEvalBlocksWide) k_eval(EvalArgs A) {
   __shared__ longlong2 tile[kEvalWarps][256 + 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int n_items = A.ctl->n_ew * A.m;
+  const int n_items = A.ctl->n_ew * A.mf;
   const int nw = (int)(gridDim.x * blockDim.x) >> 5;
   for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < n_items; t += nw) {
-    const int e = t / A.m;
+    const int e = t / A.mf;
     const int2 en = A.ent[e];
-    eval_item_wide<HAS_MISSING>(A, en.x, en.y, t - e * A.m, lane, tile[wib]);
+    eval_item_wide<HAS_MISSING>(A, en.x, en.y, A.f0 + t - e * A.mf, lane, tile[wib]);
   }
 }
 
@@ -728,16 +747,18 @@ __device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int s
   if (A.streamed && A.dn[node].feature == -2) return;
   const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;
   int g[8], h[8];  // strided: element i is bin 32 i + lane
-  const size_t hsz = (size_t)A.m * kBins * 2;
+  const size_t hsz = (size_t)A.hm * kBins * 2;  // built64 / parent rows: this rank's feature slice
+  const int jl = j - A.f0;
+  const size_t dsz = (size_t)A.m * kBins * 2;    // debug dumps: every feature
   int2 par[8];
   if (side) {
     const int ps = P.parent - level_first(A.d - 1);
     if (P.compact & 1) {
-      const int2 *src = reinterpret_cast<const int2 *>(A.phist_prev + (size_t)ps * hsz) + (size_t)j * kBins;
+      const int2 *src = reinterpret_cast<const int2 *>(A.phist_prev + (size_t)ps * hsz) + (size_t)jl * kBins;
 #pragma unroll
       for (int i = 0; i < 8; ++i) par[i] = __ldg(src + 32 * i + lane);
     } else {  // low words of the int64 pairs
-      const int4 *src = reinterpret_cast<const int4 *>(A.phist_prev + (size_t)ps * hsz + (size_t)j * kBins * 2);
+      const int4 *src = reinterpret_cast<const int4 *>(A.phist_prev + (size_t)ps * hsz + (size_t)jl * kBins * 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int4 v = __ldg(src + 32 * i + lane);
@@ -746,7 +767,7 @@ __device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int s
     }
   }
   if (A.built64) {
-    const int4 *src = reinterpret_cast<const int4 *>(A.built64 + (size_t)p * hsz + (size_t)j * kBins * 2);
+    const int4 *src = reinterpret_cast<const int4 *>(A.built64 + (size_t)p * hsz + (size_t)jl * kBins * 2);
 #pragma unroll
     for (int i = 0; i < 8; ++i) { const int4 v = src[32 * i + lane]; g[i] = v.x; h[i] = v.z; }
   } else {
@@ -770,17 +791,17 @@ __device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int s
   const int f_d = level_first(A.d);
   if (A.d <= A.D - 2 && !A.streamed) {
     if (P.compact & (side ? 4 : 2)) {
-      int2 *dst = reinterpret_cast<int2 *>(A.phist_next + (size_t)(node - f_d) * hsz) + (size_t)j * kBins;
+      int2 *dst = reinterpret_cast<int2 *>(A.phist_next + (size_t)(node - f_d) * hsz) + (size_t)jl * kBins;
 #pragma unroll
       for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_int2(g[i], h[i]);
     } else {
-      longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)j * kBins * 2);
+      longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)jl * kBins * 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
     }
   }
   if (A.dbg) {
-    longlong2 *dst = reinterpret_cast<longlong2 *>(A.dbg + (size_t)node * hsz + (size_t)j * kBins * 2);
+    longlong2 *dst = reinterpret_cast<longlong2 *>(A.dbg + (size_t)node * dsz + (size_t)j * kBins * 2);
 #pragma unroll
     for (int i = 0; i < 8; ++i) dst[32 * i + lane] = make_longlong2(g[i], h[i]);
   }
@@ -807,12 +828,12 @@ template <bool HAS_MISSING>
 __global__ void __launch_bounds__(kEvalWarps * 32, OOCGB_EVAL_NARROW_MINB) k_eval_narrow(EvalArgs A) {
   __shared__ int2 tile2[kEvalWarps][256 + 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int n_items = A.ctl->n_en * A.m;
+  const int n_items = A.ctl->n_en * A.mf;
   const int nw = (int)(gridDim.x * blockDim.x) >> 5;
   for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < n_items; t += nw) {
-    const int e = t / A.m;
+    const int e = t / A.mf;
     const int2 en = A.ent[A.ent_cap + e];
-    eval_item_narrow<HAS_MISSING>(A, en.x, en.y, t - e * A.m, lane, tile2[wib]);
+    eval_item_narrow<HAS_MISSING>(A, en.x, en.y, A.f0 + t - e * A.mf, lane, tile2[wib]);
   }
 }
 
@@ -839,9 +860,9 @@ __device__ __forceinline__ BestSplit shfl_best(const BestSplit &x, int o) {
 }
 
 __global__ void __launch_bounds__(256)
-k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Cand *__restrict__ cand,
-           DNode *dn, const float *__restrict__ cut_values, const int *__restrict__ cut_ptrs,
-           const RoundParams *__restrict__ rp, double lambda, double eta) {
+k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs, LevelCtl *ctl,
+           const Cand *__restrict__ cand, DNode *dn, const float *__restrict__ cut_values,
+           const int *__restrict__ cut_ptrs, const RoundParams *__restrict__ rp, double lambda, double eta) {
   const int p = blockIdx.x >> 1;
   if (p >= ctl->n_pairs) return;
   const Pair P = pairs[p];
@@ -851,7 +872,7 @@ k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Ca
   const int slot = node - level_first(d);
   BestSplit best{0.0, 0, 0x7fffffff, 0, 0, 0};
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    const Cand cd = cand[(size_t)slot * m + j];
+    const Cand cd = cand[cand_index(msl, max_slots, slot, j)];
     BestSplit x{cd.gain, cd.valid, j, cd.bin, cd.GL, cd.HL};
     if (better(x, best)) best = x;
   }
@@ -886,8 +907,9 @@ k_finalize(int d, int m, const Pair *__restrict__ pairs, LevelCtl *ctl, const Ca
   }
 }
 
-static void launch_eval(const EvalArgs &A, int max_pairs, int num_sms, cudaStream_t st) {
-  const int64_t blocks = ((int64_t)max_pairs * A.m * 2 + kEvalWarps - 1) / kEvalWarps;
+static void launch_eval(const EvalArgs &A, int max_pairs, oocgb_ctx c, cudaStream_t st) {
+  const int num_sms = c->num_sms;
+  const int64_t blocks = ((int64_t)max_pairs * std::max(1, A.mf) * 2 + kEvalWarps - 1) / kEvalWarps;
   const unsigned gw = (unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * kEvalBlocksWide);
   const unsigned gn = (unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * OOCGB_EVAL_NARROW_MINB);
   if (A.has_missing) {  // R27: candidates in both default directions
@@ -897,8 +919,13 @@ static void launch_eval(const EvalArgs &A, int max_pairs, int num_sms, cudaStrea
     k_eval<false><<<gw, kEvalWarps * 32, 0, st>>>(A);
     k_eval_narrow<false><<<gn, kEvalWarps * 32, 0, st>>>(A);
   }
-  k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, st>>>(A.d, A.m, A.pairs, A.ctl, A.cand, A.dn, A.cut_values,
-                                                         A.cut_ptrs, A.rp, A.lambda, A.eta);
+  OOCGB_CK(cudaGetLastError());
+  // world > 1: every rank evaluated its feature slice; gather the candidates of all features
+  if (c->coll && !A.streamed)
+    allgather_i64_inplace(c, reinterpret_cast<long long *>(A.cand),
+                          (size_t)A.max_slots * A.msl * (sizeof(Cand) / sizeof(long long)));
+  k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, st>>>(A.d, A.m, A.msl, A.max_slots, A.pairs, A.ctl, A.cand, A.dn,
+                                                         A.cut_values, A.cut_ptrs, A.rp, A.lambda, A.eta);
   OOCGB_CK(cudaGetLastError());
 }
 
@@ -1536,11 +1563,17 @@ static void ensure_work(oocgb_data d, int D) {
   w->seg_cnt = (long long *)dmalloc(sizeof(long long) * 2 * max_segs);
   w->pairs = (Pair *)dmalloc(sizeof(Pair) * max_pairs);
   w->partial = (int *)dmalloc((size_t)items * kFG * kBins * 2 * sizeof(int));
-  const size_t hsz = (size_t)m * kBins * 2;
+  // world > 1: each rank evaluates a slice of msl = ceil(m / W) features (reduce-scattered
+  // histograms), so parent histograms and the received sums hold msl features per row
+  const int W = c->coll ? c->world : 1;
+  w->msl = (m + W - 1) / W;
+  w->max_slots = (int)(2 * max_pairs);
+  const size_t hsz = (size_t)m * kBins * 2, hsl = (size_t)w->msl * kBins * 2;
   const int64_t pslots = D >= 2 ? (1LL << (D - 2)) : 1;
-  for (int i = 0; i < 2; ++i) w->phist[i] = (long long *)dmalloc(sizeof(long long) * hsz * pslots);
+  for (int i = 0; i < 2; ++i) w->phist[i] = (long long *)dmalloc(sizeof(long long) * hsl * pslots);
   if (need64) w->built64 = (long long *)dmalloc(sizeof(long long) * hsz * 2 * max_pairs);
-  w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)max_pairs * 2 * m);
+  if (c->coll) w->rs_send = (long long *)dmalloc(sizeof(long long) * hsl * (size_t)W * max_pairs);
+  w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)W * w->max_slots * w->msl);
   w->ent_cap = (int)(2 * max_pairs);
   w->ent = (int2 *)dmalloc(sizeof(int2) * 2 * w->ent_cap);
   w->dnodes = (DNode *)dmalloc(sizeof(DNode) * ((1LL << (D + 1)) - 1));
@@ -1559,7 +1592,7 @@ void free_work(oocgb_data d) {
   Work *w = d->work;
   if (!w) return;
   for (int i = 0; i < 2; ++i) { dfree(w->ridx[i]); dfree(w->q[i]); dfree(w->segs[i]); dfree(w->phist[i]); }
-  dfree(w->seg_cur[0]); dfree(w->seg_cur[1]); dfree(w->tile_seg); dfree(w->chunk_pair); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64);
+  dfree(w->seg_cur[0]); dfree(w->seg_cur[1]); dfree(w->tile_seg); dfree(w->chunk_pair); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64); dfree(w->rs_send);
   dfree(w->cand); dfree(w->ent); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg); dfree(w->d_rp);
   dfree(w->sw.row_node); dfree(w->sw.b_slot); dfree(w->sw.b_ridx); dfree(w->sw.b_q); dfree(w->sw.slot_cnt);
   dfree(w->sw.slot_cur);
@@ -1620,11 +1653,11 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
                                                                  d->gw == 64 ? 1 : 0);
     OOCGB_CK(cudaGetLastError());
     mark(0, false);
-    if (c->coll) {
+    if (c->coll) {  // every rank receives the global sums of its feature slice
       int64_t tot = (int64_t)max_pairs * m * kBins;
       k_reduce_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
-          w->partial, w->pairs, w->ctl, m, n_fg, w->built64);
-      allreduce_sum_i64(c, w->built64, hsz * max_pairs);
+          w->partial, w->pairs, w->ctl, m, n_fg, w->msl, max_pairs, w->rs_send);
+      reduce_scatter_i64(c, w->rs_send, w->built64, (size_t)max_pairs * w->msl * kBins * 2);
     }
     mark(1, true);
     EvalArgs A;
@@ -1638,7 +1671,10 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 0;
     A.cut_values = d->d_cut_values; A.eta = eta;
     A.ent = w->ent; A.ent_cap = w->ent_cap; A.has_missing = d->has_missing ? 1 : 0;
-    launch_eval(A, max_pairs, c->num_sms, c->stream);
+    A.msl = w->msl; A.max_slots = w->max_slots; A.hm = w->msl;
+    A.f0 = c->coll ? std::min(m, c->rank * w->msl) : 0;
+    A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
+    launch_eval(A, max_pairs, c, c->stream);
     mark(1, false);
     mark(2, true);
     PlanArgs PA;
@@ -1668,6 +1704,8 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     mark(2, false);
     cur ^= 1;
   }
+  // world > 1: each rank dumped its feature slice of every node histogram (debug builds only)
+  if (keep_debug && c->coll) allreduce_sum_i64(c, w->dbg, hsz * (size_t)std::max(1, (1 << D) - 1));
   w->final_cur = cur;
 }
 
@@ -2016,7 +2054,10 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 1;
     A.cut_values = d->d_cut_values; A.eta = eta;
     A.ent = w->ent; A.ent_cap = w->ent_cap; A.has_missing = d->has_missing ? 1 : 0;
-    launch_eval(A, n_slots, c->num_sms, c->stream);
+    A.msl = w->msl; A.max_slots = w->max_slots; A.hm = w->msl;
+    A.f0 = c->coll ? std::min(m, c->rank * w->msl) : 0;
+    A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
+    launch_eval(A, n_slots, c, c->stream);
   }
   // export (same as the in-core path)
   const DNode *hn = w->h_dn;

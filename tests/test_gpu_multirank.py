@@ -34,8 +34,10 @@ g_all, h_all = oracle.logistic_grad(margin, y)  # host gradients: identical inpu
 d.set_gradients(g_all[row0:row0 + nl], h_all[row0:row0 + nl])
 info = d.sample(mode, ratio, 1.0, seed=7, round=2, quant_bits=16)
 gid, qg, qh = d.get_sample(info["n_selected_local"])
-t = d.build_tree(depth)
+t = d.build_tree(depth, keep_debug=True)
 nodes = t.export()
+hist0 = t.get_histogram(0)   # complete over all features (each rank evaluated a feature slice)
+hist1 = t.get_histogram(1) if nodes["feature"][0] >= 0 else None
 cv, cp = d.get_cuts()
 pm = d.predict([t], np.zeros(nl, np.float32))
 res = dict(rank=rank, cuts=cv.tobytes().hex()[:4000], ncuts=int(cp[-1]), cuts_hash=hash(cv.tobytes()),
@@ -71,9 +73,12 @@ if rank == 0:
     oqg, oe_g = oracle.quantise(s_["gs"][sel_], 16)
     oqh, oe_h = oracle.quantise(s_["hs"][sel_], 16)
     assert (oe_g, oe_h) == (info["e_g"], info["e_h"]), "fixed-point exponents differ from the oracle"
-    on_, _, _ = oracle.build_tree(OB[sel_], m, ocv, ocp, oqg, oqh, oe_g, oe_h, depth)
+    on_, _, ohist_ = oracle.build_tree(OB[sel_], m, ocv, ocp, oqg, oqh, oe_g, oe_h, depth, want_hist=True)
     for f in on_.dtype.names:
         assert np.array_equal(on_[f], nodes[f]), f"tree field {f} differs (2 ranks vs oracle)"
+    assert np.array_equal(hist0, ohist_[0]), "root histogram differs from the oracle"
+    if hist1 is not None:
+        assert np.array_equal(hist1, ohist_[1]), "node-1 histogram differs from the oracle"
     op = oracle.predict(OB, on_, np.zeros(n, np.float32))
     assert np.array_equal(op[row0:row0 + nl], pm), "predict differs from the oracle"
     print("RANK0-REFERENCE-OK", info["n_selected_global"], int((n1["feature"] >= 0).sum()))
@@ -96,15 +101,19 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("n,m,mode,ratio", [(30000, 40, 0, 1.0), (25000, 33, 2, 0.3), (20000, 24, 1, 0.5),
-                                            ((1 << 20) + 5000, 8, 2, 0.1)])
-def test_two_ranks_one_gpu_bit_exact(ctx, tmp_path, n, m, mode, ratio):
+@pytest.mark.parametrize("n,m,mode,ratio,world", [(30000, 40, 0, 1.0, 2), (25000, 33, 2, 0.3, 2),
+                                                  (20000, 24, 1, 0.5, 2), ((1 << 20) + 5000, 8, 2, 0.1, 2),
+                                                  (20000, 8, 0, 1.0, 3)])
+def test_two_ranks_one_gpu_bit_exact(ctx, tmp_path, n, m, mode, ratio, world):
+    """World 2 (and 3: feature slices of 3, 3 and 2 features) on one GPU through the host transport:
+    sharded rows, reduce-scattered histograms with a feature-sharded evaluation, all-gathered
+    candidates -- bit-identical to 1 rank and to the oracle."""
     script = tmp_path / "w.py"
     script.write_text(WORKER)
     port = _port()
     procs = []
-    for r in range(2):
-        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
                    MASTER_PORT=str(port), OOCGB_ROOT=ROOT, N=str(n), M=str(m), MODE=str(mode), RATIO=str(ratio))
         procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
                                       stderr=subprocess.STDOUT, text=True))
