@@ -98,7 +98,8 @@ typedef struct {
  * oocgb_nccl_unique_id: rank 0 creates the NCCL id; the caller broadcasts the 128 bytes
  * (e.g. with torch.distributed) and passes them to oocgb_ctx_create on every rank.
  * oocgb_ctx_create: binds `device`; rank/world describe the row sharding (the
- * histograms are "summed across all GPUs using AllReduce").  nccl_id may be NULL iff
+ * histograms are "summed across all GPUs"; here a reduce-scatter by feature slice, each rank
+ * evaluates its slice and the candidates are all-gathered).  nccl_id may be NULL iff
  * world == 1; world == 1 WITH an nccl_id runs the multi-GPU code path (every exchange step
  * through NCCL) on a 1-rank communicator, results identical to the plain context (tests).  cuda_stream: a cudaStream_t cast to uint64 to order work on, 0 = library
  * creates its own non-blocking stream.  ERR_ARG on rank/world mismatch; ERR_DEVICE on
@@ -110,7 +111,8 @@ int oocgb_ctx_destroy(oocgb_ctx ctx);
 
 /* Test-only transport for the exchange steps (several ranks sharing one GPU, or no NCCL):
  * every collective is run as: synchronise the ctx stream, copy the device buffer to host,
- * call fn, copy back.  op: 0 all-reduce sum, 1 all-reduce max, 2 all-gather (buf holds
+ * call fn, copy back (a reduce-scatter is an all-reduce sum of every block, then the rank keeps
+ * its own).  op: 0 all-reduce sum, 1 all-reduce max, 2 all-gather (buf holds
  * world * count elements, this rank's block at rank * count); dtype: 0 int64, 1 uint64,
  * 2 uint32.  fn returns 0 on success.  The compute path is unchanged (all kernels on the GPU);
  * build_tree is not graph-captured in this mode.  ERR_ARG if fn is NULL or world < 1.       */

@@ -1671,7 +1671,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 0;
     A.cut_values = d->d_cut_values; A.eta = eta;
     A.ent = w->ent; A.ent_cap = w->ent_cap; A.has_missing = d->has_missing ? 1 : 0;
-    A.msl = w->msl; A.max_slots = w->max_slots; A.hm = w->msl;
+    A.msl = w->msl; A.max_slots = 2 * max_pairs; A.hm = w->msl;  // candidate blocks sized for this level
     A.f0 = c->coll ? std::min(m, c->rank * w->msl) : 0;
     A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
     launch_eval(A, max_pairs, c, c->stream);
@@ -2054,7 +2054,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     A.lambda = lambda; A.gamma = gamma; A.mcw = mcw; A.rp = w->d_rp; A.kmax = kmax; A.streamed = 1;
     A.cut_values = d->d_cut_values; A.eta = eta;
     A.ent = w->ent; A.ent_cap = w->ent_cap; A.has_missing = d->has_missing ? 1 : 0;
-    A.msl = w->msl; A.max_slots = w->max_slots; A.hm = w->msl;
+    A.msl = w->msl; A.max_slots = n_slots; A.hm = w->msl;
     A.f0 = c->coll ? std::min(m, c->rank * w->msl) : 0;
     A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
     launch_eval(A, n_slots, c, c->stream);
