@@ -487,38 +487,30 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
   };
   const I hmin = clampI(rp.h_min);
   const I hmax = clampI((long long)H_ - rp.h_min);
-  const float lamf = (float)A.lambda;
-  const float gPf = (float)G * rp.sg_inv_f, hPf = (float)H * rp.sh_inv_f;
-  const float tPf = __fdividef(gPf * gPf, hPf + lamf);
-  const float gamf = (float)A.gamma;
-  // Error bound of the float gain: each float op adds <= 2^-24 relative error (the two divisions
-  // <= 2 ulp), so every term carries <= ~10 2^-24 and 2^-18 (tL + tR + tP + |gamma|) bounds the
-  // error with a >= 6x margin (tL, tR, tP >= 0: squares over positive denominators).  Its per-node
-  // part is hoisted; with the pre-filter off every valid candidate survives (tol = inf).
-  const float tol0 = rp.prefilter ? 0x1p-18f * (tPf + fabsf(gamf)) + 0x1p-100f : INFINITY;
-  // Folded scales, branch-free: with sg = 2^-e_g, sh = 2^-e_h (exact powers of two) the float
-  // terms are tL = c GL^2 / (HL + lq) with c = sg^2 / sh and lq = lambda / sh, the same values up
-  // to rounding order as the unfolded form; the gain and its bound scale by c exactly (the
-  // pre-filter is on only when c and lq are normal floats, see k_init_build).
-  const float c = rp.fold_c, lq = rp.fold_lq;  // hoisted to k_init_build (same values)
-  const float chalf = 0.5f * c, tolc = 0x1p-18f * c, K = 0.5f * tPf + gamf;
+  // Float pre-filter on T = GL^2 / (HL + lq) + GR^2 / (HR + lq) (folded scales: with sg = 2^-e_g,
+  // sh = 2^-e_h exact powers of two, tL + tR = c T with c = sg^2 / sh, lq = lambda / sh; the
+  // pre-filter is on only while c and lq are normal floats, see k_init_build).  For one node the
+  // gain 0.5 (c T - tP) - gamma is increasing in T, so the exact argmax (and every exact tie) has
+  // the largest exact T.  The float T carries <= ~8 2^-24 relative error (int -> float, squares, the
+  // lambda add, two __fdividef of <= 2 ulp, the sum) and the double evaluation of the gain
+  // rounds at ~2^-50 of c T + tP, so keeping every candidate with T_f >= (1 - 2^-18) max T_f
+  // keeps the true argmax and its ties with a >= 8x margin; only those are evaluated in double.
+  const float lq = rp.fold_lq;
   // candidate key 2 b + dir: dir 0 = missing rows right (left sums = the prefix), dir 1 = missing
   // rows left (prefix + the missing bin's sums; MISS only, R27)
-  float ub[MISS ? 2 : 1][8];
+  float tv[MISS ? 2 : 1][8];  // T_f; -inf invalid; +inf not finite (always re-evaluated)
   unsigned vmask = 0;  // bit 2 i + dir
-  float Lmax = -INFINITY;
+  float Tmax = -INFINITY;
   auto pre = [&](I GLx, I HLx, bool vb, float &u, int bit) {
     const bool v = vb && HLx >= hmin && HLx <= hmax;
     const float GLf = (float)GLx, HLf = (float)HLx, GRf = (float)(G - GLx), HRf = (float)(H - HLx);
     const float T = __fdividef(GLf * GLf, HLf + lq) + __fdividef(GRf * GRf, HRf + lq);
-    const float gain = chalf * T - K;
-    const float tol = tolc * T + tol0;  // NaN / inf when a term is not finite
-    const bool fin = tol < INFINITY;
+    const bool fin = T < INFINITY;  // false for inf and NaN
     vmask |= v ? 1u << bit : 0u;
-    u = v ? (fin ? gain + tol : INFINITY) : -INFINITY;
-    Lmax = fmaxf(Lmax, (v && fin) ? gain - tol : -INFINITY);
+    u = v ? (fin ? T : INFINITY) : -INFINITY;
+    Tmax = fmaxf(Tmax, (v && fin) ? T : -INFINITY);
   };
-  // pass 1: float gains; ub = gain + tol (inf for a non-finite term: always re-evaluated)
+  // pass 1: float T of every candidate
   I GL = eg, HL = eh;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -527,11 +519,12 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
     const int b = lane * 8 + i;
     // an empty bin repeats the previous candidate exactly, which wins the tie (lower bin)
     const bool vb = b <= B - 2 && ((g[i] | h[i]) != 0 || b == 0);
-    pre(GL, HL, vb, ub[0][i], 2 * i);
-    if constexpr (MISS) pre(GL + Gm, HL + Hm, vb, ub[MISS ? 1 : 0][i], 2 * i + 1);
+    pre(GL, HL, vb, tv[0][i], 2 * i);
+    if constexpr (MISS) pre(GL + Gm, HL + Hm, vb, tv[MISS ? 1 : 0][i], 2 * i + 1);
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) Lmax = fmaxf(Lmax, __shfl_xor_sync(0xffffffffu, Lmax, o));
+  for (int o = 16; o; o >>= 1) Tmax = fmaxf(Tmax, __shfl_xor_sync(0xffffffffu, Tmax, o));
+  const float thr = rp.prefilter ? Tmax * (1.0f - 0x1p-18f) : -INFINITY;
   // pass 2: exact double gains of the survivors, in key order (strict > keeps the lower key)
   double tP = 0.0;
   {
@@ -549,7 +542,7 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
     HL += h[i];
 #pragma unroll
     for (int dir = 0; dir < (MISS ? 2 : 1); ++dir) {
-      if (((vmask >> (2 * i + dir)) & 1u) && ub[dir][i] >= Lmax) {
+      if (((vmask >> (2 * i + dir)) & 1u) && tv[dir][i] >= thr) {
         const I GLx = dir ? GL + Gm : GL, HLx = dir ? HL + Hm : HL;
         const double gain = gain_exact(GLx, HLx, G, H, tP, rp.sg_inv, rp.sh_inv, A.lambda, A.gamma);
         if (!have || gain > best) {
