@@ -86,6 +86,7 @@ struct DNode {
   long long Gq, Hq;    // fixed-point sums (global)
   int32_t default_left;  // R27: missing values (symbol 255) go left
   int32_t pad;
+  double tP;             // G^2 / (H + lambda) of the node (Eq. 8's parent term), set with the sums
 };
 
 // Row segment of the partition at one depth (pass-through segments carry leaves).

@@ -124,6 +124,7 @@ __device__ void node_fill(DNode &nd, long long Gq, long long Hq, double sg_inv, 
   nd.sum_h = h;
   double den = __dadd_rn(h, lambda);
   if (!(den > 0.0)) atomicExch(err, 1);
+  nd.tP = __ddiv_rn(__dmul_rn(g, g), den);  // the split evaluation's parent term (R14 order)
   double w = __ddiv_rn(-g, den);
   nd.leaf_value = __double2float_rn(__dmul_rn(eta, w));
 }
@@ -464,8 +465,8 @@ __device__ __forceinline__ double gain_exact(long long GL, long long HL, long lo
 // Returns the lane that owns the winning bin (it wrote the candidate), or 0.
 template <typename I, bool MISS>
 __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, const I (&g)[8], const I (&h)[8],
-                              const RoundParams &rp, const long long G_, const long long H_, const I Gm,
-                              const I Hm) {
+                              const RoundParams &rp, const long long G_, const long long H_, const double tP,
+                              const I Gm, const I Hm) {
   const int B = A.cut_ptrs[j + 1] - A.cut_ptrs[j];
   const I G = (I)G_, H = (I)H_;
   I lg = 0, lh = 0;
@@ -526,11 +527,6 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
   for (int o = 16; o; o >>= 1) Tmax = fmaxf(Tmax, __shfl_xor_sync(0xffffffffu, Tmax, o));
   const float thr = rp.prefilter ? Tmax * (1.0f - 0x1p-18f) : -INFINITY;
   // pass 2: exact double gains of the survivors, in key order (strict > keeps the lower key)
-  double tP = 0.0;
-  {
-    const double gP = __dmul_rn((double)G, rp.sg_inv), hP = __dmul_rn((double)H, rp.sh_inv);
-    tP = __ddiv_rn(__dmul_rn(gP, gP), __dadd_rn(hP, A.lambda));
-  }
   double best = 0.0;
   int bkey = 0x7fffffff, have = 0;
   long long bGL = 0, bHL = 0;
@@ -582,12 +578,12 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
 template <typename I, bool HAS_MISSING>
 __device__ int eval_node(const EvalArgs &A, int node, int j, int lane, const I (&g)[8],
                                          const I (&h)[8], const RoundParams &rp, const long long G_,
-                                         const long long H_) {
+                                         const long long H_, const double tP) {
   if constexpr (HAS_MISSING) {  // a separate kernel instantiation: dense data keeps its registers
     const I Gm = __shfl_sync(0xffffffffu, g[7], 31), Hm = __shfl_sync(0xffffffffu, h[7], 31);
-    if (Gm != 0 || Hm != 0) return eval_node_impl<I, true>(A, node, j, lane, g, h, rp, G_, H_, Gm, Hm);
+    if (Gm != 0 || Hm != 0) return eval_node_impl<I, true>(A, node, j, lane, g, h, rp, G_, H_, tP, Gm, Hm);
   }
-  return eval_node_impl<I, false>(A, node, j, lane, g, h, rp, G_, H_, (I)0, (I)0);
+  return eval_node_impl<I, false>(A, node, j, lane, g, h, rp, G_, H_, tP, (I)0, (I)0);
 }
 
 __device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)[8], const long long (&h)[8]) {
@@ -611,6 +607,7 @@ __device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int sid
   if (node < 0) return;
   if (A.streamed && A.dn[node].feature == -2) return;  // streamed levels list every slot
   const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;  // prefetched for eval_node
+  const double nodeTP = A.dn[node].tP;
   const long long nodeRows = A.dn[node].n_rows;
   long long g[8], h[8];  // strided: element i is bin 32 i + lane
   const size_t hsz = (size_t)A.hm * kBins * 2;  // built64 / parent rows: this rank's feature slice
@@ -704,9 +701,9 @@ __device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int sid
     int g32[8], h32[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) { g32[i] = (int)g[i]; h32[i] = (int)h[i]; }
-    eval_node<int, HAS_MISSING>(A, node, j, lane, g32, h32, rp, nodeG, nodeH);
+    eval_node<int, HAS_MISSING>(A, node, j, lane, g32, h32, rp, nodeG, nodeH, nodeTP);
   } else {
-    eval_node<long long, HAS_MISSING>(A, node, j, lane, g, h, rp, nodeG, nodeH);
+    eval_node<long long, HAS_MISSING>(A, node, j, lane, g, h, rp, nodeG, nodeH, nodeTP);
   }
 }
 
@@ -739,6 +736,7 @@ __device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int s
   if (node < 0) return;
   if (A.streamed && A.dn[node].feature == -2) return;
   const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;
+  const double nodeTP = A.dn[node].tP;
   int g[8], h[8];  // strided: element i is bin 32 i + lane
   const size_t hsz = (size_t)A.hm * kBins * 2;  // built64 / parent rows: this rank's feature slice
   const int jl = j - A.f0;
@@ -813,7 +811,7 @@ __device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int s
   }
   __syncwarp();  // the tile is reused by the warp's next item
   const RoundParams rp = *A.rp;
-  eval_node<int, HAS_MISSING>(A, node, j, lane, g, h, rp, nodeG, nodeH);
+  eval_node<int, HAS_MISSING>(A, node, j, lane, g, h, rp, nodeG, nodeH, nodeTP);
 }
 
 // Persistent warps over the level's narrow list (nodes with <= kmax global rows, from the plan).
