@@ -5,7 +5,7 @@
  * THIS IS TEST INFRASTRUCTURE, NOT PRODUCT CODE.  Only tests/, __graft_entry__.smoke() and
  * bench.py's cpu_baseline / --impl reference legs may load it.  It shares no code, header,
  * table or constant generator with the CUDA library under paper_2005_09148_b200/; the two
- * meet only through the seeded input generators (paper_2005_09148_b200_inputs/) and the tests.
+ * meet only through the seeded input generators (synth/) and the tests.
  *
  * Citations: "P:Lx" = PAPER.md line x; "S:Lx" = SPEC.md line x (interface/test ideas only);
  * "Ox" = the reading numbered in DESIGN.md §3 (restated from SURVEY.md §8(c)).
