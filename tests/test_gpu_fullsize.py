@@ -71,14 +71,16 @@ def test_config2_cuts_bins_root_histogram_split(ctx, config2, config2_oracle):
     d.close()
 
 
-@pytest.mark.parametrize("quant_bits", [16])
-def test_config2_depth8_two_rounds_vs_oracle(ctx, config2, config2_oracle, quant_bits):
+@pytest.mark.parametrize("quant_bits,mode,ratio", [(16, 0, 1.0), (16, 2, 0.1)])
+def test_config2_depth8_two_rounds_vs_oracle(ctx, config2, config2_oracle, quant_bits, mode, ratio):
     """The benchmarked configuration itself (bench.py: 1M x 500, 256 bins, depth 8, f = 1,
     lambda 1, gamma 0, mcw 1, eta 0.1, the same CUDA graph and kernels), two consecutive boosting
     rounds with the margin updated in between (Eq. 1 via the partition, update_margin): every
     tree field, the histogram of every node of depth < 8 (built and derived), the leaf of every
     row and the updated margins are bit-exact against the oracle (Alg. 1; Eq. 8
-    P:L144-151; Eq. 6)."""
+    P:L144-151; Eq. 6).  Also with MVS f = 0.1 at full size (the in-core sampled path:
+    the selected-row list, Eq. 9 sampling R9, the build graph reused across rounds whose sample
+    sizes differ, predict by traversal)."""
     X, y = config2
     cv, cp, B = config2_oracle
     n, m = X.shape
@@ -89,11 +91,15 @@ def test_config2_depth8_two_rounds_vs_oracle(ctx, config2, config2_oracle, quant
         np.testing.assert_array_equal(gm, om, err_msg=f"margins before round {r}")
         g, h = oracle.logistic_grad(om, y)  # identical gradients on both sides
         d.set_gradients(g, h)
-        d.sample(ob.SAMPLE_NONE, 1.0, round=r, quant_bits=quant_bits)
+        info = d.sample(mode, ratio, 1.0, seed=3, round=r, quant_bits=quant_bits)
         t = d.build_tree(8, 1.0, 0.0, 1.0, 0.1, keep_debug=True)
-        qg, e_g = oracle.quantise(g.astype(np.float64), quant_bits)
-        qh, e_h = oracle.quantise(h.astype(np.float64), quant_bits)
-        on, lor, hist = oracle.build_tree(B, m, cv, cp, qg, qh, e_g, e_h, 8, 1.0, 0.0, 1.0, 0.1, want_hist=True)
+        s_ = oracle.sample(g, h, mode, ratio, 1.0, 3, r)
+        sel = s_["selected"].astype(bool)
+        assert info["n_selected_local"] == int(sel.sum())
+        qg, e_g = oracle.quantise(s_["gs"][sel], quant_bits)
+        qh, e_h = oracle.quantise(s_["hs"][sel], quant_bits)
+        on, lor, hist = oracle.build_tree(B[sel], m, cv, cp, qg, qh, e_g, e_h, 8, 1.0, 0.0, 1.0, 0.1,
+                                          want_hist=True)
         gn = t.export()
         for f in on.dtype.names:
             np.testing.assert_array_equal(gn[f], on[f], err_msg=f"round {r}: {f}")
@@ -102,9 +108,11 @@ def test_config2_depth8_two_rounds_vs_oracle(ctx, config2, config2_oracle, quant
             if on["feature"][v] == -2:
                 continue
             np.testing.assert_array_equal(t.get_histogram(v), hist[v], err_msg=f"round {r}: node {v}")
-        np.testing.assert_array_equal(t.get_partition(n), lor, err_msg=f"round {r}: leaf of row")
-        check_row_order(t.get_row_order(n), on, lor)
-        gm = d.update_margin(t, gm)
+        ns = int(sel.sum())
+        np.testing.assert_array_equal(t.get_partition(ns), lor, err_msg=f"round {r}: leaf of row")
+        check_row_order(t.get_row_order(ns), on, lor)
+        # every row gets the new tree (R18): from the partition at f = 1, by traversal otherwise
+        gm = d.update_margin(t, gm) if mode == 0 else d.predict([t], gm)
         om = oracle.predict(B, on, om)
         np.testing.assert_array_equal(gm, om, err_msg=f"round {r}: margins after the update")
         t.close()
