@@ -443,6 +443,13 @@ __device__ __forceinline__ long long warp_excl_scan_ll(long long v, int lane, lo
   return incl - v;
 }
 
+// 1 / x to <= 1 ulp with no denormal range handling (a denormal x flushes to 0 -> +inf).
+__device__ __forceinline__ float frcp_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // Exact Eq. 8 gain in double, the oracle's operation order (R14).
 __device__ __forceinline__ double gain_exact(long long GL, long long HL, long long G, long long H, double tP,
                                              double sg_inv, double sh_inv, double lambda, double gamma) {
@@ -492,10 +499,12 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
   // sh = 2^-e_h exact powers of two, tL + tR = c T with c = sg^2 / sh, lq = lambda / sh; the
   // pre-filter is on only while c and lq are normal floats, see k_init_build).  For one node the
   // gain 0.5 (c T - tP) - gamma is increasing in T, so the exact argmax (and every exact tie) has
-  // the largest exact T.  The float T carries <= ~8 2^-24 relative error (int -> float, squares, the
-  // lambda add, two __fdividef of <= 2 ulp, the sum) and the double evaluation of the gain
-  // rounds at ~2^-50 of c T + tP, so keeping every candidate with T_f >= (1 - 2^-18) max T_f
-  // keeps the true argmax and its ties with a >= 8x margin; only those are evaluated in double.
+  // the largest exact T.  With u = 2^-24, each float T carries <= 10 u relative error (int ->
+  // float u each, the square 3 u, the lambda add 2 u, rcp.approx.ftz <= 1 ulp = 2 u, the product
+  // u, the sum u) and the double evaluation of the gain rounds at ~2^-50 of c T + tP, so keeping
+  // every candidate with T_f >= (1 - 2^-18) max T_f (2^-18 = 64 u > 2 x 10 u) keeps the true
+  // argmax and its ties; only those are evaluated in double.  A denominator below FLT_MIN flushes
+  // to 0 in the ftz reciprocal -> T_f = inf or NaN -> "not finite" -> always evaluated exactly.
   const float lq = rp.fold_lq;
   // candidate key 2 b + dir: dir 0 = missing rows right (left sums = the prefix), dir 1 = missing
   // rows left (prefix + the missing bin's sums; MISS only, R27)
@@ -505,7 +514,7 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
   auto pre = [&](I GLx, I HLx, bool vb, float &u, int bit) {
     const bool v = vb && HLx >= hmin && HLx <= hmax;
     const float GLf = (float)GLx, HLf = (float)HLx, GRf = (float)(G - GLx), HRf = (float)(H - HLx);
-    const float T = __fdividef(GLf * GLf, HLf + lq) + __fdividef(GRf * GRf, HRf + lq);
+    const float T = GLf * GLf * frcp_ftz(HLf + lq) + GRf * GRf * frcp_ftz(HRf + lq);
     const bool fin = T < INFINITY;  // false for inf and NaN
     vmask |= v ? 1u << bit : 0u;
     u = v ? (fin ? T : INFINITY) : -INFINITY;
@@ -547,18 +556,22 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
       }
     }
   }
-  // warp argmax over (gain, key): larger gain, then lower key; invalid = -inf.  Only the pair is
+  // warp argmax over (gain, key): larger gain, then lower key; invalid = -inf.  Usually one lane
+  // holds every survivor of the pre-filter: its best is the warp's.  Otherwise only the pair is
   // shuffled; the lane that owns the winning key writes its own G_L, H_L.
   double bg = have ? best : -INFINITY;
   int bb = have ? bkey : 0x7fffffff;
+  const unsigned hv = __ballot_sync(0xffffffffu, have);
+  if (hv & (hv - 1)) {
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const double og = __shfl_xor_sync(0xffffffffu, bg, o);
-    const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
-    if (og > bg || (og == bg && ob < bb)) { bg = og; bb = ob; }
+    for (int o = 16; o; o >>= 1) {
+      const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+      if (og > bg || (og == bg && ob < bb)) { bg = og; bb = ob; }
+    }
   }
-  const bool any = bb != 0x7fffffff;
-  const int owner = any ? (bb >> 4) : 0;  // 16 keys (8 bins x 2 directions) per lane
+  const bool any = hv != 0;
+  const int owner = any ? ((hv & (hv - 1)) ? (bb >> 4) : __ffs(hv) - 1) : 0;  // 16 keys per lane
   if (lane == owner) {
     const int slot = node - level_first(A.d);
     Cand cd;
@@ -714,11 +727,17 @@ __global__ void __launch_bounds__(kEvalWarps * 32, kEvalBlocksWide) k_eval(EvalA
   __shared__ longlong2 tile[kEvalWarps][256 + 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n_items = A.ctl->n_ew * A.mf;
+  if (n_items <= 0) return;  // (also mf = 0: a rank with no features)
   const int nw = (int)(gridDim.x * blockDim.x) >> 5;
-  for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < n_items; t += nw) {
-    const int e = t / A.mf;
+  int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int e = t / A.mf, jj = t - e * A.mf;  // item t = (entry e, feature f0 + jj), advanced by nw
+  const int de = nw / A.mf, dj = nw - de * A.mf;
+  for (; t < n_items; t += nw) {
     const int2 en = A.ent[e];
-    eval_item_wide<HAS_MISSING>(A, en.x, en.y, A.f0 + t - e * A.mf, lane, tile[wib]);
+    eval_item_wide<HAS_MISSING>(A, en.x, en.y, A.f0 + jj, lane, tile[wib]);
+    e += de;
+    jj += dj;
+    if (jj >= A.mf) { jj -= A.mf; ++e; }
   }
 }
 
@@ -820,11 +839,17 @@ __global__ void __launch_bounds__(kEvalWarps * 32, OOCGB_EVAL_NARROW_MINB) k_eva
   __shared__ int2 tile2[kEvalWarps][256 + 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n_items = A.ctl->n_en * A.mf;
+  if (n_items <= 0) return;  // (also mf = 0: a rank with no features)
   const int nw = (int)(gridDim.x * blockDim.x) >> 5;
-  for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < n_items; t += nw) {
-    const int e = t / A.mf;
+  int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  int e = t / A.mf, jj = t - e * A.mf;  // item t = (entry e, feature f0 + jj), advanced by nw
+  const int de = nw / A.mf, dj = nw - de * A.mf;
+  for (; t < n_items; t += nw) {
     const int2 en = A.ent[A.ent_cap + e];
-    eval_item_narrow<HAS_MISSING>(A, en.x, en.y, A.f0 + t - e * A.mf, lane, tile2[wib]);
+    eval_item_narrow<HAS_MISSING>(A, en.x, en.y, A.f0 + jj, lane, tile2[wib]);
+    e += de;
+    jj += dj;
+    if (jj >= A.mf) { jj -= A.mf; ++e; }
   }
 }
 
