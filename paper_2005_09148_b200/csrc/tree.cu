@@ -356,6 +356,158 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// BuildHistograms at an identity level (the root of an in-core build: position = row, and the
+// gradient pairs in position order) with a bulk-asynchronous feed: the rows of an item are a
+// contiguous 32-B-per-row run of the group plane (and a contiguous run of q), so one thread
+// streams them into a shared-memory ring with cp.async.bulk (TMA engine, no per-thread load
+// instructions, no registers held by loads in flight) and the 16 warps only read shared memory
+// and issue the shared reductions.  Ring: kTmaStages stages of kTmaRows rows (one CTA step:
+// 16 warps x 16 rows); stage s is complete when its mbarrier full[s] has seen the bytes, and free
+// again when the 16 warps have arrived on empty[s].  Same accumulators, lane mapping, rotation
+// and flush as k_hist (identical partials).
+// Measured on B200 (config 2 root, r02): 219 us against k_hist's 181 us.  The kernel stays
+// L1-pipe bound (80% busy) and the bulk writes into shared memory take bank cycles from the
+// reductions (ncu: 41.1 M atomic wavefronts for 32 M ideal, 9.1 M of them bank conflicts; k_hist
+// has none), so it is built only with -DOOCGB_HIST_TMA=1 (tools/gpu_ab.sh) and off by default.
+#ifndef OOCGB_HIST_TMA
+#define OOCGB_HIST_TMA 0
+#endif
+#if OOCGB_HIST_TMA
+constexpr int kTmaRows = kHistThreads / 2;                 // rows per stage = rows per CTA step
+constexpr int kTmaStages = 4;
+constexpr int kTmaSymBytes = kTmaRows * 32;                 // 8 KB
+constexpr int kTmaQBytes = ((kTmaRows + 2) * 8 + 15) / 16 * 16;  // even-aligned q run (+ 1 row each end)
+constexpr int kTmaSmem = kHistSmem + kTmaStages * (kTmaSymBytes + kTmaQBytes) + 2 * kTmaStages * 8;
+
+__device__ __forceinline__ void mbar_init(uint32_t a, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, unsigned bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
+k_hist_tma(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int2 *__restrict__ q,
+           const Pair *__restrict__ pairs, LevelCtl *ctl, const int *__restrict__ chunk_pair,
+           int *__restrict__ partial) {
+  extern __shared__ int4 smem4[];
+  int *S = reinterpret_cast<int *>(smem4);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem4);
+  const uint32_t s_sym = sbase + kHistSmem;
+  const uint32_t s_q = s_sym + kTmaStages * kTmaSymBytes;
+  const uint32_t s_full = s_q + kTmaStages * kTmaQBytes, s_empty = s_full + 8 * kTmaStages;
+  const int n_items = ctl->n_items;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int half = lane & 1, rslot = lane >> 1;
+  const int wq = rslot >> 2, bq = (rslot & 3) * 8;
+  uint32_t f4[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) f4[s] = sbase + 4u * (uint32_t)(16 * half + ((rslot + s) & 15));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(s_full + 8 * s, 1);
+      mbar_init(s_empty + 8 * s, kHistThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // ring position: batches issued / consumed so far by this CTA (stage = n % S, phase = n / S)
+  unsigned n_issued = 0, n_used = 0;
+  __shared__ int s_next[2];
+  int par = 0;
+  for (int item = blockIdx.x; item < n_items; par ^= 1) {
+    if (threadIdx.x == 0) s_next[par] = (int)gridDim.x + atomicAdd(&ctl->hist_next, 1);
+    const int fg = item % n_fg, cg = item / n_fg;
+    const Pair P = pairs[chunk_pair[cg]];
+    const int c = cg - P.chunk_base;
+    const int r0 = P.begin + c * P.chunk_rows;
+    const int r1 = min(P.begin + P.count, r0 + P.chunk_rows);
+    const int nb = r1 > r0 ? (r1 - r0 + kTmaRows - 1) / kTmaRows : 0;
+    const uint8_t *plane = bins + (size_t)fg * pitch;
+    // producer: batch b of this item into the next ring slot (thread 0 only)
+    auto issue = [&](int b) {
+      const unsigned st = n_issued % kTmaStages;
+      if (n_issued >= kTmaStages) mbar_wait(s_empty + 8 * st, ((n_issued / kTmaStages) - 1) & 1);
+      const int rb = r0 + b * kTmaRows, re = min(r1, rb + kTmaRows);
+      const int qa = rb & ~1, qe = (re + 1) & ~1;
+      const unsigned sb = (unsigned)(re - rb) * 32u, qb = (unsigned)(qe - qa) * 8u;
+      mbar_expect_tx(s_full + 8 * st, sb + qb);
+      bulk_g2s(s_sym + st * kTmaSymBytes, plane + (size_t)rb * 32, sb, s_full + 8 * st);
+      bulk_g2s(s_q + st * kTmaQBytes, q + qa, qb, s_full + 8 * st);
+      ++n_issued;
+    };
+    int b_next = 0;  // next batch of this item to issue (thread 0's view)
+    if (threadIdx.x == 0)
+      for (; b_next < nb && b_next < kTmaStages; ++b_next) issue(b_next);
+    for (int i = threadIdx.x; i < 2 * kBins * kFG / 4; i += kHistThreads) smem4[i] = make_int4(0, 0, 0, 0);
+    __syncthreads();
+    for (int b = 0; b < nb; ++b) {
+      const unsigned st = n_used % kTmaStages;
+      mbar_wait(s_full + 8 * st, (n_used / kTmaStages) & 1);
+      const int rb = r0 + b * kTmaRows;
+      const int ib = warp * 16 + rslot;  // this lane's row in the batch
+      if (rb + ib < r1) {
+        uint4 x;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                     : "r"(s_sym + st * kTmaSymBytes + ib * 32 + half * 16));
+        int2 qq;
+        asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];"
+                     : "=r"(qq.x), "=r"(qq.y)
+                     : "r"(s_q + st * kTmaQBytes + (rb + ib - (rb & ~1)) * 8));
+        uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        uint32_t t[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[i] = (wq & 1) ? w[(i + 1) & 3] : w[i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = (wq & 2) ? t[(i + 2) & 3] : t[i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[i] = __funnelshift_r(w[i], w[(i + 1) & 3], bq);
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          const uint32_t a = __byte_perm(t[s >> 2], 0u, 0x4404u | ((uint32_t)(s & 3) << 4)) + f4[s];
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(qq.x));
+          asm volatile("red.shared.add.s32 [%0+128], %1;" ::"r"(a), "r"(qq.y));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty + 8 * st);
+      ++n_used;
+      if (threadIdx.x == 0 && b_next < nb) issue(b_next++);
+    }
+    __syncthreads();
+    const int f = fg * kFG + lane;
+    for (int bb = warp; bb < kBins / 32; bb += kHistThreads / 32) {
+      int4 *dst = reinterpret_cast<int4 *>(partial + (((size_t)item * kFG + lane) * kBins + bb * 32) * 2);
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const int i0 = (bb * 32 + i) * 64 + lane, i1 = i0 + 64;
+        const int4 v = make_int4(S[i0], S[i0 + 32], S[i1], S[i1 + 32]);
+        if (f < m) dst[i >> 1] = v;
+      }
+    }
+    __syncthreads();
+    item = s_next[par];
+  }
+}
+#endif  // OOCGB_HIST_TMA
+
 // Multi-GPU: sum a pair's s32 chunk partials into int64 histograms that are then reduce-scattered
 // over the ranks ("summed across all GPUs"; each rank receives the sums of its feature
 // slice and evaluates only those features).  Thread per (pair, feature, bin).
@@ -853,6 +1005,232 @@ __global__ void __launch_bounds__(kEvalWarps * 32, OOCGB_EVAL_NARROW_MINB) k_eva
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// General list (nodes with > kmax rows, and every node of a streamed level): these items are few
+// (config 2: the root's m, then the one or two large nodes of a level) and each is a latency
+// chain (chunk sums, int64 scans, exact double gains), so one 128-thread block works on one
+// (pair, feature j, side) item: thread t owns the consecutive bins 2t, 2t + 1 (coalesced 16-B
+// partial loads and 32-B int64 loads/stores, no transpose), block scans in int64, the same float
+// pre-filter and exact double pass as eval_node_impl, and a block argmax with the same order
+// (larger gain, then lower key 2 b + dir).  The results are those of the warp version: every
+// sum is the same exact integer, every float and double operation the same.
+// Measured (config 2, cold-cache launch list): root 19.9 -> 12.5 us, level 1 15.4 -> 14.9 us, but
+// slower where a level has several large nodes (level 5: 14.8 -> 20.5 us: a block per item has
+// less throughput than four warps on four items), so it runs where every item gets its own
+// block: levels whose general list fits one wave (the root; OOCGB_EVAL_WIDE_BLOCK=0: never).
+#ifndef OOCGB_EVAL_WIDE_BLOCK
+#define OOCGB_EVAL_WIDE_BLOCK 1
+#endif
+constexpr int kBlkThreads = 128, kBlkPerSm = 4, kBlkChunkUnroll = 4;
+struct BlkShared {
+  long long wg[kBlkThreads / 32], wh[kBlkThreads / 32];  // warp totals for the block scan
+  float wT[kBlkThreads / 32];                            // warp max of T_f
+  double bg[kBlkThreads / 32];                           // warp best (gain, key)
+  int bk[kBlkThreads / 32];
+  long long Gm, Hm;                                      // the missing bin's sums (R27)
+  int win;                                               // the block's winning key
+};
+
+__device__ __forceinline__ long long warp_incl_scan_ll(long long v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+template <bool HAS_MISSING>
+__device__ __forceinline__ void eval_item_blk(const EvalArgs &A, int p, int side, int j, BlkShared &S) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const Pair P = A.pairs[p];
+  const int node = side ? P.derived : P.built;
+  if (node < 0) return;                                // uniform over the block
+  if (A.streamed && A.dn[node].feature == -2) return;  // streamed levels list every slot
+  const long long G = A.dn[node].Gq, H = A.dn[node].Hq;
+  const double tP = A.dn[node].tP;
+  const size_t hsz = (size_t)A.hm * kBins * 2;
+  const int jl = j - A.f0;
+  const size_t dsz = (size_t)A.m * kBins * 2;
+  long long g[2], h[2];
+  long long pg[2] = {0, 0}, ph[2] = {0, 0};
+  if (side) {  // parent first so its loads overlap the chunk loads
+    const int ps = P.parent - level_first(A.d - 1);
+    if (P.compact & 1) {
+      const int4 v = __ldg(reinterpret_cast<const int4 *>(A.phist_prev + (size_t)ps * hsz) + (size_t)jl * (kBins / 2) + tid);
+      pg[0] = v.x; ph[0] = v.y; pg[1] = v.z; ph[1] = v.w;
+    } else {
+      const longlong2 *src = reinterpret_cast<const longlong2 *>(A.phist_prev + (size_t)ps * hsz + (size_t)jl * kBins * 2) + 2 * tid;
+      const longlong2 a = __ldg(src), b = __ldg(src + 1);
+      pg[0] = a.x; ph[0] = a.y; pg[1] = b.x; ph[1] = b.y;
+    }
+  }
+  if (A.built64) {
+    const longlong2 *src = reinterpret_cast<const longlong2 *>(A.built64 + (size_t)p * hsz + (size_t)jl * kBins * 2) + 2 * tid;
+    const longlong2 a = src[0], b = src[1];
+    g[0] = a.x; h[0] = a.y; g[1] = b.x; h[1] = b.y;
+  } else {
+    g[0] = g[1] = h[0] = h[1] = 0;
+    const size_t cstride = (size_t)A.n_fg * kFG * kBins / 2;  // int4 (= 2 bins) between chunks
+    const int4 *src0 = reinterpret_cast<const int4 *>(A.partial) +
+                       (((size_t)P.chunk_base * A.n_fg + j / kFG) * kFG + (j % kFG)) * (kBins / 2) + tid;
+    int c = 0;
+    for (; c + kBlkChunkUnroll <= P.n_chunks; c += kBlkChunkUnroll) {
+      int4 v[kBlkChunkUnroll];
+#pragma unroll
+      for (int u = 0; u < kBlkChunkUnroll; ++u) v[u] = __ldg(src0 + (c + u) * cstride);
+#pragma unroll
+      for (int u = 0; u < kBlkChunkUnroll; ++u) { g[0] += v[u].x; h[0] += v[u].y; g[1] += v[u].z; h[1] += v[u].w; }
+    }
+    for (; c < P.n_chunks; ++c) {
+      const int4 v = __ldg(src0 + c * cstride);
+      g[0] += v.x; h[0] += v.y; g[1] += v.z; h[1] += v.w;
+    }
+  }
+  if (side) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) { g[i] = pg[i] - g[i]; h[i] = ph[i] - h[i]; }
+  }
+  const int f_d = level_first(A.d);
+  if (A.d <= A.D - 2 && !A.streamed) {
+    if (P.compact & (side ? 4 : 2)) {
+      int4 *dst = reinterpret_cast<int4 *>(A.phist_next + (size_t)(node - f_d) * hsz) + (size_t)jl * (kBins / 2) + tid;
+      *dst = make_int4((int)g[0], (int)h[0], (int)g[1], (int)h[1]);
+    } else {
+      longlong2 *dst = reinterpret_cast<longlong2 *>(A.phist_next + (size_t)(node - f_d) * hsz + (size_t)jl * kBins * 2) + 2 * tid;
+      dst[0] = make_longlong2(g[0], h[0]);
+      dst[1] = make_longlong2(g[1], h[1]);
+    }
+  }
+  if (A.dbg) {
+    longlong2 *dst = reinterpret_cast<longlong2 *>(A.dbg + (size_t)node * dsz + (size_t)j * kBins * 2) + 2 * tid;
+    dst[0] = make_longlong2(g[0], h[0]);
+    dst[1] = make_longlong2(g[1], h[1]);
+  }
+  // block exclusive scan of the thread's (g, h) pair sums
+  const long long ig = warp_incl_scan_ll(g[0] + g[1], lane), ih = warp_incl_scan_ll(h[0] + h[1], lane);
+  if (lane == 31) { S.wg[w] = ig; S.wh[w] = ih; }
+  if (HAS_MISSING && tid == kBlkThreads - 1) { S.Gm = g[1]; S.Hm = h[1]; }  // bin 255
+  __syncthreads();
+  long long eg = ig - (g[0] + g[1]), eh = ih - (h[0] + h[1]);
+#pragma unroll
+  for (int u = 0; u < kBlkThreads / 32; ++u)
+    if (u < w) { eg += S.wg[u]; eh += S.wh[u]; }
+  long long Gm = 0, Hm = 0;
+  if (HAS_MISSING) { Gm = S.Gm; Hm = S.Hm; }
+  const bool miss = HAS_MISSING && (Gm != 0 || Hm != 0);  // uniform over the block
+  const RoundParams &rp = *A.rp;
+  const int B = A.cut_ptrs[j + 1] - A.cut_ptrs[j];
+  const long long hmin = rp.h_min, hmax = H - rp.h_min;
+  const float lq = rp.fold_lq;
+  // pass 1: float T of the thread's candidates (see eval_node_impl for the bound and the rules)
+  float tv[2][2];
+  unsigned vmask = 0;
+  float Tmax = -INFINITY;
+  long long GL = eg, HL = eh;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    GL += g[i];
+    HL += h[i];
+    const int b = 2 * tid + i;
+    const bool vb = b <= B - 2 && ((g[i] | h[i]) != 0 || b == 0);
+#pragma unroll
+    for (int dir = 0; dir < 2; ++dir) {
+      if (dir == 1 && !miss) { tv[i][1] = -INFINITY; continue; }
+      const long long GLx = dir ? GL + Gm : GL, HLx = dir ? HL + Hm : HL;
+      const bool v = vb && HLx >= hmin && HLx <= hmax;
+      const float GLf = (float)GLx, HLf = (float)HLx, GRf = (float)(G - GLx), HRf = (float)(H - HLx);
+      const float T = GLf * GLf * frcp_ftz(HLf + lq) + GRf * GRf * frcp_ftz(HRf + lq);
+      const bool fin = T < INFINITY;
+      vmask |= v ? 1u << (2 * i + dir) : 0u;
+      tv[i][dir] = v ? (fin ? T : INFINITY) : -INFINITY;
+      Tmax = fmaxf(Tmax, (v && fin) ? T : -INFINITY);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) Tmax = fmaxf(Tmax, __shfl_xor_sync(0xffffffffu, Tmax, o));
+  if (lane == 0) S.wT[w] = Tmax;
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kBlkThreads / 32; ++u) Tmax = fmaxf(Tmax, S.wT[u]);
+  const float thr = rp.prefilter ? Tmax * (1.0f - 0x1p-18f) : -INFINITY;
+  // pass 2: exact double gains of the survivors, in key order
+  double best = 0.0;
+  int bkey = 0x7fffffff, have = 0;
+  long long bGL = 0, bHL = 0;
+  GL = eg;
+  HL = eh;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    GL += g[i];
+    HL += h[i];
+#pragma unroll
+    for (int dir = 0; dir < 2; ++dir) {
+      if (((vmask >> (2 * i + dir)) & 1u) && tv[i][dir] >= thr) {
+        const long long GLx = dir ? GL + Gm : GL, HLx = dir ? HL + Hm : HL;
+        const double gain = gain_exact(GLx, HLx, G, H, tP, rp.sg_inv, rp.sh_inv, A.lambda, A.gamma);
+        if (!have || gain > best) {
+          have = 1; best = gain; bkey = 2 * (2 * tid + i) + dir; bGL = GLx; bHL = HLx;
+        }
+      }
+    }
+  }
+  // block argmax over (gain, key): warp shuffles only where a warp has more than one survivor
+  double bg = have ? best : -INFINITY;
+  int bb = have ? bkey : 0x7fffffff;
+  const unsigned hv = __ballot_sync(0xffffffffu, have);
+  if (hv & (hv - 1)) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+      if (og > bg || (og == bg && ob < bb)) { bg = og; bb = ob; }
+    }
+  } else if (hv) {
+    const int src = __ffs(hv) - 1;
+    bg = __shfl_sync(0xffffffffu, bg, src);
+    bb = __shfl_sync(0xffffffffu, bb, src);
+  }
+  if (lane == 0) { S.bg[w] = bg; S.bk[w] = bb; }
+  __syncthreads();
+  double wg = S.bg[0];
+  int wk = S.bk[0];
+#pragma unroll
+  for (int u = 1; u < kBlkThreads / 32; ++u)
+    if (S.bg[u] > wg || (S.bg[u] == wg && S.bk[u] < wk)) { wg = S.bg[u]; wk = S.bk[u]; }
+  const bool any = wk != 0x7fffffff;
+  const int owner = any ? (wk >> 2) : 0;  // 4 keys (2 bins x 2 directions) per thread
+  if (tid == owner) {
+    const int slot = node - level_first(A.d);
+    Cand cd;
+    cd.gain = any ? wg : 0.0;
+    cd.bin = wk;
+    cd.valid = any ? 1 : 0;
+    cd.GL = any ? bGL : 0;
+    cd.HL = any ? bHL : 0;
+    A.cand[cand_index(A.msl, A.max_slots, slot, j)] = cd;
+  }
+  __syncthreads();  // the shared block is reused by the next item
+}
+
+// Persistent blocks over the general list: item t = (entry t / mf, feature t mod mf).
+template <bool HAS_MISSING>
+__global__ void __launch_bounds__(kBlkThreads, kBlkPerSm) k_eval_blk(EvalArgs A) {
+  __shared__ BlkShared S;
+  const int n_items = A.ctl->n_ew * A.mf;
+  if (n_items <= 0) return;
+  int t = blockIdx.x;
+  int e = t / A.mf, jj = t - e * A.mf;
+  const int de = (int)gridDim.x / A.mf, dj = (int)gridDim.x - de * A.mf;
+  for (; t < n_items; t += gridDim.x) {
+    const int2 en = A.ent[e];
+    eval_item_blk<HAS_MISSING>(A, en.x, en.y, A.f0 + jj, S);
+    e += de;
+    jj += dj;
+    if (jj >= A.mf) { jj -= A.mf; ++e; }
+  }
+}
+
 // Split decision per node at depth d: argmax over features (ties: lowest feature, R13),
 // split iff gain > 0; children get their exact sums and Eq. 6 leaf values.  One 256-thread
 // block per node (blockIdx.x = 2 pair + side).
@@ -928,7 +1306,18 @@ static void launch_eval(const EvalArgs &A, int max_pairs, oocgb_ctx c, cudaStrea
   const int64_t blocks = ((int64_t)max_pairs * std::max(1, A.mf) * 2 + kEvalWarps - 1) / kEvalWarps;
   const unsigned gw = (unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * kEvalBlocksWide);
   const unsigned gn = (unsigned)std::min<int64_t>(blocks, (int64_t)num_sms * OOCGB_EVAL_NARROW_MINB);
-  if (A.has_missing) {  // R27: candidates in both default directions
+  // the general list fits one wave of blocks (the root level: one built node, no sibling)
+  const bool blk = OOCGB_EVAL_WIDE_BLOCK && !A.streamed && A.d == 0 && A.mf <= num_sms * kBlkPerSm;
+  if (blk) {
+    const unsigned gb = (unsigned)std::max(1, A.mf);
+    if (A.has_missing) {  // R27: candidates in both default directions
+      k_eval_blk<true><<<gb, kBlkThreads, 0, st>>>(A);
+      k_eval_narrow<true><<<gn, kEvalWarps * 32, 0, st>>>(A);
+    } else {
+      k_eval_blk<false><<<gb, kBlkThreads, 0, st>>>(A);
+      k_eval_narrow<false><<<gn, kEvalWarps * 32, 0, st>>>(A);
+    }
+  } else if (A.has_missing) {  // R27: candidates in both default directions
     k_eval<true><<<gw, kEvalWarps * 32, 0, st>>>(A);
     k_eval_narrow<true><<<gn, kEvalWarps * 32, 0, st>>>(A);
   } else {
@@ -1570,7 +1959,7 @@ static void ensure_work(oocgb_data d, int D) {
   const int64_t max_segs = 1LL << std::max(D, 1);
   for (int i = 0; i < 2; ++i) {
     w->ridx[i] = (int32_t *)dmalloc(sizeof(int32_t) * n);
-    w->q[i] = (int2 *)dmalloc(sizeof(int2) * n);
+    w->q[i] = (int2 *)dmalloc(sizeof(int2) * (n + 2));  // k_hist_tma reads q in even-aligned runs
     w->segs[i] = (Seg *)dmalloc(sizeof(Seg) * max_segs);
   }
   for (int i = 0; i < 2; ++i) w->seg_cur[i] = (int *)dmalloc(sizeof(int) * 2 * max_segs);
@@ -1600,6 +1989,9 @@ static void ensure_work(oocgb_data d, int D) {
   OOCGB_CK(cudaMallocHost(&w->h_ctl, sizeof(LevelCtl)));
   OOCGB_CK(cudaMallocHost(&w->h_pn, sizeof(PNode) * ((1LL << (D + 1)) - 1)));
   OOCGB_CK(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem));
+#if OOCGB_HIST_TMA
+  OOCGB_CK(cudaFuncSetAttribute(k_hist_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+#endif
 }
 
 static void drop_graph(Work *w);
@@ -1663,10 +2055,16 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   for (int lv = 0; lv < D; ++lv) {
     const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
     mark(0, true);
-    k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur], w->q[cur],
-                                                                 w->pairs, w->ctl, w->chunk_pair, w->partial,
-                                                                 (lv == 0 && ridx_mode == 0) ? 1 : 0, d->gw,
-                                                                 d->gw == 64 ? 1 : 0);
+#if OOCGB_HIST_TMA
+    if (lv == 0 && ridx_mode == 0 && d->gw == 32)  // identity level: bulk feed
+      k_hist_tma<<<w->hist_grid, kHistThreads, kTmaSmem, c->stream>>>(bins, pitch, m, n_fg, w->q[cur], w->pairs,
+                                                                      w->ctl, w->chunk_pair, w->partial);
+    else
+#endif
+      k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur], w->q[cur],
+                                                                   w->pairs, w->ctl, w->chunk_pair, w->partial,
+                                                                   (lv == 0 && ridx_mode == 0) ? 1 : 0, d->gw,
+                                                                   d->gw == 64 ? 1 : 0);
     OOCGB_CK(cudaGetLastError());
     mark(0, false);
     if (c->coll) {  // every rank receives the global sums of its feature slice
