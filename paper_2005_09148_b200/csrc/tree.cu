@@ -564,12 +564,18 @@ struct EvalArgs {
   // feature slice (world > 1: this rank evaluates features [f0, f0 + mf) from reduce-scattered
   // histograms whose rows hold hm = msl features; world == 1: f0 = 0, mf = hm = msl = m)
   int f0, mf, hm, msl, max_slots;
+  int crank;  // candidate block of this rank's slice: f0 / msl
 };
 
 // candidates [owner rank][slot][msl]: rank r writes features [r msl, (r + 1) msl) into block r,
 // the blocks are all-gathered, and every rank's k_finalize reads all m features
 __host__ __device__ __forceinline__ size_t cand_index(int msl, int max_slots, int slot, int j) {
   const int r = j / msl;
+  return ((size_t)r * max_slots + slot) * msl + (j - r * msl);
+}
+// the same for a feature of this rank's slice (j in [r msl, (r + 1) msl), r = the slice's owner):
+// no integer division on the evaluation's per-item path
+__device__ __forceinline__ size_t cand_index_own(int msl, int max_slots, int r, int slot, int j) {
   return ((size_t)r * max_slots + slot) * msl + (j - r * msl);
 }
 
@@ -660,17 +666,18 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
   const float lq = rp.fold_lq;
   // candidate key 2 b + dir: dir 0 = missing rows right (left sums = the prefix), dir 1 = missing
   // rows left (prefix + the missing bin's sums; MISS only, R27)
-  float tv[MISS ? 2 : 1][8];  // T_f; -inf invalid; +inf not finite (always re-evaluated)
-  unsigned vmask = 0;  // bit 2 i + dir
+  // tv: T_f of a valid candidate (+inf when not finite: always re-evaluated), NaN when invalid
+  // (fails every >= test).  Tmax = fmaxf over the valid T_f (fmaxf ignores NaN); a valid +inf
+  // makes Tmax = +inf, and then every valid candidate is evaluated exactly (thr = -inf below): a
+  // superset of the survivors, so the same argmax.
+  float tv[MISS ? 2 : 1][8];
   float Tmax = -INFINITY;
-  auto pre = [&](I GLx, I HLx, bool vb, float &u, int bit) {
+  auto pre = [&](I GLx, I HLx, bool vb, float &u, int) {
     const bool v = vb && HLx >= hmin && HLx <= hmax;
     const float GLf = (float)GLx, HLf = (float)HLx, GRf = (float)(G - GLx), HRf = (float)(H - HLx);
     const float T = GLf * GLf * frcp_ftz(HLf + lq) + GRf * GRf * frcp_ftz(HRf + lq);
-    const bool fin = T < INFINITY;  // false for inf and NaN
-    vmask |= v ? 1u << bit : 0u;
-    u = v ? (fin ? T : INFINITY) : -INFINITY;
-    Tmax = fmaxf(Tmax, (v && fin) ? T : -INFINITY);
+    u = v ? (T < INFINITY ? T : INFINITY) : __int_as_float(0x7fc00000);
+    Tmax = fmaxf(Tmax, v ? T : -INFINITY);
   };
   // pass 1: float T of every candidate
   I GL = eg, HL = eh;
@@ -686,7 +693,7 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) Tmax = fmaxf(Tmax, __shfl_xor_sync(0xffffffffu, Tmax, o));
-  const float thr = rp.prefilter ? Tmax * (1.0f - 0x1p-18f) : -INFINITY;
+  const float thr = (rp.prefilter && Tmax < INFINITY) ? Tmax * (1.0f - 0x1p-18f) : -INFINITY;
   // pass 2: exact double gains of the survivors, in key order (strict > keeps the lower key)
   double best = 0.0;
   int bkey = 0x7fffffff, have = 0;
@@ -699,7 +706,7 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
     HL += h[i];
 #pragma unroll
     for (int dir = 0; dir < (MISS ? 2 : 1); ++dir) {
-      if (((vmask >> (2 * i + dir)) & 1u) && tv[dir][i] >= thr) {
+      if (tv[dir][i] >= thr) {  // NaN (invalid) fails
         const I GLx = dir ? GL + Gm : GL, HLx = dir ? HL + Hm : HL;
         const double gain = gain_exact(GLx, HLx, G, H, tP, rp.sg_inv, rp.sh_inv, A.lambda, A.gamma);
         if (!have || gain > best) {
@@ -732,7 +739,7 @@ __device__ int eval_node_impl(const EvalArgs &A, int node, int j, int lane, cons
     cd.valid = any ? 1 : 0;
     cd.GL = any ? bGL : 0;
     cd.HL = any ? bHL : 0;
-    A.cand[cand_index(A.msl, A.max_slots, slot, j)] = cd;
+    A.cand[cand_index_own(A.msl, A.max_slots, A.crank, slot, j)] = cd;
   }
   return owner;
 }
@@ -1208,7 +1215,7 @@ __device__ __forceinline__ void eval_item_blk(const EvalArgs &A, int p, int side
     cd.valid = any ? 1 : 0;
     cd.GL = any ? bGL : 0;
     cd.HL = any ? bHL : 0;
-    A.cand[cand_index(A.msl, A.max_slots, slot, j)] = cd;
+    A.cand[cand_index_own(A.msl, A.max_slots, A.crank, slot, j)] = cd;
   }
   __syncthreads();  // the shared block is reused by the next item
 }
@@ -2088,6 +2095,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.msl = w->msl; A.max_slots = 2 * max_pairs; A.hm = w->msl;  // candidate blocks sized for this level
     A.f0 = c->coll ? std::min(m, c->rank * w->msl) : 0;
     A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
+    A.crank = c->coll ? c->rank : 0;
     launch_eval(A, max_pairs, c, c->stream);
     mark(1, false);
     mark(2, true);
@@ -2471,6 +2479,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     A.msl = w->msl; A.max_slots = n_slots; A.hm = w->msl;
     A.f0 = c->coll ? std::min(m, c->rank * w->msl) : 0;
     A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
+    A.crank = c->coll ? c->rank : 0;
     launch_eval(A, n_slots, c, c->stream);
   }
   // export (same as the in-core path)
