@@ -497,20 +497,39 @@ __global__ void k_select_scatter(SelParams P0, const MvsDev *mv, const long long
   if (lane == 0) { atomic_max_abs(&maxbits[0], mg); atomic_max_abs(&maxbits[1], mh); }
 }
 
-// max |g|, |h| over all rows (NONE mode)
-__global__ void k_absmax2(const float *__restrict__ g, const float *__restrict__ h, int64_t n,
-                          unsigned long long *maxbits) {
-  double mg = 0.0, mh = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    mg = fmax(mg, fabs((double)g[i]));
-    mh = fmax(mh, fabs((double)h[i]));
+// max |g|, |h| over all rows (NONE mode): 16-B loads (4 rows per thread and step), the maxima
+// reduced per block and one 64-bit atomic max per block and value (r01: one per warp, ~9.5k
+// same-address atomics serialised at L2).  |x| maxima in float are exact; the bits are those
+// of the same value as a double.
+__device__ __forceinline__ float block_max_f(float v, float *s_w) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) s_w[w] = v;
+  __syncthreads();
+  v = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0.0f;
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  return v;
+}
+__global__ void __launch_bounds__(256) k_absmax2(const float *__restrict__ g, const float *__restrict__ h, int64_t n,
+                                                 unsigned long long *maxbits) {
+  __shared__ float s_w[32];
+  float mg = 0.0f, mh = 0.0f;
+  const int64_t n4 = n >> 2;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  const float4 *g4 = reinterpret_cast<const float4 *>(g), *h4 = reinterpret_cast<const float4 *>(h);
+  for (int64_t i = tid; i < n4; i += nth) {
+    const float4 a = __ldg(g4 + i), b = __ldg(h4 + i);
+    mg = fmaxf(mg, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+    mh = fmaxf(mh, fmaxf(fmaxf(fabsf(b.x), fabsf(b.y)), fmaxf(fabsf(b.z), fabsf(b.w))));
   }
-  for (int o = 16; o; o >>= 1) {
-    mg = fmax(mg, __shfl_down_sync(0xffffffffu, mg, o));
-    mh = fmax(mh, __shfl_down_sync(0xffffffffu, mh, o));
+  for (int64_t i = 4 * n4 + tid; i < n; i += nth) {
+    mg = fmaxf(mg, fabsf(g[i]));
+    mh = fmaxf(mh, fabsf(h[i]));
   }
-  if ((threadIdx.x & 31) == 0) { atomic_max_abs(&maxbits[0], mg); atomic_max_abs(&maxbits[1], mh); }
+  mg = block_max_f(mg, s_w);
+  mh = block_max_f(mh, s_w);
+  if (threadIdx.x == 0) { atomic_max_abs(&maxbits[0], (double)mg); atomic_max_abs(&maxbits[1], (double)mh); }
 }
 
 // e = P - k with frexp(max |x|) = (., k); 0 when max = 0 (R12).  Device copy of the host rule.
@@ -538,9 +557,22 @@ __global__ void k_sstate_globalise(SampleState *ss) {
 
 // q = rint(x 2^e) (half to even), plus exact int64 sums for the root node; the exponents come
 // from the (all-reduced) maxima in the sample state, the row count from the selection scan.
+// 4 rows per thread and step (16-B loads of float rows, 2 x 16-B stores of q), the sums reduced
+// per block with one 64-bit atomic per block and value (r01: one per warp).
+__device__ __forceinline__ long long block_sum_ll(long long v, long long *s_w) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) s_w[w] = v;
+  __syncthreads();
+  v = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  return v;
+}
 template <typename T>
-__global__ void k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, SampleState *ss,
-                           int2 *__restrict__ q) {
+__global__ void __launch_bounds__(256) k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, SampleState *ss,
+                                                  int2 *__restrict__ q) {
+  __shared__ long long s_w[32];
   const int eg = quant_exponent(ss->maxbits[0], ss->quant_bits);
   const int eh = quant_exponent(ss->maxbits[1], ss->quant_bits);
   if (blockIdx.x == 0 && threadIdx.x == 0) { ss->e_g = eg; ss->e_h = eh; }
@@ -548,19 +580,31 @@ __global__ void k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, S
   const int64_t n = ss->n_sel_local;
   long long *sums = &ss->G;
   long long G = 0, H = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int qg = (int)__double2ll_rn(__dmul_rn((double)gs[i], sg));
-    int qh = (int)__double2ll_rn(__dmul_rn((double)hs[i], sh));
-    q[i] = make_int2(qg, qh);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  auto one = [&](T x, T y) -> int2 {
+    const int qg = (int)__double2ll_rn(__dmul_rn((double)x, sg));
+    const int qh = (int)__double2ll_rn(__dmul_rn((double)y, sh));
     G += qg;
     H += qh;
+    return make_int2(qg, qh);
+  };
+  int64_t i0 = 0;
+  if constexpr (sizeof(T) == 4) {  // float rows: vectorised
+    const int64_t n4 = n >> 2;
+    const float4 *g4 = reinterpret_cast<const float4 *>(gs), *h4 = reinterpret_cast<const float4 *>(hs);
+    int4 *q4 = reinterpret_cast<int4 *>(q);
+    for (int64_t i = tid; i < n4; i += nth) {
+      const float4 a = __ldg(g4 + i), b = __ldg(h4 + i);
+      const int2 r0 = one(a.x, b.x), r1 = one(a.y, b.y), r2 = one(a.z, b.z), r3 = one(a.w, b.w);
+      q4[2 * i] = make_int4(r0.x, r0.y, r1.x, r1.y);
+      q4[2 * i + 1] = make_int4(r2.x, r2.y, r3.x, r3.y);
+    }
+    i0 = 4 * n4;
   }
-  for (int o = 16; o; o >>= 1) {
-    G += __shfl_down_sync(0xffffffffu, G, o);
-    H += __shfl_down_sync(0xffffffffu, H, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
+  for (int64_t i = i0 + tid; i < n; i += nth) q[i] = one(gs[i], hs[i]);
+  G = block_sum_ll(G, s_w);
+  H = block_sum_ll(H, s_w);
+  if (threadIdx.x == 0) {
     atomicAdd((unsigned long long *)&sums[0], (unsigned long long)G);
     atomicAdd((unsigned long long *)&sums[1], (unsigned long long)H);
   }
@@ -591,8 +635,8 @@ __global__ void k_rows_to_tiled(const uint8_t *__restrict__ src, int stride, int
 }
 
 // ---------------------------------------------------------------------------------------------
-static int grid_for(oocgb_ctx c, int64_t n, int threads = 256) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)c->num_sms * 8));
+static int grid_for(oocgb_ctx c, int64_t n, int threads = 256, int per_sm = 8) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)c->num_sms * per_sm));
 }
 
 static int ceil_log2(int64_t n) {
@@ -743,7 +787,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
     d->all_selected = true;
     d->n_sel = n;
     k_sstate_init<<<1, 1, 0, c->stream>>>(ss, n, quant_bits);
-    if (n > 0) k_absmax2<<<grid_for(c, n), 256, 0, c->stream>>>(d->d_g, d->d_h, n, ss->maxbits);
+    if (n > 0) k_absmax2<<<grid_for(c, (n + 3) / 4, 256, 2), 256, 0, c->stream>>>(d->d_g, d->d_h, n, ss->maxbits);
   } else {
     d->all_selected = false;
     need_sync = true;  // the host needs n_sel (grids, graph key, compaction)
@@ -786,7 +830,7 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
   allreduce_max_u64(c, ss->maxbits, 2);
   k_sstate_globalise<<<1, 1, 0, c->stream>>>(ss);
   allreduce_sum_i64(c, &ss->n_sel_global, 1);
-  const int qgrid = grid_for(c, std::max<int64_t>(1, d->n_sel));
+  const int qgrid = grid_for(c, std::max<int64_t>(1, (d->n_sel + 3) / 4), 256, 2);
   if (d->all_selected)
     k_quantise<float><<<qgrid, 256, 0, c->stream>>>(d->d_g, d->d_h, ss, d->d_q);
   else
