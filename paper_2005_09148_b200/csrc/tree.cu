@@ -157,10 +157,14 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
     nd.feature = -2;
     dn[v] = nd;
   }
-  for (int i = tid; i < n_sel; i += nth) {
-    ridx[i] = (ridx_mode == 1) ? sel_rows[i] : i;  // 1: in-core sampled (bins of the full page)
-    q_out[i] = q_in[i];
-  }
+  // the level loop reads the sample's own buffers at level 0 (identity rows / the selected rows,
+  // the sample's q) and the partition writes buffer 1 first; only a depth-0 build (no level)
+  // needs buffer 0 filled for its exports
+  if (max_depth == 0)
+    for (int i = tid; i < n_sel; i += nth) {
+      ridx[i] = (ridx_mode == 1) ? sel_rows[i] : i;  // 1: in-core sampled (bins of the full page)
+      q_out[i] = q_in[i];
+    }
   if (tid == 0) {
     RoundParams P;
     P.G = ss->G;
@@ -1481,7 +1485,7 @@ k_part_fused(const long long *__restrict__ n_dev, const Seg *__restrict__ segs, 
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int p = t0 + u * kPartThreads + threadIdx.x;
-    if (p < t1) { rows[u] = ridx[p]; qs[u] = q[p]; }
+    if (p < t1) { rows[u] = ridx ? ridx[p] : p; qs[u] = q[p]; }  // ridx null: identity (level 0)
   }
   load_tile_segs(T, segs, n_segs, dn, tile_seg, blockIdx.x, n_tiles);
   const bool staged = T.count <= kTileSegs;
@@ -1913,13 +1917,23 @@ __global__ void k_predict(const uint8_t *__restrict__ bins, size_t row_step, siz
 }
 
 // margin[row] += leaf of the row's final segment (in-core, all rows selected).
+// margin[row] += leaf value of the row's final segment (Eq. 1).  The segment comes from the last
+// plan's tile -> segment table (the segment holding the tile's first position) and a short
+// forward scan, instead of a binary search over every segment per position.
 __global__ void k_update_margin(int n, const Seg *__restrict__ segs, const LevelCtl *__restrict__ ctl,
                                 const DNode *__restrict__ dn, const int32_t *__restrict__ ridx,
-                                float *__restrict__ margin) {
+                                const int *__restrict__ tile_seg, float *__restrict__ margin) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int s = seg_of(segs, ctl->n_segs, i);
-  margin[ridx[i]] = margin[ridx[i]] + dn[segs[s].node].leaf_value;
+  int s;
+  if (tile_seg) {
+    s = tile_seg[i / kPartTile];
+    while (segs[s].begin + segs[s].count <= i) ++s;
+  } else {
+    s = seg_of(segs, ctl->n_segs, i);
+  }
+  const int r = ridx[i];
+  margin[r] = margin[r] + dn[segs[s].node].leaf_value;
 }
 
 __global__ void k_leaf_of_pos(int n, const Seg *__restrict__ segs, int n_segs, const int32_t *__restrict__ ridx,
@@ -2061,14 +2075,18 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   if (tiles > 0) OOCGB_CK(cudaMemsetAsync(w->tile_seg, 0, sizeof(int) * tiles, c->stream));  // one root segment
   for (int lv = 0; lv < D; ++lv) {
     const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
+    // this level's positions: level 0 reads the sample's buffers directly (identity rows or the
+    // selected rows, the sample's q), later levels the previous partition's output
+    const int32_t *lv_ridx = lv > 0 ? w->ridx[cur] : (ridx_mode == 1 ? d->d_sel_rows : nullptr);
+    const int2 *lv_q = lv > 0 ? w->q[cur] : d->d_q;
     mark(0, true);
 #if OOCGB_HIST_TMA
     if (lv == 0 && ridx_mode == 0 && d->gw == 32)  // identity level: bulk feed
-      k_hist_tma<<<w->hist_grid, kHistThreads, kTmaSmem, c->stream>>>(bins, pitch, m, n_fg, w->q[cur], w->pairs,
+      k_hist_tma<<<w->hist_grid, kHistThreads, kTmaSmem, c->stream>>>(bins, pitch, m, n_fg, lv_q, w->pairs,
                                                                       w->ctl, w->chunk_pair, w->partial);
     else
 #endif
-      k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, w->ridx[cur], w->q[cur],
+      k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, lv_ridx, lv_q,
                                                                    w->pairs, w->ctl, w->chunk_pair, w->partial,
                                                                    (lv == 0 && ridx_mode == 0) ? 1 : 0, d->gw,
                                                                    d->gw == 64 ? 1 : 0);
@@ -2110,7 +2128,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     if (n > 0) {
       k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n_dev, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
                                                           d->gw == 64 ? 6 : 5,
-                                                          w->ridx[cur], w->q[cur], w->ridx[cur ^ 1], w->q[cur ^ 1],
+                                                          lv_ridx, lv_q, w->ridx[cur ^ 1], w->q[cur ^ 1],
                                                           w->seg_cur[lv & 1], w->tile_seg, inline_plan ? 1 : 0, PA);
       OOCGB_CK(cudaGetLastError());
     }
@@ -2558,7 +2576,8 @@ void update_margin(oocgb_data d, oocgb_tree t, float *d_margin) {
   const int n = (int)d->n_sel;
   if (n > 0)
     k_update_margin<<<(n + 255) / 256, 256, 0, c->stream>>>(n, w->segs[w->final_cur], w->ctl, w->dnodes,
-                                                            w->ridx[w->final_cur], d_margin);
+                                                            w->ridx[w->final_cur],
+                                                            w->tile_seg, d_margin);
   OOCGB_CK(cudaGetLastError());
 }
 
