@@ -142,9 +142,12 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
                              Pair *pairs, LevelCtl *ctl, int n_sel_arg, int n_fg, int target_items,
                              int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
                              const int2 *q_in, int2 *q_out, int ridx_mode, int *chunk_pair, int2 *ent,
-                             int ent_cap) {
+                             int ent_cap, int *tile_seg, int n_tiles, int *seg_cur0) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nth = gridDim.x * blockDim.x;
+  // (the former memsets of the build's graph) one root segment for every partition tile
+  if (tile_seg)
+    for (int t = tid; t < n_tiles; t += nth) tile_seg[t] = 0;
   // n_sel_arg < 0: the sample's row count from the device sample state (graph independent of it)
   const int n_sel = n_sel_arg >= 0 ? n_sel_arg : (int)ss->n_sel_local;
   {
@@ -166,6 +169,8 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
       q_out[i] = q_in[i];
     }
   if (tid == 0) {
+    *ctl = LevelCtl{};  // the control block and the root segment's cursors start at zero
+    if (seg_cur0) { seg_cur0[0] = 0; seg_cur0[1] = 0; }
     RoundParams P;
     P.G = ss->G;
     P.H = ss->H;
@@ -2064,15 +2069,13 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     }
   };
   if (keep_debug) OOCGB_CK(cudaMemsetAsync(w->dbg, 0, sizeof(long long) * hsz * (size_t)std::max(1, (1 << D) - 1), c->stream));
-  OOCGB_CK(cudaMemsetAsync(w->ctl, 0, sizeof(LevelCtl), c->stream));
-  k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
-      w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta, w->segs[0], w->pairs, w->ctl, -1, n_fg, target, kmax,
-      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode, w->chunk_pair, w->ent, w->ent_cap);
-  OOCGB_CK(cudaGetLastError());
   int cur = 0;
   const int tiles = (n + kPartTile - 1) / kPartTile;
-  OOCGB_CK(cudaMemsetAsync(w->seg_cur[0], 0, 2 * sizeof(int), c->stream));  // the root segment's cursors
-  if (tiles > 0) OOCGB_CK(cudaMemsetAsync(w->tile_seg, 0, sizeof(int) * tiles, c->stream));  // one root segment
+  k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
+      w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta, w->segs[0], w->pairs, w->ctl, -1, n_fg, target, kmax,
+      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode, w->chunk_pair, w->ent, w->ent_cap, w->tile_seg, tiles,
+      w->seg_cur[0]);
+  OOCGB_CK(cudaGetLastError());
   for (int lv = 0; lv < D; ++lv) {
     const int max_pairs = lv == 0 ? 1 : (1 << (lv - 1));
     // this level's positions: level 0 reads the sample's buffers directly (identity rows or the
@@ -2450,7 +2453,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta,
                                                        w->segs[0], w->pairs, w->ctl, 0, n_fg, target, kmax, D,
                                                        d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], 0, w->chunk_pair, w->ent,
-                                                       w->ent_cap);
+                                                       w->ent_cap, nullptr, 0, nullptr);
   k_stream_init<<<c->num_sms * 4, 256, 0, c->stream>>>(sw.row_node, n);
   OOCGB_CK(cudaGetLastError());
   const int grid = c->num_sms * 8;
