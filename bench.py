@@ -182,11 +182,13 @@ def measured_traffic():
         return None
 
 
-def launches_per_round(D: int) -> int:
-    # update_margin 1 + logistic 1 + sample(NONE): sstate_init, absmax2, sstate_globalise, quantise 4
-    # build_tree: init 1 + per level (k_hist, k_eval, k_eval_narrow, k_finalize, k_part_fused) 5
-    # (matches the ncu launch list, profiles/r01_launches_summary.txt: 47 per depth-8 round)
-    return 6 + 1 + 5 * D
+def launches_per_round(D: int, world: int = 1) -> int:
+    # update_margin 1 + logistic 1 + sample(NONE): absmax2, quantise (one rank; with W > 1 also
+    # sstate_init, sstate_globalise around the all-reduces)
+    # build_tree: init 1 + per level (k_hist, k_eval or k_eval_blk, k_eval_narrow, k_finalize,
+    # k_part_fused) 5 (matches the ncu launch list: 45 per depth-8 round at W = 1); W > 1 adds
+    # k_reduce_partials, k_part_counts and k_part_plan per level
+    return (4 if world == 1 else 6) + 1 + (5 if world == 1 else 8) * D
 
 
 def make_data(rows, rank):
@@ -711,7 +713,7 @@ def main():
                        "max_bin": MAX_BIN, "max_depth": DEPTH, "quant_bits": QBITS,
                        "parallelism": f"row-sharded dp{world}" + (" (NCCL 1-rank exchange path)" if args.nccl1 and world == 1 else ""),
                        "l2": f"inputs larger than L2 ({rows * 512 / 1e6:.0f} MB ELLPACK per GPU vs 126 MB L2), no flush"},
-            "gpu_launches": launches_per_round(DEPTH) * args.steps,
+            "gpu_launches": launches_per_round(DEPTH, world) * args.steps,
             "rows_rounds_per_s": rows_global / (ms_step / 1e3),
             "histogram": {"row_features_per_s": hist_rowfeat / (hist_ms * 1e-3), "ms_per_round": hist_ms / args.steps,
                           "launches": n_hist, "algorithmic_bytes_per_round": hist_bytes / args.steps},

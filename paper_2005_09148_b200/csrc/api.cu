@@ -283,6 +283,7 @@ static void free_data(oocgb_data d) {
   dfree(d->d_cut_values); dfree(d->d_cut_ptrs); dfree(d->d_bins); dfree(d->d_sketch);
   dfree(d->d_sketch_count); dfree(d->d_g); dfree(d->d_h); dfree(d->d_sel_rows); dfree(d->d_q);
   dfree(d->d_sampled_page); dfree(d->d_gs); dfree(d->d_hs); dfree(d->d_tmp64); dfree(d->d_mvs); dfree(d->d_mvs_stats);
+  dfree(d->d_absparts);
   dfree(d->d_missing);
   for (int i = 0; i < 3; ++i) dfree(d->d_stage[i]);
   for (int i = 0; i < 2; ++i) dfree(d->d_arg[i]);

@@ -271,6 +271,7 @@ struct oocgb_data_s {
   int64_t sel_cap = 0;
   double *d_gs = nullptr, *d_hs = nullptr;  // scaled g', h' of the selected rows
   long long *d_tmp64 = nullptr;             // MVS g_hat / q64 [n_local]
+  float *d_absparts = nullptr;              // f = 1, one rank: per-block max |g|, |h| (k_absmax2)
   void *d_mvs = nullptr;                    // MVS device threshold state (sample.cu MvsDev)
   unsigned long long *d_mvs_stats = nullptr;  // its per-bucket (count, sum, max) [3][2048]
   int64_t tmp_cap = 0;

@@ -526,8 +526,12 @@ __device__ __forceinline__ float block_max_f(float v, float *s_w) {
   __syncthreads();
   return v;
 }
+// One rank (parts != nullptr): each block writes its (max |g|, max |h|) to parts[2 b .. 2 b + 1]
+// (no atomics, so nothing to zero first) and block 0 also initialises the sample state for f = 1
+// (k_sstate_init + k_sstate_globalise folded in); k_quantise reduces the parts.
 __global__ void __launch_bounds__(256) k_absmax2(const float *__restrict__ g, const float *__restrict__ h, int64_t n,
-                                                 unsigned long long *maxbits) {
+                                                 unsigned long long *maxbits, float *parts, SampleState *ss,
+                                                 int quant_bits) {
   __shared__ float s_w[32];
   float mg = 0.0f, mh = 0.0f;
   const int64_t n4 = n >> 2;
@@ -544,7 +548,22 @@ __global__ void __launch_bounds__(256) k_absmax2(const float *__restrict__ g, co
   }
   mg = block_max_f(mg, s_w);
   mh = block_max_f(mh, s_w);
-  if (threadIdx.x == 0) { atomic_max_abs(&maxbits[0], (double)mg); atomic_max_abs(&maxbits[1], (double)mh); }
+  if (threadIdx.x == 0) {
+    if (parts) {
+      parts[2 * blockIdx.x] = mg;
+      parts[2 * blockIdx.x + 1] = mh;
+      if (blockIdx.x == 0) {
+        ss->G = 0;
+        ss->H = 0;
+        ss->n_sel_local = n;
+        ss->n_sel_global = n;
+        ss->quant_bits = quant_bits;
+      }
+    } else {
+      atomic_max_abs(&maxbits[0], (double)mg);
+      atomic_max_abs(&maxbits[1], (double)mh);
+    }
+  }
 }
 
 // e = P - k with frexp(max |x|) = (., k); 0 when max = 0 (R12).  Device copy of the host rule.
@@ -586,10 +605,30 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long *s_w) {
 }
 template <typename T>
 __global__ void __launch_bounds__(256) k_quantise(const T *__restrict__ gs, const T *__restrict__ hs, SampleState *ss,
-                                                  int2 *__restrict__ q) {
+                                                  int2 *__restrict__ q, const float *__restrict__ parts, int n_parts) {
   __shared__ long long s_w[32];
-  const int eg = quant_exponent(ss->maxbits[0], ss->quant_bits);
-  const int eh = quant_exponent(ss->maxbits[1], ss->quant_bits);
+  __shared__ unsigned long long s_mb[2];
+  if (parts) {  // one rank, f = 1: the maxima from k_absmax2's per-block parts
+    __shared__ float s_f[32];
+    float mg = 0.0f, mh = 0.0f;
+    for (int i = threadIdx.x; i < n_parts; i += blockDim.x) {
+      mg = fmaxf(mg, parts[2 * i]);
+      mh = fmaxf(mh, parts[2 * i + 1]);
+    }
+    mg = block_max_f(mg, s_f);
+    mh = block_max_f(mh, s_f);
+    if (threadIdx.x == 0) {
+      s_mb[0] = (unsigned long long)__double_as_longlong((double)mg);
+      s_mb[1] = (unsigned long long)__double_as_longlong((double)mh);
+      if (blockIdx.x == 0) { ss->maxbits[0] = s_mb[0]; ss->maxbits[1] = s_mb[1]; }
+    }
+  } else if (threadIdx.x == 0) {
+    s_mb[0] = ss->maxbits[0];
+    s_mb[1] = ss->maxbits[1];
+  }
+  __syncthreads();
+  const int eg = quant_exponent(s_mb[0], ss->quant_bits);
+  const int eh = quant_exponent(s_mb[1], ss->quant_bits);
   if (blockIdx.x == 0 && threadIdx.x == 0) { ss->e_g = eg; ss->e_h = eh; }
   const double sg = ldexp(1.0, eg), sh = ldexp(1.0, eh);
   const int64_t n = ss->n_sel_local;
@@ -798,11 +837,23 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
   SampleState *ss = d->d_ss;
   d->quant_bits = quant_bits;
   bool need_sync = (info != nullptr);
+  // one rank, f = 1, rows present: 2 launches (k_absmax2 with the state init, k_quantise with the
+  // maxima reduction) instead of 4
+  const bool fuse1 = eff_mode == OOCGB_SAMPLE_NONE && !c->coll && n > 0;
+  int abs_parts = 0;
+  if (fuse1 && !d->d_absparts) d->d_absparts = (float *)dmalloc(sizeof(float) * 2 * (size_t)c->num_sms * 2);
   if (eff_mode == OOCGB_SAMPLE_NONE) {
     d->all_selected = true;
     d->n_sel = n;
-    k_sstate_init<<<1, 1, 0, c->stream>>>(ss, n, quant_bits);
-    if (n > 0) k_absmax2<<<grid_for(c, (n + 3) / 4, 256, 2), 256, 0, c->stream>>>(d->d_g, d->d_h, n, ss->maxbits);
+    if (fuse1) {  // one rank: state init folded into k_absmax2, maxima reduced by k_quantise
+      abs_parts = grid_for(c, (n + 3) / 4, 256, 2);
+      k_absmax2<<<abs_parts, 256, 0, c->stream>>>(d->d_g, d->d_h, n, nullptr, d->d_absparts, ss, quant_bits);
+    } else {
+      k_sstate_init<<<1, 1, 0, c->stream>>>(ss, n, quant_bits);
+      if (n > 0)
+        k_absmax2<<<grid_for(c, (n + 3) / 4, 256, 2), 256, 0, c->stream>>>(d->d_g, d->d_h, n, ss->maxbits, nullptr,
+                                                                          nullptr, 0);
+    }
   } else {
     d->all_selected = false;
     need_sync = true;  // the host needs n_sel (grids, graph key, compaction)
@@ -842,14 +893,17 @@ void sample_rows(oocgb_data d, int mode, double ratio, double mvs_lambda, uint64
       si.e_prime = hmv->e;
     }
   }
-  allreduce_max_u64(c, ss->maxbits, 2);
-  k_sstate_globalise<<<1, 1, 0, c->stream>>>(ss);
-  allreduce_sum_i64(c, &ss->n_sel_global, 1);
+  if (!fuse1) {
+    allreduce_max_u64(c, ss->maxbits, 2);
+    k_sstate_globalise<<<1, 1, 0, c->stream>>>(ss);
+    allreduce_sum_i64(c, &ss->n_sel_global, 1);
+  }
   const int qgrid = grid_for(c, std::max<int64_t>(1, (d->n_sel + 3) / 4), 256, 2);
   if (d->all_selected)
-    k_quantise<float><<<qgrid, 256, 0, c->stream>>>(d->d_g, d->d_h, ss, d->d_q);
+    k_quantise<float><<<qgrid, 256, 0, c->stream>>>(d->d_g, d->d_h, ss, d->d_q, fuse1 ? d->d_absparts : nullptr,
+                                                    abs_parts);
   else
-    k_quantise<double><<<qgrid, 256, 0, c->stream>>>(d->d_gs, d->d_hs, ss, d->d_q);
+    k_quantise<double><<<qgrid, 256, 0, c->stream>>>(d->d_gs, d->d_hs, ss, d->d_q, nullptr, 0);
   OOCGB_CK(cudaGetLastError());
   allreduce_sum_i64(c, &ss->G, 2);
   if (need_sync || d->placement == OOCGB_PLACE_PINNED_HOST) {
