@@ -713,7 +713,7 @@ def main():
                        "max_bin": MAX_BIN, "max_depth": DEPTH, "quant_bits": QBITS,
                        "parallelism": f"row-sharded dp{world}" + (" (NCCL 1-rank exchange path)" if args.nccl1 and world == 1 else ""),
                        "l2": f"inputs larger than L2 ({rows * 512 / 1e6:.0f} MB ELLPACK per GPU vs 126 MB L2), no flush"},
-            "gpu_launches": launches_per_round(DEPTH, world) * args.steps,
+            "gpu_launches": launches_per_round(DEPTH, 2 if (world > 1 or args.nccl1) else 1) * args.steps,
             "rows_rounds_per_s": rows_global / (ms_step / 1e3),
             "histogram": {"row_features_per_s": hist_rowfeat / (hist_ms * 1e-3), "ms_per_round": hist_ms / args.steps,
                           "launches": n_hist, "algorithmic_bytes_per_round": hist_bytes / args.steps},
