@@ -186,9 +186,10 @@ def launches_per_round(D: int, world: int = 1) -> int:
     # update_margin 1 + logistic 1 + sample(NONE): absmax2, quantise (one rank; with W > 1 also
     # sstate_init, sstate_globalise around the all-reduces)
     # build_tree: init 1 + per level (k_hist, k_eval or k_eval_blk, k_eval_narrow, k_finalize,
-    # k_part_fused) 5 (matches the ncu launch list: 45 per depth-8 round at W = 1); W > 1 adds
-    # k_reduce_partials, k_part_counts and k_part_plan per level
-    return (4 if world == 1 else 6) + 1 + (5 if world == 1 else 8) * D
+    # k_part_fused) 5, at level 0 of an f = 1 build only the root's own list (4) (matches the ncu
+    # launch list: 44 per depth-8 round at W = 1); W > 1 adds k_reduce_partials, k_part_counts and
+    # k_part_plan per level
+    return (4 if world == 1 else 6) + 1 + (5 if world == 1 else 8) * D - (1 if D > 0 else 0)
 
 
 def make_data(rows, rank):

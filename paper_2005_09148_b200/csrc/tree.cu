@@ -48,14 +48,14 @@ struct RoundParams {
 };
 
 struct GraphKey {
-  int n, D, m, ridx_mode, keep_debug, profiling, world, has_missing;
+  int n, D, m, ridx_mode, keep_debug, profiling, world, has_missing, root_list;
   double lambda, gamma, mcw, eta;
   const void *bins;
   size_t pitch;
   int quant_bits;
   bool operator==(const GraphKey &o) const {
     return n == o.n && D == o.D && m == o.m && ridx_mode == o.ridx_mode && keep_debug == o.keep_debug &&
-           has_missing == o.has_missing &&
+           has_missing == o.has_missing && root_list == o.root_list &&
            profiling == o.profiling && world == o.world && lambda == o.lambda && gamma == o.gamma &&
            mcw == o.mcw && eta == o.eta && bins == o.bins && pitch == o.pitch && quant_bits == o.quant_bits;
   }
@@ -98,6 +98,7 @@ struct Work {
   long long *dbg = nullptr;
   size_t dbg_bytes = 0;
   int final_cur = 0;  // which ridx / segs buffer holds the final partition
+  int root_list = 0;  // level 0's evaluation list when known (1 general, 2 narrow; 0 both)
   int hist_grid = 0;
   RoundParams *d_rp = nullptr;     // device copy of the per-call scalars
   RoundParams *h_rp = nullptr;     // pinned staging
@@ -574,6 +575,7 @@ struct EvalArgs {
   // histograms whose rows hold hm = msl features; world == 1: f0 = 0, mf = hm = msl = m)
   int f0, mf, hm, msl, max_slots;
   int crank;  // candidate block of this rank's slice: f0 / msl
+  int root_list;  // level 0 only: 1 the root is on the general list, 2 narrow, 0 unknown
 };
 
 // candidates [owner rank][slot][msl]: rank r writes features [r msl, (r + 1) msl) into block r,
@@ -1281,10 +1283,15 @@ k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs,
   if (dn[node].feature != -1) return;  // absent slot (streamed mode lists every slot)
   const int slot = node - level_first(d);
   BestSplit best{0.0, 0, 0x7fffffff, 0, 0, 0};
+  // candidate (slot, j) at cand_index(msl, max_slots, slot, j), the owner block r = j / msl
+  // carried along instead of divided per candidate
+  int r = (int)threadIdx.x / msl, jr = (int)threadIdx.x - r * msl;
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    const Cand cd = cand[cand_index(msl, max_slots, slot, j)];
+    const Cand cd = cand[((size_t)r * max_slots + slot) * msl + jr];
     BestSplit x{cd.gain, cd.valid, j, cd.bin, cd.GL, cd.HL};
     if (better(x, best)) best = x;
+    jr += blockDim.x;
+    while (jr >= msl) { jr -= msl; ++r; }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -1326,12 +1333,14 @@ static void launch_eval(const EvalArgs &A, int max_pairs, oocgb_ctx c, cudaStrea
   const bool blk = OOCGB_EVAL_WIDE_BLOCK && !A.streamed && A.d == 0 && A.mf <= num_sms * kBlkPerSm;
   if (blk) {
     const unsigned gb = (unsigned)std::max(1, A.mf);
+    // the root is on exactly one list; root_list (host-known when every row is selected): 1
+    // general, 2 narrow, 0 unknown (a sampled graph serves every row count: both launched)
     if (A.has_missing) {  // R27: candidates in both default directions
-      k_eval_blk<true><<<gb, kBlkThreads, 0, st>>>(A);
-      k_eval_narrow<true><<<gn, kEvalWarps * 32, 0, st>>>(A);
+      if (A.root_list != 2) k_eval_blk<true><<<gb, kBlkThreads, 0, st>>>(A);
+      if (A.root_list != 1) k_eval_narrow<true><<<gn, kEvalWarps * 32, 0, st>>>(A);
     } else {
-      k_eval_blk<false><<<gb, kBlkThreads, 0, st>>>(A);
-      k_eval_narrow<false><<<gn, kEvalWarps * 32, 0, st>>>(A);
+      if (A.root_list != 2) k_eval_blk<false><<<gb, kBlkThreads, 0, st>>>(A);
+      if (A.root_list != 1) k_eval_narrow<false><<<gn, kEvalWarps * 32, 0, st>>>(A);
     }
   } else if (A.has_missing) {  // R27: candidates in both default directions
     k_eval<true><<<gw, kEvalWarps * 32, 0, st>>>(A);
@@ -1951,6 +1960,8 @@ __global__ void k_leaf_of_pos(int n, const Seg *__restrict__ segs, int n_segs, c
 }
 
 // ---------------------------------------------------------------------------------------------
+static int kmax_of(oocgb_data d) { return (int)((0x7fffffffLL) >> d->quant_bits); }
+
 static void ensure_work(oocgb_data d, int D) {
   oocgb_ctx c = d->ctx;
   Work *&w = d->work;
@@ -2117,6 +2128,8 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.f0 = c->coll ? std::min(m, c->rank * w->msl) : 0;
     A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
     A.crank = c->coll ? c->rank : 0;
+    // f = 1: the root's global row count is fixed, so its list is known when capturing
+    A.root_list = lv == 0 ? w->root_list : 0;
     launch_eval(A, max_pairs, c, c->stream);
     mark(1, false);
     mark(2, true);
@@ -2194,8 +2207,11 @@ oocgb_tree build_tree(oocgb_data d, int D, double lambda, double gamma, double m
     if (w->dbg_bytes < need) { drop_graph(w); dfree(w->dbg); w->dbg = (long long *)dmalloc(need); w->dbg_bytes = need; }
   }
   // keyed by the capacity, not the sample's row count: sampled rounds replay one graph
+  // f = 1: every row is selected, so the root's list (general iff > kmax global rows) is known
+  // here and the other list's level-0 launch is left out of the graph
+  w->root_list = d->all_selected ? (d->n_global > kmax_of(d) ? 1 : 2) : 0;
   GraphKey key{(int)w->cap_rows, D, m, ridx_mode, keep_debug ? 1 : 0, c->profiling ? 1 : 0, c->world,
-               d->has_missing ? 1 : 0, lambda, gamma, mcw, eta, bins, pitch, d->quant_bits};
+               d->has_missing ? 1 : 0, w->root_list, lambda, gamma, mcw, eta, bins, pitch, d->quant_bits};
   if (c->host_coll) {
     // host-callback collectives synchronise the stream: run the level loop directly
     drop_graph(w);
@@ -2501,6 +2517,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     A.f0 = c->coll ? std::min(m, c->rank * w->msl) : 0;
     A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
     A.crank = c->coll ? c->rank : 0;
+    A.root_list = 0;
     launch_eval(A, n_slots, c, c->stream);
   }
   // export (same as the in-core path)
