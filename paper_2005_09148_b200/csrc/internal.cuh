@@ -85,7 +85,7 @@ struct DNode {
   long long n_rows;    // global sampled rows
   long long Gq, Hq;    // fixed-point sums (global)
   int32_t default_left;  // R27: missing values (symbol 255) go left
-  int32_t pad;
+  int32_t seg;           // the node's segment index at its level (set by the plan that creates it)
   double tP;             // G^2 / (H + lambda) of the node (Eq. 8's parent term), set with the sums
 };
 
@@ -93,8 +93,12 @@ struct DNode {
 struct Seg {
   int32_t begin, count;  // local positions
   int32_t node;          // heap index
-  int32_t pad;
+  int32_t dec;           // the node's split at this level, written by k_finalize: -1 none, else
+                         // feature << 10 | default_left << 9 | split_bin (the partition's one read)
 };
+__host__ __device__ __forceinline__ int seg_dec(int feature, int default_left, int split_bin) {
+  return (feature << 10) | (default_left << 9) | split_bin;
+}
 
 // Sibling pair built at a level: `built` gets a histogram from rows, `derived` = parent - built.
 struct Pair {

@@ -196,7 +196,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
     r.n_rows = P.n_rows_global;
     node_fill(r, P.G, P.H, P.sg_inv, P.sh_inv, lambda, eta, &ctl->error);
     dn[0] = r;
-    segs[0] = Seg{0, n_sel, 0, 0};
+    segs[0] = Seg{0, n_sel, 0, -1};
     const long long cr = hist_chunk_rows(n_sel, 1, n_fg, target_items, kmax);
     const int nch = (int)((n_sel + cr - 1) / cr);
     const int crq = nch > 0 ? (int)((n_sel + nch - 1) / nch) : (int)cr;  // equal chunks
@@ -576,6 +576,7 @@ struct EvalArgs {
   int f0, mf, hm, msl, max_slots;
   int crank;  // candidate block of this rank's slice: f0 / msl
   int root_list;  // level 0 only: 1 the root is on the general list, 2 narrow, 0 unknown
+  Seg *segs;      // this level's segments (k_finalize records each split in its node's segment)
 };
 
 // candidates [owner rank][slot][msl]: rank r writes features [r msl, (r + 1) msl) into block r,
@@ -1274,7 +1275,8 @@ __device__ __forceinline__ BestSplit shfl_best(const BestSplit &x, int o) {
 __global__ void __launch_bounds__(256)
 k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs, LevelCtl *ctl,
            const Cand *__restrict__ cand, DNode *dn, const float *__restrict__ cut_values,
-           const int *__restrict__ cut_ptrs, const RoundParams *__restrict__ rp, double lambda, double eta) {
+           const int *__restrict__ cut_ptrs, const RoundParams *__restrict__ rp, double lambda, double eta,
+           Seg *segs) {
   const int p = blockIdx.x >> 1;
   if (p >= ctl->n_pairs) return;
   const Pair P = pairs[p];
@@ -1312,6 +1314,7 @@ k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs,
       nd.default_left = best.bin & 1;
       nd.split_value = cut_values[cut_ptrs[best.j] + (best.bin >> 1)];
       nd.gain = best.gain;
+      if (segs) segs[nd.seg].dec = seg_dec(best.j, best.bin & 1, best.bin >> 1);  // for the partition
       DNode L{}, R{};
       L.feature = -1;
       R.feature = -1;
@@ -1355,7 +1358,7 @@ static void launch_eval(const EvalArgs &A, int max_pairs, oocgb_ctx c, cudaStrea
     allgather_i64_inplace(c, reinterpret_cast<long long *>(A.cand),
                           (size_t)A.max_slots * A.msl * (sizeof(Cand) / sizeof(long long)));
   k_finalize<<<(unsigned)(max_pairs * 2), 256, 0, st>>>(A.d, A.m, A.msl, A.max_slots, A.pairs, A.ctl, A.cand, A.dn,
-                                                         A.cut_values, A.cut_ptrs, A.rp, A.lambda, A.eta);
+                                                         A.cut_values, A.cut_ptrs, A.rp, A.lambda, A.eta, A.segs);
   OOCGB_CK(cudaGetLastError());
 }
 
@@ -1406,9 +1409,8 @@ __device__ __forceinline__ void load_tile_segs(TileSegs &T, const Seg *__restric
     const Seg S = segs[T.first + k];
     T.begin[k] = S.begin;
     T.end[k] = S.begin + S.count;
-    const DNode &nd = dn[S.node];
-    T.feat[k] = nd.feature;
-    T.sbin[k] = nd.split_bin | (nd.default_left << 9);  // bit 9: missing values go left (R27)
+    T.feat[k] = S.dec >= 0 ? S.dec >> 10 : -1;     // the decision rides in the segment (one read)
+    T.sbin[k] = S.dec >= 0 ? (S.dec & 0x3ff) : 0;   // split_bin | default_left << 9 (R27); bit 8 clear
   }
   __syncthreads();
 }
@@ -1522,9 +1524,9 @@ k_part_fused(const long long *__restrict__ n_dev, const Seg *__restrict__ segs, 
         } else {
           k = k < 0 ? seg_of(segs, n_segs, p) : k;
           while (segs[k].begin + segs[k].count <= p) ++k;
-          const DNode &nd = dn[segs[k].node];
-          f = nd.feature;
-          sb[u] = nd.split_bin | (nd.default_left << 9);
+          const int dec = segs[k].dec;
+          f = dec >= 0 ? dec >> 10 : -1;
+          sb[u] = dec >= 0 ? (dec & 0x3ff) : 0;
         }
         sg[u] = k;
       }
@@ -1675,7 +1677,7 @@ __device__ void plan_level_loop(const PlanArgs &A) {
   for (int base = 0; base < n_segs; base += T) {
     const int s = base + threadIdx.x;
     int split = 0;
-    if (s < n_segs) split = dn[segs[s].node].feature >= 0;
+    if (s < n_segs) split = segs[s].dec >= 0;
     int tot_s, tot_p;
     const int es = block_excl_scan(s < n_segs ? 1 + split : 0, &tot_s);
     const int ep = block_excl_scan(split, &tot_p);
@@ -1687,8 +1689,10 @@ __device__ void plan_level_loop(const PlanArgs &A) {
         const long long gl = seg_cnt ? seg_cnt[2 * s] : nl, gr = seg_cnt ? seg_cnt[2 * s + 1] : nr;
         dn[2 * S.node + 1].n_rows = gl;
         dn[2 * S.node + 2].n_rows = gr;
-        segs_next[ns] = Seg{S.begin, nl, 2 * S.node + 1, 0};
-        segs_next[ns + 1] = Seg{S.begin + nl, nr, 2 * S.node + 2, 0};
+        segs_next[ns] = Seg{S.begin, nl, 2 * S.node + 1, -1};
+        segs_next[ns + 1] = Seg{S.begin + nl, nr, 2 * S.node + 2, -1};
+        dn[2 * S.node + 1].seg = ns;
+        dn[2 * S.node + 2].seg = ns + 1;
         Pair pr;
         pr.parent = S.node;
         long long gb, gd;
@@ -1794,7 +1798,7 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
     nl = __ldcg(A.cur + 2 * s);  // final cursor atomics (L2)
     nr = __ldcg(A.cur + 2 * s + 1);
     if (A.seg_cnt) { gl = A.seg_cnt[2 * s]; gr = A.seg_cnt[2 * s + 1]; }
-    split = A.dn[S.node].feature >= 0;
+    split = S.dec >= 0;
   }
   if (!A.seg_cnt) { gl = nl; gr = nr; }
   int tot_s, tot_p;
@@ -1814,8 +1818,10 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
     if (split) {
       A.dn[2 * S.node + 1].n_rows = gl;
       A.dn[2 * S.node + 2].n_rows = gr;
-      emit(ns, Seg{S.begin, nl, 2 * S.node + 1, 0});
-      emit(ns + 1, Seg{S.begin + nl, nr, 2 * S.node + 2, 0});
+      emit(ns, Seg{S.begin, nl, 2 * S.node + 1, -1});
+      emit(ns + 1, Seg{S.begin + nl, nr, 2 * S.node + 2, -1});
+      A.dn[2 * S.node + 1].seg = ns;
+      A.dn[2 * S.node + 2].seg = ns + 1;
       pr.parent = S.node;
       long long gb, gd;
       if (gl <= gr) { pr.built = 2 * S.node + 1; pr.derived = 2 * S.node + 2; pr.begin = S.begin; pr.count = nl; gb = gl; gd = gr; }
@@ -2130,6 +2136,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     A.crank = c->coll ? c->rank : 0;
     // f = 1: the root's global row count is fixed, so its list is known when capturing
     A.root_list = lv == 0 ? w->root_list : 0;
+    A.segs = w->segs[cur];
     launch_eval(A, max_pairs, c, c->stream);
     mark(1, false);
     mark(2, true);
@@ -2518,6 +2525,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     A.mf = std::max(0, std::min(m, A.f0 + w->msl) - A.f0);
     A.crank = c->coll ? c->rank : 0;
     A.root_list = 0;
+    A.segs = nullptr;  // no partition in the streamed build
     launch_eval(A, n_slots, c, c->stream);
   }
   // export (same as the in-core path)
