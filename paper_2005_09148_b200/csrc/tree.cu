@@ -1462,6 +1462,7 @@ struct PlanArgs {
   int n_fg, target_items, kmax;
   int2 *ent;        // eval work lists (EvalArgs::ent)
   int ent_cap;
+  int last;         // the tree's last level: only segments, children counts and the tile table
 };
 __device__ void plan_level(const PlanArgs &A, int n_segs);
 #ifdef OOCGB_PLAN_TRACE
@@ -1832,6 +1833,27 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
       emit(ns, S);
     }
   }
+  if (A.last) {  // no next level: its pairs, work lists and chunking are never read
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+      int lo = 0, hi = tot_s - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_begin[mid] <= t * kPartTile) lo = mid; else hi = mid - 1;
+      }
+      A.tile_seg[t] = lo;
+    }
+    if (threadIdx.x == 0) {
+      A.ctl->n_pairs = 0;
+      A.ctl->n_items = 0;
+      A.ctl->n_segs = tot_s;
+      A.ctl->n_splits = 0;
+      A.ctl->hist_next = 0;
+      A.ctl->n_ew = 0;
+      A.ctl->n_en = 0;
+    }
+    return;
+  }
   // eval work lists: (pair, side) of nodes with <= kmax global rows -> narrow, else general
   {
     long long gb = 0, gd = 0;
@@ -2147,6 +2169,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     PA.chunk_pair = w->chunk_pair;
     PA.n_dev = n_dev; PA.n_fg = n_fg; PA.target_items = target; PA.kmax = kmax;
     PA.ent = w->ent; PA.ent_cap = w->ent_cap;
+    PA.last = lv == D - 1 ? 1 : 0;
     const bool inline_plan = !c->coll && n > 0;
     if (n > 0) {
       k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n_dev, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
