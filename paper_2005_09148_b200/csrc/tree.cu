@@ -1803,8 +1803,12 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
   }
   if (!A.seg_cnt) { gl = nl; gr = nr; }
   int tot_s, tot_p;
-  const int ns = block_excl_scan(s < n_segs ? 1 + split : 0, &tot_s);
-  const int np = block_excl_scan(split, &tot_p);
+  // one scan of two packed 16-bit counts (next segments | pairs << 16; totals <= 512)
+  int tot_sp;
+  const int nsp = block_excl_scan((s < n_segs ? 1 + split : 0) | (split << 16), &tot_sp);
+  const int ns = nsp & 0xffff, np = nsp >> 16;
+  tot_s = tot_sp & 0xffff;
+  tot_p = tot_sp >> 16;
   Pair pr{};
   const int n_tiles = (int)((*A.n_dev + kPartTile - 1) / kPartTile);
   // next-level segment starts staged in shared memory for the tile table (filled block-wide below)
@@ -1860,8 +1864,11 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
     if (split) { gb = pr.built == 2 * S.node + 1 ? gl : gr; gd = pr.built == 2 * S.node + 1 ? gr : gl; }
     const int nn = split ? (gb <= A.kmax) + (gd <= A.kmax) : 0;
     int tw, tn;
-    const int ew = block_excl_scan(split ? 2 - nn : 0, &tw);
-    const int en = block_excl_scan(nn, &tn);
+    int twn;  // one scan of (general | narrow << 16) entry counts (totals <= 512)
+    const int ewn = block_excl_scan((split ? 2 - nn : 0) | (nn << 16), &twn);
+    const int ew = ewn & 0xffff, en = ewn >> 16;
+    tw = twn & 0xffff;
+    tn = twn >> 16;
     if (split) {
       int iw = ew, in = en;
       if (gb <= A.kmax) A.ent[A.ent_cap + in++] = make_int2(np, 0); else A.ent[iw++] = make_int2(np, 0);
