@@ -1447,6 +1447,36 @@ __device__ int block_excl_scan(int v, int *total) {
   return r;
 }
 
+// The same with two alternating buffers and no trailing barrier: call sites pass buf = 0, 1, 0,
+// 1, ... so a buffer is rewritten only after the next call's two barriers (plan_level's scans).
+__device__ int block_excl_scan2(int v, int *total, int buf) {
+  __shared__ int s_w2[2][32];
+  __shared__ int s_tot2[2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) s_w2[buf][w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    int x = lane < nw ? s_w2[buf][lane] : 0, xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += u;
+    }
+    if (lane < nw) s_w2[buf][lane] = xi - x;
+    if (lane == 31) s_tot2[buf] = xi;
+  }
+  __syncthreads();
+  *total = s_tot2[buf];
+  return s_w2[buf][w] + incl - v;
+}
+
 struct PlanArgs {
   const Seg *segs;
   Seg *segs_next;
@@ -1805,7 +1835,7 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
   int tot_s, tot_p;
   // one scan of two packed 16-bit counts (next segments | pairs << 16; totals <= 512)
   int tot_sp;
-  const int nsp = block_excl_scan((s < n_segs ? 1 + split : 0) | (split << 16), &tot_sp);
+  const int nsp = block_excl_scan2((s < n_segs ? 1 + split : 0) | (split << 16), &tot_sp, 0);
   const int ns = nsp & 0xffff, np = nsp >> 16;
   tot_s = tot_sp & 0xffff;
   tot_p = tot_sp >> 16;
@@ -1865,7 +1895,7 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
     const int nn = split ? (gb <= A.kmax) + (gd <= A.kmax) : 0;
     int tw, tn;
     int twn;  // one scan of (general | narrow << 16) entry counts (totals <= 512)
-    const int ewn = block_excl_scan((split ? 2 - nn : 0) | (nn << 16), &twn);
+    const int ewn = block_excl_scan2((split ? 2 - nn : 0) | (nn << 16), &twn, 1);
     const int ew = ewn & 0xffff, en = ewn >> 16;
     tw = twn & 0xffff;
     tn = twn >> 16;
@@ -1880,7 +1910,7 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
   // chunks are numbered in decreasing chunk size (longest-processing-time-first order for
   // k_hist's dynamic item fetch; ties: pair order)
   int tot_rows;
-  block_excl_scan(split ? pr.count : 0, &tot_rows);
+  block_excl_scan2(split ? pr.count : 0, &tot_rows, 0);
   const long long cr = hist_chunk_rows(tot_rows, tot_p, A.n_fg, A.target_items, A.kmax);
   const int nch = split ? (int)((pr.count + cr - 1) / cr) : 0;
   const int crp = nch > 0 ? (pr.count + nch - 1) / nch : 0;
@@ -1899,7 +1929,7 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
   if (split) { s_key[rank] = np; s_cbase[rank] = nch; }
   __syncthreads();
   int tot_c;
-  const int cb = block_excl_scan(s < tot_p ? s_cbase[s] : 0, &tot_c);  // scan in rank order
+  const int cb = block_excl_scan2(s < tot_p ? s_cbase[s] : 0, &tot_c, 1);  // scan in rank order
   if (s < tot_p) s_cbase[s] = cb;
   __syncthreads();
   if (split) {
