@@ -1278,11 +1278,14 @@ k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs,
            const int *__restrict__ cut_ptrs, const RoundParams *__restrict__ rp, double lambda, double eta,
            Seg *segs) {
   const int p = blockIdx.x >> 1;
-  if (p >= ctl->n_pairs) return;
+  // the pair record is read together with the pair count (no dependent round trip; a slot past
+  // the count holds a stale record that is then ignored)
+  const int n_pairs = ctl->n_pairs;
   const Pair P = pairs[p];
+  if (p >= n_pairs) return;
   const int node = (blockIdx.x & 1) ? P.derived : P.built;
   if (node < 0) return;
-  if (dn[node].feature != -1) return;  // absent slot (streamed mode lists every slot)
+  if (!segs && dn[node].feature != -1) return;  // absent slot (streamed mode lists every slot)
   const int slot = node - level_first(d);
   BestSplit best{0.0, 0, 0x7fffffff, 0, 0, 0};
   // candidate (slot, j) at cand_index(msl, max_slots, slot, j), the owner block r = j / msl
@@ -2069,6 +2072,7 @@ static void ensure_work(oocgb_data d, int D) {
   w->chunk_pair = (int *)dmalloc(sizeof(int) * items);  // chunks <= items
   w->seg_cnt = (long long *)dmalloc(sizeof(long long) * 2 * max_segs);
   w->pairs = (Pair *)dmalloc(sizeof(Pair) * max_pairs);
+  OOCGB_CK(cudaMemset(w->pairs, 0, sizeof(Pair) * max_pairs));  // k_finalize reads past the count
   w->partial = (int *)dmalloc((size_t)items * kFG * kBins * 2 * sizeof(int));
   // world > 1: each rank evaluates a slice of msl = ceil(m / W) features (reduce-scattered
   // histograms), so parent histograms and the received sums hold msl features per row
