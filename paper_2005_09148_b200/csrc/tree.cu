@@ -30,6 +30,9 @@
 #ifndef OOCGB_EVAL_FOLD
 #define OOCGB_EVAL_FOLD 1
 #endif
+#ifndef OOCGB_NARROW_CU
+#define OOCGB_NARROW_CU 2  // chunk partials per load batch in k_eval_narrow
+#endif
 #ifndef OOCGB_HIST_LOAD
 #define OOCGB_HIST_LOAD 1  // measured: -4% at the levels below the root (profiles/r01_microbench_hist_levels.txt)
 #endif
@@ -957,7 +960,23 @@ __device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int s
     const size_t cstride = (size_t)A.n_fg * kFG * kBins;
     const int2 *src0 = reinterpret_cast<const int2 *>(A.partial) +
                        (((size_t)P.chunk_base * A.n_fg + j / kFG) * kFG + (j % kFG)) * kBins + lane;
-    for (int c = 0; c < P.n_chunks; ++c) {
+    // chunk partials NARROW_CU at a time (their loads in flight together: a multi-chunk node is
+    // one L2 round trip per NARROW_CU chunks, not per chunk)
+    int c = 0;
+#if OOCGB_NARROW_CU > 1
+    for (; c + OOCGB_NARROW_CU <= P.n_chunks; c += OOCGB_NARROW_CU) {
+      int2 v[OOCGB_NARROW_CU][8];
+#pragma unroll
+      for (int u = 0; u < OOCGB_NARROW_CU; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[u][i] = __ldg(src0 + (c + u) * cstride + 32 * i);
+#pragma unroll
+      for (int u = 0; u < OOCGB_NARROW_CU; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { g[i] += v[u][i].x; h[i] += v[u][i].y; }
+    }
+#endif
+    for (; c < P.n_chunks; ++c) {
       int2 v[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = __ldg(src0 + c * cstride + 32 * i);
