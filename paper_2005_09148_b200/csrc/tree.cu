@@ -36,6 +36,9 @@
 #ifndef OOCGB_HIST_LOAD
 #define OOCGB_HIST_LOAD 1  // measured: -4% at the levels below the root (profiles/r01_microbench_hist_levels.txt)
 #endif
+#ifndef OOCGB_FLUSH256
+#define OOCGB_FLUSH256 1  // k_hist flush with 256-bit stores (STG.E.ENL2.256)
+#endif
 #ifndef OOCGB_HIST_EXPERIMENT
 #define OOCGB_HIST_EXPERIMENT 0  // tools/microbench/hist_levels.cu only
 #endif
@@ -350,18 +353,31 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
     __syncthreads();
     // flush: warp w owns bins [32w, 32w+32); lane l = feature l -> conflict-free reads; each lane
     // writes its feature's 32 (g, h) pairs = 256 contiguous bytes of the [32][256][2] partial.
+    // Each store is one 256-bit STG of 4 bins (g, h): a lane-strided store touches one line per
+    // lane whatever its width, so 32-B stores halve the flush's L1 wavefronts against 16-B ones.
     const int f = fg * kFG + lane;
     for (int bb = warp; bb < kBins / 32; bb += kHistThreads / 32) {
-      int4 *dst = reinterpret_cast<int4 *>(partial + (((size_t)item * kFG + lane) * kBins + bb * 32) * 2);
+      int *dst = partial + (((size_t)item * kFG + lane) * kBins + bb * 32) * 2;
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const int i0 = (bb * 32 + i) * 64 + lane, i1 = i0 + 64;
-        int4 v = make_int4(S[i0], S[i0 + 32], S[i1], S[i1 + 32]);
+      for (int i = 0; i < 32; i += 4) {
+        const int i0 = (bb * 32 + i) * 64 + lane;
+        const int a0 = S[i0], a1 = S[i0 + 32], a2 = S[i0 + 64], a3 = S[i0 + 96];
+        const int a4 = S[i0 + 128], a5 = S[i0 + 160], a6 = S[i0 + 192], a7 = S[i0 + 224];
 #if OOCGB_HIST_EXPERIMENT & 2  // microbenchmark: no partial stores
-        if (f < m && v.x == 0x7fffffff) dst[i >> 1] = v;
+        if (f < m && a0 == 0x7fffffff)
 #else
-        if (f < m) dst[i >> 1] = v;
+        if (f < m)
 #endif
+        {
+#if OOCGB_FLUSH256
+          asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 2 * i), "r"(a0),
+                       "r"(a1), "r"(a2), "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
+                       : "memory");
+#else
+          reinterpret_cast<int4 *>(dst + 2 * i)[0] = make_int4(a0, a1, a2, a3);
+          reinterpret_cast<int4 *>(dst + 2 * i)[1] = make_int4(a4, a5, a6, a7);
+#endif
+        }
       }
     }
     __syncthreads();
