@@ -29,6 +29,21 @@ constexpr int kSelTile = kSelThreads * kSelPerThread;
 __device__ __forceinline__ void atomic_max_abs(unsigned long long *dst, double x) {
   atomicMax(dst, (unsigned long long)__double_as_longlong(fabs(x)));
 }
+// The same from one thread per block after a block reduction, and only when the value can raise
+// the current maximum (a plain read filters the rest: same-address atomics serialise at L2).
+__device__ __forceinline__ void atomic_max_bits_filtered(unsigned long long *dst, unsigned long long bits) {
+  if (bits > *(volatile unsigned long long *)dst) atomicMax(dst, bits);
+}
+__device__ __forceinline__ double block_max_d(double v, double *s_w) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) s_w[w] = v;
+  __syncthreads();
+  v = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0.0;
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  return v;
+}
 
 // binary:logistic gradients (Eq. 5; harness helper): double arithmetic, float32 results.
 // 4 rows per thread and step (16-B loads and stores), the same per-row arithmetic.
@@ -93,8 +108,9 @@ __global__ void k_mvs_ghat_max(const float *__restrict__ g, const float *__restr
     const double gi = (double)g[i], hi = (double)h[i];
     mx = fmax(mx, __dsqrt_rn(__dadd_rn(__dmul_rn(gi, gi), __dmul_rn(lam, __dmul_rn(hi, hi)))));
   }
-  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, (unsigned long long)__double_as_longlong(mx));
+  __shared__ double s_w[32];
+  mx = block_max_d(mx, s_w);
+  if (threadIdx.x == 0) atomic_max_bits_filtered(maxbits, (unsigned long long)__double_as_longlong(mx));
 }
 
 __device__ __forceinline__ void mvs_geometry(MvsDev *mv) {
@@ -306,7 +322,15 @@ __global__ void k_mvs_totals(const long long *__restrict__ q, int64_t n, MvsDev 
     c += __shfl_down_sync(0xffffffffu, c, o);
     s += __shfl_down_sync(0xffffffffu, s, o);
   }
-  if ((threadIdx.x & 31) == 0) { atomicAdd(&mv->tot[0], c); atomicAdd(&mv->tot[1], s); }
+  __shared__ unsigned long long s_c[32], s_s[32];  // block sums: one atomic per block and value
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { s_c[w] = c; s_s[w] = s; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) { c += s_c[k]; s += s_s[k]; }
+    atomicAdd(&mv->tot[0], c);
+    atomicAdd(&mv->tot[1], s);
+  }
 }
 
 __global__ void k_mvs_finish(MvsDev *mv, unsigned long long f_q, long long n_global) {
@@ -505,11 +529,13 @@ __global__ void k_select_scatter(SelParams P0, const MvsDev *mv, const long long
     }
   }
   (void)s_flags;
-  for (int o = 16; o; o >>= 1) {
-    mg = fmax(mg, __shfl_down_sync(0xffffffffu, mg, o));
-    mh = fmax(mh, __shfl_down_sync(0xffffffffu, mh, o));
+  __shared__ double s_m[32];
+  mg = block_max_d(mg, s_m);  // (|g'|, |h'| >= 0)
+  mh = block_max_d(mh, s_m);
+  if (threadIdx.x == 0) {
+    atomic_max_bits_filtered(&maxbits[0], (unsigned long long)__double_as_longlong(mg));
+    atomic_max_bits_filtered(&maxbits[1], (unsigned long long)__double_as_longlong(mh));
   }
-  if (lane == 0) { atomic_max_abs(&maxbits[0], mg); atomic_max_abs(&maxbits[1], mh); }
 }
 
 // max |g|, |h| over all rows (NONE mode): 16-B loads (4 rows per thread and step), the maxima
