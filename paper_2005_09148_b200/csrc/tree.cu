@@ -1546,7 +1546,7 @@ k_part_fused(const long long *__restrict__ n_dev, const Seg *__restrict__ segs, 
              const DNode *__restrict__ dn, const uint8_t *__restrict__ bins, size_t pitch, int lgw,
              const int32_t *__restrict__ ridx, const int2 *__restrict__ q, int32_t *__restrict__ ridx_out,
              int2 *__restrict__ q_out, int *__restrict__ cur, const int *__restrict__ tile_seg, int plan_inline,
-             PlanArgs PA) {
+             PlanArgs PA, int cap) {
   static_assert(kPartTile == 8 * kPartThreads, "8 positions per thread");
 #ifdef OOCGB_PLAN_TRACE
   if (threadIdx.x == 0) {
@@ -1558,20 +1558,22 @@ k_part_fused(const long long *__restrict__ n_dev, const Seg *__restrict__ segs, 
   __shared__ TileSegs T;
   __shared__ int s_pre[8][kPartThreads / 32];  // (left | right << 16) per (u, warp), then exclusive prefix
   __shared__ int s_tot;
-  const int n_segs = ctl->n_segs;
-  const int n = (int)*n_dev;  // the sample's rows (the grid covers the capacity)
-  const int n_tiles = (n + kPartTile - 1) / kPartTile;
   const int t0 = blockIdx.x * kPartTile;
-  const int t1 = min(n, t0 + kPartTile);
-  if (t0 < n) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // row ids and gradient pairs first, bounded by the buffers' capacity (not the sample's row
+  // count, which is itself a load): both round trips overlap
   int rows[8], sg[8];
   int2 qs[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int p = t0 + u * kPartThreads + threadIdx.x;
-    if (p < t1) { rows[u] = ridx ? ridx[p] : p; qs[u] = q[p]; }  // ridx null: identity (level 0)
+    if (p < cap) { rows[u] = ridx ? ridx[p] : p; qs[u] = q[p]; }  // ridx null: identity (level 0)
   }
+  const int n_segs = ctl->n_segs;
+  const int n = (int)*n_dev;  // the sample's rows (the grid covers the capacity)
+  const int n_tiles = (n + kPartTile - 1) / kPartTile;
+  const int t1 = min(n, t0 + kPartTile);
+  if (t0 < n) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   load_tile_segs(T, segs, n_segs, dn, tile_seg, blockIdx.x, n_tiles);
   const bool staged = T.count <= kTileSegs;
   uint32_t rbits = 0, lbits = 0;  // right / left (of a split segment) per u
@@ -2251,7 +2253,8 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
       k_part_fused<<<tiles, kPartThreads, 0, c->stream>>>(n_dev, w->segs[cur], w->ctl, w->dnodes, bins, pitch,
                                                           d->gw == 64 ? 6 : 5,
                                                           lv_ridx, lv_q, w->ridx[cur ^ 1], w->q[cur ^ 1],
-                                                          w->seg_cur[lv & 1], w->tile_seg, inline_plan ? 1 : 0, PA);
+                                                          w->seg_cur[lv & 1], w->tile_seg, inline_plan ? 1 : 0, PA,
+                                                          n);
       OOCGB_CK(cudaGetLastError());
     }
     if (c->coll) {
