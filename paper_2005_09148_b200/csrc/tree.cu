@@ -88,7 +88,7 @@ struct Work {
   oocgb::Seg *segs[2] = {nullptr, nullptr};
   int *seg_cur[2] = {nullptr, nullptr};  // per-segment (left, right) cursors, ping-pong by level
   int *tile_seg = nullptr;               // partition tile -> first segment
-  int *chunk_pair = nullptr;             // histogram chunk -> pair
+  int2 *chunk_rng = nullptr;            // histogram chunk -> its position range [r0, r1)
   long long *seg_cnt = nullptr;
   oocgb::Pair *pairs = nullptr;
   int *partial = nullptr;
@@ -148,7 +148,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
                              double lambda, double mcw, double eta, Seg *segs,
                              Pair *pairs, LevelCtl *ctl, int n_sel_arg, int n_fg, int target_items,
                              int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
-                             const int2 *q_in, int2 *q_out, int ridx_mode, int *chunk_pair, int2 *ent,
+                             const int2 *q_in, int2 *q_out, int ridx_mode, int2 *chunk_rng, int2 *ent,
                              int ent_cap, int *tile_seg, int n_tiles, int *seg_cur0) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nth = gridDim.x * blockDim.x;
@@ -160,7 +160,8 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
   {
     const long long cr = hist_chunk_rows(n_sel, 1, n_fg, target_items, kmax);
     const int nch = (int)((n_sel + cr - 1) / cr);
-    for (int c = tid; c < nch; c += nth) chunk_pair[c] = 0;  // every root chunk belongs to pair 0
+    const int crq = nch > 0 ? (int)((n_sel + nch - 1) / nch) : (int)cr;  // equal chunks of the root
+    for (int c = tid; c < nch; c += nth) chunk_rng[c] = make_int2(c * crq, min(n_sel, (c + 1) * crq));
   }
   for (int v = tid; v < n_nodes; v += nth) {
     DNode nd{};
@@ -233,7 +234,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
 __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
 k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int32_t *__restrict__ ridx,
        const int2 *__restrict__ q, const Pair *__restrict__ pairs, LevelCtl *ctl,
-       const int *__restrict__ chunk_pair, int *__restrict__ partial, int identity, int row_step, int gshift) {
+       const int2 *__restrict__ chunk_rng, int *__restrict__ partial, int identity, int row_step, int gshift) {
   extern __shared__ int4 smem4[];
   int *S = reinterpret_cast<int *>(smem4);
   char *Sb = reinterpret_cast<char *>(smem4);
@@ -260,10 +261,8 @@ k_hist(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const in
   for (int item = blockIdx.x; item < n_items; par ^= 1) {
     if (threadIdx.x == 0) s_next[par] = (int)gridDim.x + atomicAdd(&ctl->hist_next, 1);
     const int fg = item % n_fg, cg = item / n_fg;
-    const Pair P = pairs[chunk_pair[cg]];
-    const int c = cg - P.chunk_base;
-    const int r0 = P.begin + c * P.chunk_rows;
-    const int r1 = min(P.begin + P.count, r0 + P.chunk_rows);
+    const int2 rg = chunk_rng[cg];  // the chunk's positions (written by the plan: one load)
+    const int r0 = rg.x, r1 = rg.y;
 #if !(OOCGB_HIST_EXPERIMENT & 4)  // microbenchmark: no zero fill
     for (int i = threadIdx.x; i < 2 * kBins * kFG / 4; i += kHistThreads) smem4[i] = make_int4(0, 0, 0, 0);
 #endif
@@ -433,7 +432,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, unsigned
 
 __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
 k_hist_tma(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, const int2 *__restrict__ q,
-           const Pair *__restrict__ pairs, LevelCtl *ctl, const int *__restrict__ chunk_pair,
+           const Pair *__restrict__ pairs, LevelCtl *ctl, const int2 *__restrict__ chunk_rng,
            int *__restrict__ partial) {
   extern __shared__ int4 smem4[];
   int *S = reinterpret_cast<int *>(smem4);
@@ -463,7 +462,7 @@ k_hist_tma(const uint8_t *__restrict__ bins, size_t pitch, int m, int n_fg, cons
   for (int item = blockIdx.x; item < n_items; par ^= 1) {
     if (threadIdx.x == 0) s_next[par] = (int)gridDim.x + atomicAdd(&ctl->hist_next, 1);
     const int fg = item % n_fg, cg = item / n_fg;
-    const Pair P = pairs[chunk_pair[cg]];
+    const Pair P = pairs[chunk_rng[cg]];
     const int c = cg - P.chunk_base;
     const int r0 = P.begin + c * P.chunk_rows;
     const int r1 = min(P.begin + P.count, r0 + P.chunk_rows);
@@ -1525,7 +1524,7 @@ struct PlanArgs {
   int *cur_next;
   Pair *pairs;
   int *tile_seg;
-  int *chunk_pair;  // histogram chunk -> pair (k_hist's item lookup)
+  int2 *chunk_rng;  // histogram chunk -> its position range (k_hist's item lookup)
   const long long *n_dev;  // the sample's rows (device sample state)
   int n_fg, target_items, kmax;
   int2 *ent;        // eval work lists (EvalArgs::ent)
@@ -1835,7 +1834,8 @@ __device__ void plan_level_loop(const PlanArgs &A) {
       pairs[p].chunk_base = chunk_carry + e;
       pairs[p].n_chunks = nch;
       pairs[p].chunk_rows = nch > 0 ? (cnt + nch - 1) / nch : (int)cr;  // equal chunks
-      for (int c = 0; c < nch; ++c) A.chunk_pair[chunk_carry + e + c] = p;
+      const int b0 = pairs[p].begin, crp = nch > 0 ? (cnt + nch - 1) / nch : 0;
+      for (int c = 0; c < nch; ++c) A.chunk_rng[chunk_carry + e + c] = make_int2(b0 + c * crp, min(b0 + cnt, b0 + (c + 1) * crp));
     }
     chunk_carry += tot;
   }
@@ -1966,7 +1966,8 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
     }
   }
   __syncthreads();
-  if (split) { s_key[rank] = np; s_cbase[rank] = nch; }
+  __shared__ int s_pb[1024], s_pe[1024], s_pr[1024];  // by LPT rank: pair begin, end, chunk rows
+  if (split) { s_key[rank] = np; s_cbase[rank] = nch; s_pb[rank] = pr.begin; s_pe[rank] = pr.begin + pr.count; s_pr[rank] = crp; }
   __syncthreads();
   int tot_c;
   const int cb = block_excl_scan2(s < tot_p ? s_cbase[s] : 0, &tot_c, 1);  // scan in rank order
@@ -1996,7 +1997,8 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
       const int mid = (lo + hi + 1) >> 1;
       if (s_cbase[mid] <= c) lo = mid; else hi = mid - 1;
     }
-    A.chunk_pair[c] = s_key[lo];
+    const int b0 = s_pb[lo] + (c - s_cbase[lo]) * s_pr[lo];
+    A.chunk_rng[c] = make_int2(b0, min(s_pe[lo], b0 + s_pr[lo]));
   }
   if (threadIdx.x == 0) {
     A.ctl->n_pairs = tot_p;
@@ -2106,7 +2108,7 @@ static void ensure_work(oocgb_data d, int D) {
   }
   for (int i = 0; i < 2; ++i) w->seg_cur[i] = (int *)dmalloc(sizeof(int) * 2 * max_segs);
   w->tile_seg = (int *)dmalloc(sizeof(int) * std::max<int64_t>(1, tiles));
-  w->chunk_pair = (int *)dmalloc(sizeof(int) * items);  // chunks <= items
+  w->chunk_rng = (int2 *)dmalloc(sizeof(int2) * items);  // chunks <= items
   w->seg_cnt = (long long *)dmalloc(sizeof(long long) * 2 * max_segs);
   w->pairs = (Pair *)dmalloc(sizeof(Pair) * max_pairs);
   OOCGB_CK(cudaMemset(w->pairs, 0, sizeof(Pair) * max_pairs));  // k_finalize reads past the count
@@ -2143,7 +2145,7 @@ void free_work(oocgb_data d) {
   Work *w = d->work;
   if (!w) return;
   for (int i = 0; i < 2; ++i) { dfree(w->ridx[i]); dfree(w->q[i]); dfree(w->segs[i]); dfree(w->phist[i]); }
-  dfree(w->seg_cur[0]); dfree(w->seg_cur[1]); dfree(w->tile_seg); dfree(w->chunk_pair); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64); dfree(w->rs_send);
+  dfree(w->seg_cur[0]); dfree(w->seg_cur[1]); dfree(w->tile_seg); dfree(w->chunk_rng); dfree(w->seg_cnt); dfree(w->pairs); dfree(w->partial); dfree(w->built64); dfree(w->rs_send);
   dfree(w->cand); dfree(w->ent); dfree(w->dnodes); dfree(w->ctl); dfree(w->dbg); dfree(w->d_rp);
   dfree(w->sw.row_node); dfree(w->sw.b_slot); dfree(w->sw.b_ridx); dfree(w->sw.b_q); dfree(w->sw.slot_cnt);
   dfree(w->sw.slot_cur);
@@ -2190,7 +2192,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
   const int tiles = (n + kPartTile - 1) / kPartTile;
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(
       w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta, w->segs[0], w->pairs, w->ctl, -1, n_fg, target, kmax,
-      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode, w->chunk_pair, w->ent, w->ent_cap, w->tile_seg, tiles,
+      D, d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], ridx_mode, w->chunk_rng, w->ent, w->ent_cap, w->tile_seg, tiles,
       w->seg_cur[0]);
   OOCGB_CK(cudaGetLastError());
   for (int lv = 0; lv < D; ++lv) {
@@ -2203,11 +2205,11 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
 #if OOCGB_HIST_TMA
     if (lv == 0 && ridx_mode == 0 && d->gw == 32)  // identity level: bulk feed
       k_hist_tma<<<w->hist_grid, kHistThreads, kTmaSmem, c->stream>>>(bins, pitch, m, n_fg, lv_q, w->pairs,
-                                                                      w->ctl, w->chunk_pair, w->partial);
+                                                                      w->ctl, w->chunk_rng, w->partial);
     else
 #endif
       k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(bins, pitch, m, n_fg, lv_ridx, lv_q,
-                                                                   w->pairs, w->ctl, w->chunk_pair, w->partial,
+                                                                   w->pairs, w->ctl, w->chunk_rng, w->partial,
                                                                    (lv == 0 && ridx_mode == 0) ? 1 : 0, d->gw,
                                                                    d->gw == 64 ? 1 : 0);
     OOCGB_CK(cudaGetLastError());
@@ -2244,7 +2246,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
     PA.segs = w->segs[cur]; PA.segs_next = w->segs[cur ^ 1]; PA.ctl = w->ctl; PA.dn = w->dnodes;
     PA.cur = w->seg_cur[lv & 1]; PA.seg_cnt = c->coll ? w->seg_cnt : nullptr;
     PA.cur_next = w->seg_cur[(lv + 1) & 1]; PA.pairs = w->pairs; PA.tile_seg = w->tile_seg;
-    PA.chunk_pair = w->chunk_pair;
+    PA.chunk_rng = w->chunk_rng;
     PA.n_dev = n_dev; PA.n_fg = n_fg; PA.target_items = target; PA.kmax = kmax;
     PA.ent = w->ent; PA.ent_cap = w->ent_cap;
     PA.last = lv == D - 1 ? 1 : 0;
@@ -2254,7 +2256,7 @@ static void record_build(oocgb_data d, int D, double lambda, double gamma, doubl
                                                           d->gw == 64 ? 6 : 5,
                                                           lv_ridx, lv_q, w->ridx[cur ^ 1], w->q[cur ^ 1],
                                                           w->seg_cur[lv & 1], w->tile_seg, inline_plan ? 1 : 0, PA,
-                                                          n);
+                                                          lv > 0 ? n : (int)std::min<int64_t>(n, d->sel_cap));
       OOCGB_CK(cudaGetLastError());
     }
     if (c->coll) {
@@ -2466,7 +2468,7 @@ __global__ void k_stream_assign(const uint8_t *__restrict__ batch, int stride, i
 __global__ void __launch_bounds__(1024)
 k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *__restrict__ slot_cur,
               Pair *__restrict__ pairs, LevelCtl *ctl, int n_fg, int target_items, int kmax, int64_t batch_rows,
-              int *__restrict__ chunk_pair, int2 *__restrict__ ent) {
+              int2 *__restrict__ chunk_rng, int2 *__restrict__ ent) {
   const long long cr = hist_chunk_rows(batch_rows, n_slots, n_fg, target_items, kmax);
   int carry_rows = 0, carry_chunks = 0;
   for (int base = 0; base < n_slots; base += blockDim.x) {
@@ -2485,7 +2487,8 @@ k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *_
       pr.chunk_rows = nch > 0 ? (cnt + nch - 1) / nch : (int)cr;  // equal chunks
       pr.compact = 0;
       pairs[sl] = pr;
-      for (int c = 0; c < nch; ++c) chunk_pair[carry_chunks + ec + c] = sl;
+      for (int c = 0; c < nch; ++c)
+        chunk_rng[carry_chunks + ec + c] = make_int2(pr.begin + c * pr.chunk_rows, min(pr.begin + cnt, pr.begin + (c + 1) * pr.chunk_rows));
       ent[sl] = make_int2(sl, 0);  // streamed evaluation: every slot in the general list
     }
     carry_rows += tr;
@@ -2577,7 +2580,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
   const int target = w->hist_grid;
   k_init_build<<<c->num_sms * 4, 256, 0, c->stream>>>(w->dnodes, n_nodes, d->d_ss, w->d_rp, lambda, mcw, eta,
                                                        w->segs[0], w->pairs, w->ctl, 0, n_fg, target, kmax, D,
-                                                       d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], 0, w->chunk_pair, w->ent,
+                                                       d->d_sel_rows, w->ridx[0], d->d_q, w->q[0], 0, w->chunk_rng, w->ent,
                                                        w->ent_cap, nullptr, 0, nullptr);
   k_stream_init<<<c->num_sms * 4, 256, 0, c->stream>>>(sw.row_node, n);
   OOCGB_CK(cudaGetLastError());
@@ -2594,12 +2597,12 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
       OOCGB_CK(cudaGetLastError());
       if (!hist) return;
       k_stream_plan<<<1, 1024, 0, c->stream>>>(n_slots, first, sw.slot_cnt, sw.slot_cur, w->pairs, w->ctl, n_fg,
-                                               target, kmax, nr, w->chunk_pair, w->ent);
+                                               target, kmax, nr, w->chunk_rng, w->ent);
       k_stream_scatter<<<grid, 256, 0, c->stream>>>(r0, nr, sw.b_slot, sw.slot_cur, d->d_q, sw.b_ridx, sw.b_q);
       {
         PhaseTimer t(c, 0);
         k_hist<<<w->hist_grid, kHistThreads, kHistSmem, c->stream>>>(batch, 32, m, n_fg, sw.b_ridx, sw.b_q, w->pairs,
-                                                                     w->ctl, w->chunk_pair, w->partial, 0, d->stride, 0);
+                                                                     w->ctl, w->chunk_rng, w->partial, 0, d->stride, 0);
       }
       const int64_t tot = (int64_t)n_slots * m * kBins;
       k_accum_partials<<<(int)std::min<int64_t>((tot + 255) / 256, c->num_sms * 16), 256, 0, c->stream>>>(
@@ -2609,7 +2612,7 @@ oocgb_tree build_tree_streamed(oocgb_data d, int D, double lambda, double gamma,
     if (!hist) break;
     // every node of the level: pairs[s] = {built = first + s} over the whole data
     k_stream_plan<<<1, 1024, 0, c->stream>>>(n_slots, first, sw.slot_cnt, sw.slot_cur, w->pairs, w->ctl, n_fg,
-                                             target, kmax, 0, w->chunk_pair, w->ent);
+                                             target, kmax, 0, w->chunk_rng, w->ent);
     PhaseTimer t(c, 1);
     EvalArgs A;
     A.d = lv; A.D = D; A.m = m; A.n_fg = n_fg;

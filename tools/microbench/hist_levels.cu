@@ -59,9 +59,9 @@ int main(int argc, char **argv) {
     for (auto &x : h) x = (uint8_t)g();
     cudaMemcpy(bins, h.data(), h.size(), cudaMemcpyHostToDevice);
   }
-  int32_t *ridx; int2 *q; Pair *pairs; LevelCtl *ctl; int *chunk_pair, *partial;
+  int32_t *ridx; int2 *q; Pair *pairs; LevelCtl *ctl; int2 *chunk_rng; int *partial;
   cudaMalloc(&ridx, 4 * N); cudaMalloc(&q, 8 * N); cudaMalloc(&pairs, sizeof(Pair) * 1024);
-  cudaMalloc(&ctl, sizeof(LevelCtl)); cudaMalloc(&chunk_pair, 4 * 65536);
+  cudaMalloc(&ctl, sizeof(LevelCtl)); cudaMalloc(&chunk_rng, 8 * 65536);
   cudaMalloc(&partial, (size_t)65536 * 2 * kFG * kBins * 4 / 4);  // 64k items x 16 KB... sized below
   cudaFree(partial);
   cudaMalloc(&partial, (size_t)8192 * kFG * kBins * 2 * 4);  // up to 8192 items
@@ -138,14 +138,20 @@ int main(int argc, char **argv) {
     hc.n_pairs = (int)hp.size();
     cudaMemcpy(ridx, hr.data(), 4 * hr.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(pairs, hp.data(), sizeof(Pair) * hp.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(chunk_pair, cp.data(), 4 * cp.size(), cudaMemcpyHostToDevice);
+    std::vector<int2> rg;  // chunk -> position range (what the plan writes)
+    for (size_t k = 0; k < cp.size(); ++k) {
+      const Pair &P = hp[cp[k]];
+      const int b0 = P.begin + ((int)k - P.chunk_base) * P.chunk_rows;
+      rg.push_back(make_int2(b0, std::min(P.begin + P.count, b0 + P.chunk_rows)));
+    }
+    cudaMemcpy(chunk_rng, rg.data(), 8 * rg.size(), cudaMemcpyHostToDevice);
     float best = 1e30f;
     for (int it = 0; it < 20; ++it) {
       cudaMemcpy(ctl, &hc, sizeof(hc), cudaMemcpyHostToDevice);
       // flush L2 between launches (the real level reads cold data)
       cudaMemset(partial, it, (size_t)8192 * kFG * kBins * 2 * 4 / 2);
       cudaEventRecord(e0);
-      k_hist<<<grid, kHistThreads, kHistSmem>>>(bins, pitch, m, n_fg, ridx, q, pairs, ctl, chunk_pair,
+      k_hist<<<grid, kHistThreads, kHistSmem>>>(bins, pitch, m, n_fg, ridx, q, pairs, ctl, chunk_rng,
                                                partial, L.identity ? 1 : 0, MB_GW, MB_GW == 64 ? 1 : 0);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
