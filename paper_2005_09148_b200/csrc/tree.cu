@@ -97,7 +97,7 @@ struct Work {
   long long *rs_send = nullptr;  // world > 1: reduce-scatter send buffer [rank][pair][msl][256][2]
   int msl = 0, max_slots = 0;    // features per rank slice; candidate slots per level
   oocgb::Cand *cand = nullptr;
-  int2 *ent = nullptr;  // eval work lists [2][ent_cap]
+  int4 *ent = nullptr;  // eval work lists [2][ent_cap] of (pair, side, node, 0)
   int ent_cap = 0;
   oocgb::DNode *dnodes = nullptr;
   oocgb::LevelCtl *ctl = nullptr;
@@ -148,7 +148,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
                              double lambda, double mcw, double eta, Seg *segs,
                              Pair *pairs, LevelCtl *ctl, int n_sel_arg, int n_fg, int target_items,
                              int kmax, int max_depth, const int32_t *sel_rows, int32_t *ridx,
-                             const int2 *q_in, int2 *q_out, int ridx_mode, int2 *chunk_rng, int2 *ent,
+                             const int2 *q_in, int2 *q_out, int ridx_mode, int2 *chunk_rng, int4 *ent,
                              int ent_cap, int *tile_seg, int n_tiles, int *seg_cur0) {
   int tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nth = gridDim.x * blockDim.x;
@@ -214,7 +214,7 @@ __global__ void k_init_build(DNode *dn, int n_nodes, const SampleState *__restri
     ctl->n_segs = 1;
     ctl->n_splits = 0;
     const bool narrow = P.n_rows_global <= kmax;  // eval work list of the root (pair 0, side 0)
-    ent[narrow ? ent_cap : 0] = make_int2(0, 0);
+    ent[narrow ? ent_cap : 0] = make_int4(0, 0, 0, 0);
     ctl->n_ew = (max_depth > 0 && !narrow) ? 1 : 0;
     ctl->n_en = (max_depth > 0 && narrow) ? 1 : 0;
   }
@@ -586,7 +586,7 @@ struct EvalArgs {
   int streamed;    // Alg. 6 mode: every node built directly, no parent histograms kept
   const float *cut_values;
   double eta;
-  const int2 *ent;  // per-level work lists of (pair, side): general [0, n_ew), narrow [ent_cap, + n_en)
+  const int4 *ent;  // per-level work lists of (pair, side, node, 0): general [0, n_ew), narrow [ent_cap, + n_en)
   int ent_cap;
   int has_missing;  // R27: bin 255 holds missing values; candidates in both default directions
   // feature slice (world > 1: this rank evaluates features [f0, f0 + mf) from reduce-scattered
@@ -802,10 +802,9 @@ __device__ __forceinline__ void store_hist8(long long *dst, const long long (&g)
 constexpr int kEvalWarps = 4;  // 4-warp blocks: measured best of 1, 2, 4, 8
 constexpr int kEvalBlocksWide = 4, kEvalBlocksNarrow = 6;  // resident blocks per SM (registers)
 template <bool HAS_MISSING>
-__device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int side, int j, int lane,
+__device__ __forceinline__ void eval_item_wide(const EvalArgs &A, int p, int side, int node, int j, int lane,
                                                longlong2 *tl) {
-  const Pair P = A.pairs[p];
-  const int node = side ? P.derived : P.built;
+  const Pair P = A.pairs[p];  // (the node comes with the entry: its record loads alongside)
   if (node < 0) return;
   if (A.streamed && A.dn[node].feature == -2) return;  // streamed levels list every slot
   const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;  // prefetched for eval_node
@@ -922,8 +921,8 @@ __global__ void __launch_bounds__(kEvalWarps * 32, kEvalBlocksWide) k_eval(EvalA
   int e = t / A.mf, jj = t - e * A.mf;  // item t = (entry e, feature f0 + jj), advanced by nw
   const int de = nw / A.mf, dj = nw - de * A.mf;
   for (; t < n_items; t += nw) {
-    const int2 en = A.ent[e];
-    eval_item_wide<HAS_MISSING>(A, en.x, en.y, A.f0 + jj, lane, tile[wib]);
+    const int4 en = A.ent[e];
+    eval_item_wide<HAS_MISSING>(A, en.x, en.y, en.z, A.f0 + jj, lane, tile[wib]);
     e += de;
     jj += dj;
     if (jj >= A.mf) { jj -= A.mf; ++e; }
@@ -938,9 +937,9 @@ __global__ void __launch_bounds__(kEvalWarps * 32, kEvalBlocksWide) k_eval(EvalA
 #define OOCGB_EVAL_NARROW_MINB 6  // 80 registers, no spills (= kEvalBlocksNarrow)
 #endif
 template <bool HAS_MISSING>
-__device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int side, int j, int lane, int2 *tl) {
-  const Pair P = A.pairs[p];
-  const int node = side ? P.derived : P.built;
+__device__ __forceinline__ void eval_item_narrow(const EvalArgs &A, int p, int side, int node, int j, int lane,
+                                                 int2 *tl) {
+  const Pair P = A.pairs[p];  // (the node comes with the entry: its record loads alongside)
   if (node < 0) return;
   if (A.streamed && A.dn[node].feature == -2) return;
   const long long nodeG = A.dn[node].Gq, nodeH = A.dn[node].Hq;
@@ -1050,8 +1049,8 @@ __global__ void __launch_bounds__(kEvalWarps * 32, OOCGB_EVAL_NARROW_MINB) k_eva
   int e = t / A.mf, jj = t - e * A.mf;  // item t = (entry e, feature f0 + jj), advanced by nw
   const int de = nw / A.mf, dj = nw - de * A.mf;
   for (; t < n_items; t += nw) {
-    const int2 en = A.ent[A.ent_cap + e];
-    eval_item_narrow<HAS_MISSING>(A, en.x, en.y, A.f0 + jj, lane, tile2[wib]);
+    const int4 en = A.ent[A.ent_cap + e];
+    eval_item_narrow<HAS_MISSING>(A, en.x, en.y, en.z, A.f0 + jj, lane, tile2[wib]);
     e += de;
     jj += dj;
     if (jj >= A.mf) { jj -= A.mf; ++e; }
@@ -1094,10 +1093,9 @@ __device__ __forceinline__ long long warp_incl_scan_ll(long long v, int lane) {
 }
 
 template <bool HAS_MISSING>
-__device__ __forceinline__ void eval_item_blk(const EvalArgs &A, int p, int side, int j, BlkShared &S) {
+__device__ __forceinline__ void eval_item_blk(const EvalArgs &A, int p, int side, int node, int j, BlkShared &S) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const Pair P = A.pairs[p];
-  const int node = side ? P.derived : P.built;
+  const Pair P = A.pairs[p];  // (the node comes with the entry)
   if (node < 0) return;                                // uniform over the block
   if (A.streamed && A.dn[node].feature == -2) return;  // streamed levels list every slot
   const long long G = A.dn[node].Gq, H = A.dn[node].Hq;
@@ -1276,8 +1274,8 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkPerSm) k_eval_blk(EvalArgs A)
   int e = t / A.mf, jj = t - e * A.mf;
   const int de = (int)gridDim.x / A.mf, dj = (int)gridDim.x - de * A.mf;
   for (; t < n_items; t += gridDim.x) {
-    const int2 en = A.ent[e];
-    eval_item_blk<HAS_MISSING>(A, en.x, en.y, A.f0 + jj, S);
+    const int4 en = A.ent[e];
+    eval_item_blk<HAS_MISSING>(A, en.x, en.y, en.z, A.f0 + jj, S);
     e += de;
     jj += dj;
     if (jj >= A.mf) { jj -= A.mf; ++e; }
@@ -1527,7 +1525,7 @@ struct PlanArgs {
   int2 *chunk_rng;  // histogram chunk -> its position range (k_hist's item lookup)
   const long long *n_dev;  // the sample's rows (device sample state)
   int n_fg, target_items, kmax;
-  int2 *ent;        // eval work lists (EvalArgs::ent)
+  int4 *ent;        // eval work lists (EvalArgs::ent)
   int ent_cap;
   int last;         // the tree's last level: only segments, children counts and the tile table
 };
@@ -1814,8 +1812,9 @@ __device__ void plan_level_loop(const PlanArgs &A) {
       const int en = block_excl_scan(nn, &tn);
       if (p < n_pairs) {
         int iw = ew_carry + ew, in = en_carry + en;
-        if (rb <= kmax) A.ent[A.ent_cap + in++] = make_int2(p, 0); else A.ent[iw++] = make_int2(p, 0);
-        if (rd <= kmax) A.ent[A.ent_cap + in] = make_int2(p, 1); else A.ent[iw] = make_int2(p, 1);
+        const int4 eb = make_int4(p, 0, pairs[p].built, 0), ed = make_int4(p, 1, pairs[p].derived, 0);
+        if (rb <= kmax) A.ent[A.ent_cap + in++] = eb; else A.ent[iw++] = eb;
+        if (rd <= kmax) A.ent[A.ent_cap + in] = ed; else A.ent[iw] = ed;
       }
       ew_carry += tw;
       en_carry += tn;
@@ -1941,8 +1940,9 @@ __device__ void plan_level(const PlanArgs &A, int n_segs) {
     tn = twn >> 16;
     if (split) {
       int iw = ew, in = en;
-      if (gb <= A.kmax) A.ent[A.ent_cap + in++] = make_int2(np, 0); else A.ent[iw++] = make_int2(np, 0);
-      if (gd <= A.kmax) A.ent[A.ent_cap + in] = make_int2(np, 1); else A.ent[iw] = make_int2(np, 1);
+      const int4 eb = make_int4(np, 0, pr.built, 0), ed = make_int4(np, 1, pr.derived, 0);
+      if (gb <= A.kmax) A.ent[A.ent_cap + in++] = eb; else A.ent[iw++] = eb;
+      if (gd <= A.kmax) A.ent[A.ent_cap + in] = ed; else A.ent[iw] = ed;
     }
     if (threadIdx.x == 0) { A.ctl->n_ew = tw; A.ctl->n_en = tn; }
   }
@@ -2125,7 +2125,7 @@ static void ensure_work(oocgb_data d, int D) {
   if (c->coll) w->rs_send = (long long *)dmalloc(sizeof(long long) * hsl * (size_t)W * max_pairs);
   w->cand = (Cand *)dmalloc(sizeof(Cand) * (size_t)W * w->max_slots * w->msl);
   w->ent_cap = (int)(2 * max_pairs);
-  w->ent = (int2 *)dmalloc(sizeof(int2) * 2 * w->ent_cap);
+  w->ent = (int4 *)dmalloc(sizeof(int4) * 2 * w->ent_cap);
   w->dnodes = (DNode *)dmalloc(sizeof(DNode) * ((1LL << (D + 1)) - 1));
   w->ctl = (LevelCtl *)dmalloc(sizeof(LevelCtl));
   w->d_rp = (RoundParams *)dmalloc(sizeof(RoundParams));
@@ -2468,7 +2468,7 @@ __global__ void k_stream_assign(const uint8_t *__restrict__ batch, int stride, i
 __global__ void __launch_bounds__(1024)
 k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *__restrict__ slot_cur,
               Pair *__restrict__ pairs, LevelCtl *ctl, int n_fg, int target_items, int kmax, int64_t batch_rows,
-              int2 *__restrict__ chunk_rng, int2 *__restrict__ ent) {
+              int2 *__restrict__ chunk_rng, int4 *__restrict__ ent) {
   const long long cr = hist_chunk_rows(batch_rows, n_slots, n_fg, target_items, kmax);
   int carry_rows = 0, carry_chunks = 0;
   for (int base = 0; base < n_slots; base += blockDim.x) {
@@ -2489,7 +2489,7 @@ k_stream_plan(int n_slots, int first_d, const int *__restrict__ slot_cnt, int *_
       pairs[sl] = pr;
       for (int c = 0; c < nch; ++c)
         chunk_rng[carry_chunks + ec + c] = make_int2(pr.begin + c * pr.chunk_rows, min(pr.begin + cnt, pr.begin + (c + 1) * pr.chunk_rows));
-      ent[sl] = make_int2(sl, 0);  // streamed evaluation: every slot in the general list
+      ent[sl] = make_int4(sl, 0, first_d + sl, 0);  // streamed evaluation: every slot in the general list
     }
     carry_rows += tr;
     carry_chunks += tc;
