@@ -1309,16 +1309,13 @@ k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs,
            const Cand *__restrict__ cand, DNode *dn, const float *__restrict__ cut_values,
            const int *__restrict__ cut_ptrs, const RoundParams *__restrict__ rp, double lambda, double eta,
            Seg *segs) {
-  const int p = blockIdx.x >> 1;
-  // the pair record is read together with the pair count (no dependent round trip; a slot past
-  // the count holds a stale record that is then ignored)
-  const int n_pairs = ctl->n_pairs;
-  const Pair P = pairs[p];
-  if (p >= n_pairs) return;
-  const int node = (blockIdx.x & 1) ? P.derived : P.built;
-  if (node < 0) return;
-  if (!segs && dn[node].feature != -1) return;  // absent slot (streamed mode lists every slot)
-  const int slot = node - level_first(d);
+  // block b decides slot b of the level: the node index needs no pair record, so the candidate
+  // loads start at once; a slot whose node is not an unsplit node of this level (feature -2:
+  // absent) is dropped after them
+  (void)pairs;
+  const int slot = blockIdx.x;
+  const int node = level_first(d) + slot;
+  const int feat0 = dn[node].feature;
   BestSplit best{0.0, 0, 0x7fffffff, 0, 0, 0};
   // candidate (slot, j) at cand_index(msl, max_slots, slot, j), the owner block r = j / msl
   // carried along instead of divided per candidate
@@ -1339,6 +1336,7 @@ k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs,
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0) s_best[w] = best;
   __syncthreads();
+  if (feat0 != -1) return;  // absent slot (uniform over the block)
   if (threadIdx.x == 0) {
     for (int u = 1; u < (int)(blockDim.x >> 5); ++u)
       if (better(s_best[u], best)) best = s_best[u];
