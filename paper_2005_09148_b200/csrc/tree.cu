@@ -1289,6 +1289,7 @@ struct BestSplit {
   double gain;
   int have, j, bin;
   long long GL, HL;
+  int cp;  // k_finalize: cut_ptrs[j] (loaded with the candidate)
 };
 __device__ __forceinline__ bool better(const BestSplit &a, const BestSplit &b) {  // a beats b
   return a.have && (!b.have || a.gain > b.gain || (a.gain == b.gain && a.j < b.j));
@@ -1301,6 +1302,7 @@ __device__ __forceinline__ BestSplit shfl_best(const BestSplit &x, int o) {
   y.bin = __shfl_down_sync(0xffffffffu, x.bin, o);
   y.GL = __shfl_down_sync(0xffffffffu, x.GL, o);
   y.HL = __shfl_down_sync(0xffffffffu, x.HL, o);
+  y.cp = __shfl_down_sync(0xffffffffu, x.cp, o);
   return y;
 }
 
@@ -1316,13 +1318,14 @@ k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs,
   const int slot = blockIdx.x;
   const int node = level_first(d) + slot;
   const int feat0 = dn[node].feature;
-  BestSplit best{0.0, 0, 0x7fffffff, 0, 0, 0};
+  const long long Gq0 = dn[node].Gq, Hq0 = dn[node].Hq, seg0 = dn[node].seg;  // early: used at the end
+  BestSplit best{0.0, 0, 0x7fffffff, 0, 0, 0, 0};
   // candidate (slot, j) at cand_index(msl, max_slots, slot, j), the owner block r = j / msl
   // carried along instead of divided per candidate
   int r = (int)threadIdx.x / msl, jr = (int)threadIdx.x - r * msl;
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
     const Cand cd = cand[((size_t)r * max_slots + slot) * msl + jr];
-    BestSplit x{cd.gain, cd.valid, j, cd.bin, cd.GL, cd.HL};
+    BestSplit x{cd.gain, cd.valid, j, cd.bin, cd.GL, cd.HL, __ldg(cut_ptrs + j)};
     if (better(x, best)) best = x;
     jr += blockDim.x;
     while (jr >= msl) { jr -= msl; ++r; }
@@ -1345,14 +1348,14 @@ k_finalize(int d, int m, int msl, int max_slots, const Pair *__restrict__ pairs,
       nd.feature = best.j;
       nd.split_bin = best.bin >> 1;      // candidate key 2 b + dir (R27)
       nd.default_left = best.bin & 1;
-      nd.split_value = cut_values[cut_ptrs[best.j] + (best.bin >> 1)];
+      nd.split_value = cut_values[best.cp + (best.bin >> 1)];
       nd.gain = best.gain;
-      if (segs) segs[nd.seg].dec = seg_dec(best.j, best.bin & 1, best.bin >> 1);  // for the partition
+      if (segs) segs[seg0].dec = seg_dec(best.j, best.bin & 1, best.bin >> 1);  // for the partition
       DNode L{}, R{};
       L.feature = -1;
       R.feature = -1;
       node_fill(L, best.GL, best.HL, rp->sg_inv, rp->sh_inv, lambda, eta, &ctl->error);
-      node_fill(R, nd.Gq - best.GL, nd.Hq - best.HL, rp->sg_inv, rp->sh_inv, lambda, eta, &ctl->error);
+      node_fill(R, Gq0 - best.GL, Hq0 - best.HL, rp->sg_inv, rp->sh_inv, lambda, eta, &ctl->error);
       dn[2 * node + 1] = L;
       dn[2 * node + 2] = R;
       atomicAdd(&ctl->n_splits, 1);
